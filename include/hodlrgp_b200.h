@@ -1,0 +1,178 @@
+/*
+ * hodlrgp_b200 — C ABI of the B200-native HODLR maximum-likelihood hot path.
+ *
+ * Drop-in boundary for the reference C++ API in /root/reference/proj/include/
+ * hodlrgp (arXiv 2303.10102). Each entry point names the reference interface
+ * it replaces (file:line). Plain pointers and sizes only; matrices are
+ * column-major doubles. `loc` selects where X/Y live: HG_HOST (copied in/out
+ * inside the call) or HG_DEVICE (device pointers on the context's device).
+ *
+ * Every call returns an hg_status; hg_last_error() gives the message of the
+ * last failure on the calling thread. The C++ layer (include/hodlrgp_b200.hpp)
+ * maps the codes back to the reference exception types.
+ */
+#ifndef HODLRGP_B200_H
+#define HODLRGP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HG_OK = 0,
+    HG_NOT_SPD = 1,   /* NotPositiveDefinite  (factorization.hpp:14-16) */
+    HG_EINVAL = 2,    /* std::invalid_argument (dimension/tree/orientation) */
+    HG_ELENGTH = 3,   /* std::length_error    (size guards) */
+    HG_ELOGIC = 4,    /* std::logic_error     (lower() on symmetric storage) */
+    HG_ENOMEM = 5,
+    HG_ECUDA = 6,
+    HG_EOTHER = 9
+} hg_status;
+
+enum { HG_HOST = 0, HG_DEVICE = 1 };
+enum { HG_RIGHT = 0, HG_LEFT = 1 }; /* Orientation (factorization.hpp:18-21) */
+
+typedef struct hg_ctx_s* hg_ctx_t;
+typedef struct hg_hodlr_s* hg_hodlr_t;
+typedef struct hg_factor_s* hg_factor_t;
+typedef struct hg_prodrep_s* hg_prodrep_t;
+typedef struct hg_oracle_s* hg_oracle_t;
+typedef struct hg_build_s* hg_build_t;
+
+/* ---------------------------------------------------------------- context */
+const char* hg_last_error(void);
+/* One device + one CUDA stream (stream may be NULL: the context creates one). */
+hg_status hg_ctx_create(int device, void* stream, hg_ctx_t* out);
+hg_status hg_ctx_destroy(hg_ctx_t ctx);
+hg_status hg_ctx_synchronize(hg_ctx_t ctx);
+/* Number of kernels this context has launched so far. */
+uint64_t hg_ctx_launches(hg_ctx_t ctx);
+void* hg_ctx_stream(hg_ctx_t ctx);
+
+/* ----------------------------------------------------- cluster tree (host) */
+/* tree_depth — cluster_tree.cpp:34-38 */
+int hg_tree_depth(int64_t n, int64_t leaf_min, int64_t leaf_max);
+/* ClusterTree(n, tau).level(d) for d = 0..tau, depth-major (lo,hi) pairs —
+ * cluster_tree.cpp:10-22. lo_hi holds 2 * (2^(tau+1) - 1) entries. */
+hg_status hg_tree_ranges(int64_t n, int tau, int64_t* lo_hi);
+/* build_kd_ordering — cluster_tree.cpp:40-90; coords n x d col-major. */
+hg_status hg_kd_ordering(int64_t n, int d, const double* coords, int64_t leaf_min, int64_t leaf_max,
+                         int64_t* perm, int64_t* inv, int* tau);
+
+/* ------------------------------------------------------------ HodlrMatrix */
+/* HodlrMatrix::zero / identity / random_spd / random_symmetric —
+ * hodlr_matrix.cpp:68-88,126-172 */
+hg_status hg_hodlr_zero(hg_ctx_t ctx, int64_t n, int tau, int symmetric, hg_hodlr_t* out);
+hg_status hg_hodlr_identity(hg_ctx_t ctx, int64_t n, int tau, hg_hodlr_t* out);
+hg_status hg_hodlr_random(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_t seed, int spd, hg_hodlr_t* out);
+/* Panel exchange format: for l = 1..tau, U_l then V_l (n x R[l-1] each,
+ * col-major; U rows of left children = upper.left, of right children =
+ * lower.left; V rows of right children = upper.right, of left children =
+ * lower.right), then leaves m_b x m_b concatenated. ranks_* hold 2^tau - 1
+ * entries (level-major, node order). Host pointers. */
+hg_status hg_hodlr_import(hg_ctx_t ctx, int64_t n, int tau, int symmetric, const int* R, const double* flat,
+                          const int* ranks_up, const int* ranks_lo, hg_hodlr_t* out);
+hg_status hg_hodlr_info(hg_hodlr_t h, int64_t* n, int* tau, int* symmetric, int* R);
+int64_t hg_hodlr_export_size(hg_hodlr_t h);
+hg_status hg_hodlr_export(hg_ctx_t ctx, hg_hodlr_t h, double* flat, int* ranks_up, int* ranks_lo);
+hg_status hg_hodlr_copy(hg_ctx_t ctx, hg_hodlr_t h, hg_hodlr_t* out);
+hg_status hg_hodlr_free(hg_hodlr_t h);
+/* make_asymmetric — hodlr_matrix.cpp:187-196 */
+hg_status hg_hodlr_make_asymmetric(hg_ctx_t ctx, hg_hodlr_t h);
+/* Y = H X, X/Y n x s (ldx/ldy >= n) — HodlrMatrix::matvec, hodlr_matrix.cpp:198-226 */
+hg_status hg_hodlr_matvec(hg_ctx_t ctx, hg_hodlr_t h, const double* X, int64_t ldx, int64_t s, double* Y,
+                          int64_t ldy, int loc);
+/* Y = H_sub X (or H_sub^T X) for the depth-d node `node` — sub_matvec,
+ * hodlr_matrix.cpp:228-265. X/Y have the node's row count. */
+hg_status hg_hodlr_sub_matvec(hg_ctx_t ctx, hg_hodlr_t h, int d, int64_t node, const double* X, int64_t ldx,
+                              int64_t s, int transpose, double* Y, int64_t ldy, int loc);
+/* trace — hodlr_matrix.cpp:267-271; trace_product — :294-318 */
+hg_status hg_hodlr_trace(hg_ctx_t ctx, hg_hodlr_t h, double* out);
+hg_status hg_trace_product(hg_ctx_t ctx, hg_hodlr_t a, hg_hodlr_t b, double* out);
+
+/* ---------------------------------------------------------- factorization */
+/* factorize — factorization.cpp:62-168 */
+hg_status hg_factorize(hg_ctx_t ctx, hg_hodlr_t h, int orientation, hg_factor_t* out);
+hg_status hg_factor_free(hg_factor_t f);
+/* HodlrFactorization::solve — factorization.cpp:170-212 (in-place allowed on HG_DEVICE) */
+hg_status hg_factor_solve(hg_ctx_t ctx, hg_factor_t f, const double* B, int64_t ldb, int64_t s, double* X,
+                          int64_t ldx, int loc);
+/* HodlrFactorization::logdet — factorization.cpp:214-224 (HG_NOT_SPD on a
+ * non-positive capacitance or leaf determinant) */
+hg_status hg_factor_logdet(hg_ctx_t ctx, hg_factor_t f, double* out);
+/* Leaf decisions: 1 = LLT used, 0 = LU fallback (factorization.cpp:7-18). */
+hg_status hg_factor_leaf_llt(hg_ctx_t ctx, hg_factor_t f, int* out);
+
+/* ---------------------------------------------------------- trace algebra */
+/* multiply / solve_multiply — product_rep.cpp:180-186 (pipeline :47-155) */
+hg_status hg_multiply(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, hg_prodrep_t* out);
+hg_status hg_solve_multiply(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, hg_prodrep_t* out);
+hg_status hg_prodrep_free(hg_prodrep_t p);
+/* ProductRep::densify — product_rep.cpp:9-22 (n <= 2^14; host output n x n) */
+hg_status hg_prodrep_densify(hg_ctx_t ctx, hg_prodrep_t p, double* out);
+/* trace_product_rep :188-194, trace_pair :204-235, trace_solve :196-202,
+ * trace_quad :237-245 */
+hg_status hg_trace_product_rep(hg_ctx_t ctx, hg_prodrep_t p, double* out);
+hg_status hg_trace_pair(hg_ctx_t ctx, hg_prodrep_t p, hg_prodrep_t q, double* out);
+hg_status hg_trace_solve(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, double* out);
+hg_status hg_trace_quad(hg_ctx_t ctx, hg_factor_t fa, hg_hodlr_t b, hg_factor_t fc, hg_hodlr_t d, double* out);
+
+/* ------------------------------------------------------ covariance oracle */
+/* CovarianceOracle (oracle.hpp:15-52) implemented on the device.
+ * hg_oracle_dense: DenseMatrixOracle (oracle.hpp:115-143), K and p derivative
+ *   matrices n x n, host pointers (copied to the device).
+ * hg_oracle_matern: 1D Matérn nu = nu2/2 on sorted points, theta = (sigma2,
+ *   ell) plus a fixed nugget; scan = 1 uses the O(n) exponential-polynomial
+ *   recurrence, 0 the dense on-the-fly kernel.
+ * hg_oracle_callback: user forward model; fn(user, j, V, ldv, s, Y, ldy,
+ *   stream) writes Y = K V (j = -1) or dK/dtheta_j V with device pointers. */
+typedef int (*hg_apply_fn)(void* user, int j, const double* V, int64_t ldv, int64_t s, double* Y, int64_t ldy,
+                           void* stream);
+hg_status hg_oracle_dense(hg_ctx_t ctx, int64_t n, const double* K, int p, const double* dK, hg_oracle_t* out);
+hg_status hg_oracle_matern(hg_ctx_t ctx, int64_t n, const double* x, int nu2, double sigma2, double ell,
+                           double nugget, int scan, hg_oracle_t* out);
+hg_status hg_oracle_callback(hg_ctx_t ctx, int64_t n, int p, hg_apply_fn fn, void* user, hg_oracle_t* out);
+hg_status hg_oracle_set_parameters(hg_oracle_t o, const double* theta, int p);
+hg_status hg_oracle_free(hg_oracle_t o);
+/* apply (j = -1) / apply_derivative (j >= 0) — oracle.hpp:25-35 */
+hg_status hg_oracle_apply(hg_ctx_t ctx, hg_oracle_t o, int j, const double* V, int64_t ldv, int64_t s, double* Y,
+                          int64_t ldy, int loc);
+/* apply_columns / derivative_columns / reset_counters — oracle.hpp:37-42 */
+hg_status hg_oracle_counters(hg_oracle_t o, uint64_t* apply_columns, uint64_t* derivative_columns, int reset);
+
+/* ------------------------------------------------------------ sketch build */
+/* build_hodlr / build_hodlr_with_derivatives with SketchPlan(tree, k, seed)
+ * generated on the host by std::mt19937_64 + std::normal_distribution in the
+ * reference's fill order — sketch.cpp:10-31, 128-356. */
+hg_status hg_build(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, int with_derivatives,
+                   hg_build_t* out);
+hg_status hg_build_free(hg_build_t b);
+/* BuildResult::h / deriv[j] (returned handles are owned by the caller) */
+hg_status hg_build_h(hg_build_t b, hg_hodlr_t* out);
+hg_status hg_build_deriv(hg_build_t b, int j, hg_hodlr_t* out);
+int hg_build_num_warnings(hg_build_t b);
+/* Rank decisions per (level, node): numeric_rank, w2, rw[0..p) — logged for
+ * comparison with the CPU path (sketch.cpp:54-59, 214-221, 249-252). */
+int hg_build_decisions(hg_build_t b, int p, int64_t* out);
+
+/* -------------------------------------------------------------------- mle */
+/* log_likelihood / score / fisher_information — mle.cpp:25-54. y, ybar are
+ * host vectors of length n (ybar may be NULL). Fisher uses the p cached
+ * ProductReps (identical arithmetic to recomputing them per pair). */
+hg_status hg_log_likelihood(hg_ctx_t ctx, hg_factor_t f, const double* y, const double* ybar, double* out);
+hg_status hg_score(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, const double* y,
+                   const double* ybar, double* out);
+hg_status hg_fisher_information(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, double* out);
+/* One MLE iteration (acceptance.cpp:297-308): build with derivatives,
+ * factorize (Left), log-likelihood, score, Fisher. times[5] = build_deriv,
+ * factorize, loglik, score, fisher seconds (device events). */
+hg_status hg_mle_iteration(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
+                           double* loglik, double* score, double* fisher, double* times);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HODLRGP_B200_H */

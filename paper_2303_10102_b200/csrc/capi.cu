@@ -1,0 +1,294 @@
+// extern "C" boundary (include/hodlrgp_b200.h) over the device hot path.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <functional>
+#include <string>
+
+#include "../../include/hodlrgp_b200.h"
+#include "api.cuh"
+
+using namespace hg;
+
+struct hg_ctx_s {
+    Ctx c;
+};
+struct hg_hodlr_s {
+    DHodlr h;
+};
+struct hg_factor_s {
+    DFactor f;
+};
+struct hg_prodrep_s {
+    DProductRep p;
+};
+struct hg_oracle_s {
+    std::unique_ptr<DOracle> o;
+};
+struct hg_build_s {
+    DBuildResult r;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Scope {
+    Ctx* prev;
+    explicit Scope(hg_ctx_t ctx) : prev(&current()) {
+        if (ctx) {
+            cudaSetDevice(ctx->c.device);
+            set_current(&ctx->c);
+        }
+    }
+    ~Scope() { set_current(prev); }
+};
+
+template <class F>
+hg_status guard(hg_ctx_t ctx, F&& f) {
+    try {
+        Scope s(ctx);
+        f();
+        return HG_OK;
+    } catch (const NotPositiveDefinite& e) {
+        g_err = e.what();
+        return HG_NOT_SPD;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return HG_ECUDA;
+    } catch (const std::bad_alloc& e) {
+        g_err = e.what();
+        return HG_ENOMEM;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HG_EINVAL;
+    } catch (const std::length_error& e) {
+        g_err = e.what();
+        return HG_ELENGTH;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return HG_ELOGIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HG_EOTHER;
+    }
+}
+
+/// Stage a host or device n x s block on the device.
+struct Staged {
+    DVec buf;
+    const double* ptr;
+    i64 ld;
+    Staged(const double* p, i64 ldp, i64 rows, i64 s, int loc) {
+        if (loc == HG_DEVICE) {
+            ptr = p;
+            ld = ldp;
+            return;
+        }
+        buf.alloc(size_t(rows) * size_t(s));
+        if (rows * s)
+            HG_CUDA(cudaMemcpy2DAsync(buf.get(), size_t(rows) * sizeof(double), p, size_t(ldp) * sizeof(double),
+                                      size_t(rows) * sizeof(double), size_t(s), cudaMemcpyHostToDevice,
+                                      current().stream));
+        ptr = buf.get();
+        ld = rows;
+    }
+};
+
+struct Output {
+    DVec buf;
+    double* dptr;
+    i64 ld;
+    double* host;
+    i64 ldh, rows, s;
+    Output(double* p, i64 ldp, i64 r, i64 cols, int loc) : host(nullptr), ldh(ldp), rows(r), s(cols) {
+        if (loc == HG_DEVICE) {
+            dptr = p;
+            ld = ldp;
+            return;
+        }
+        buf.alloc(size_t(r) * size_t(cols));
+        dptr = buf.get();
+        ld = r;
+        host = p;
+    }
+    void finish() {
+        if (host && rows * s)
+            HG_CUDA(cudaMemcpy2DAsync(host, size_t(ldh) * sizeof(double), dptr, size_t(rows) * sizeof(double),
+                                      size_t(rows) * sizeof(double), size_t(s), cudaMemcpyDeviceToHost,
+                                      current().stream));
+        sync();
+    }
+};
+
+double scalar_result(const std::function<void(double*)>& f) {
+    DVec d(1);
+    f(d.get());
+    return read_scalar(d.get());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hg_last_error(void) { return g_err.c_str(); }
+
+hg_status hg_ctx_create(int device, void* stream, hg_ctx_t* out) {
+    auto* c = new hg_ctx_s;
+    hg_status st = guard(nullptr, [&] {
+        HG_CUDA(cudaSetDevice(device));
+        c->c.device = device;
+        if (stream) {
+            c->c.stream = static_cast<cudaStream_t>(stream);
+        } else {
+            HG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+            c->c.own_stream = true;
+        }
+        HG_CUDA(cudaDeviceGetAttribute(&c->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+        // Keep freed blocks in the stream-ordered pool (no trimming between calls).
+        cudaMemPool_t pool;
+        HG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        std::uint64_t thr = ~std::uint64_t(0);
+        HG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    });
+    if (st != HG_OK) {
+        delete c;
+        return st;
+    }
+    *out = c;
+    return HG_OK;
+}
+
+hg_status hg_ctx_destroy(hg_ctx_t ctx) {
+    return guard(ctx, [&] {
+        HG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+        set_current(nullptr);
+        delete ctx;
+    });
+}
+
+hg_status hg_ctx_synchronize(hg_ctx_t ctx) { return guard(ctx, [&] { sync(); }); }
+uint64_t hg_ctx_launches(hg_ctx_t ctx) { return ctx->c.launches; }
+void* hg_ctx_stream(hg_ctx_t ctx) { return ctx->c.stream; }
+
+// ------------------------------------------------------------------- tree
+int hg_tree_depth(int64_t n, int64_t leaf_min, int64_t leaf_max) { return tree_depth(n, leaf_min, leaf_max); }
+
+hg_status hg_tree_ranges(int64_t n, int tau, int64_t* lo_hi) {
+    return guard(nullptr, [&] {
+        ClusterTree t(n, tau);
+        size_t o = 0;
+        for (int d = 0; d <= tau; ++d)
+            for (const auto& r : t.level(d)) {
+                lo_hi[o++] = r.lo;
+                lo_hi[o++] = r.hi;
+            }
+    });
+}
+
+hg_status hg_kd_ordering(int64_t n, int d, const double* coords, int64_t leaf_min, int64_t leaf_max, int64_t* perm,
+                         int64_t* inv, int* tau) {
+    return guard(nullptr, [&] {
+        KdOrdering kd = build_kd_ordering(coords, n, d, leaf_min, leaf_max);
+        for (int64_t i = 0; i < n; ++i) {
+            perm[i] = kd.perm[size_t(i)];
+            inv[i] = kd.inv[size_t(i)];
+        }
+        *tau = kd.tree.depth();
+    });
+}
+
+// ------------------------------------------------------------------ hodlr
+hg_status hg_hodlr_zero(hg_ctx_t ctx, int64_t n, int tau, int symmetric, hg_hodlr_t* out) {
+    return guard(ctx, [&] { *out = new hg_hodlr_s{DHodlr::zero(get_tree(n, tau), symmetric != 0)}; });
+}
+
+hg_status hg_hodlr_identity(hg_ctx_t ctx, int64_t n, int tau, hg_hodlr_t* out) {
+    return guard(ctx, [&] { *out = new hg_hodlr_s{DHodlr::identity(get_tree(n, tau))}; });
+}
+
+hg_status hg_hodlr_random(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_t seed, int spd, hg_hodlr_t* out) {
+    return guard(ctx, [&] { *out = new hg_hodlr_s{DHodlr::random(get_tree(n, tau), k, seed, spd != 0)}; });
+}
+
+hg_status hg_hodlr_import(hg_ctx_t ctx, int64_t n, int tau, int symmetric, const int* R, const double* flat,
+                          const int* ranks_up, const int* ranks_lo, hg_hodlr_t* out) {
+    return guard(ctx, [&] {
+        *out = new hg_hodlr_s{DHodlr::import_panels(get_tree(n, tau), symmetric != 0, R, flat, ranks_up, ranks_lo)};
+    });
+}
+
+hg_status hg_hodlr_info(hg_hodlr_t h, int64_t* n, int* tau, int* symmetric, int* R) {
+    return guard(nullptr, [&] {
+        *n = h->h.n();
+        *tau = h->h.tau();
+        *symmetric = h->h.sym ? 1 : 0;
+        if (R)
+            for (int l = 1; l <= h->h.tau(); ++l) R[l - 1] = h->h.Rl(l);
+    });
+}
+
+int64_t hg_hodlr_export_size(hg_hodlr_t h) { return int64_t(h->h.export_size()); }
+
+hg_status hg_hodlr_export(hg_ctx_t ctx, hg_hodlr_t h, double* flat, int* ranks_up, int* ranks_lo) {
+    return guard(ctx, [&] { h->h.export_panels(flat, ranks_up, ranks_lo); });
+}
+
+hg_status hg_hodlr_copy(hg_ctx_t ctx, hg_hodlr_t h, hg_hodlr_t* out) {
+    return guard(ctx, [&] { *out = new hg_hodlr_s{hodlr_deep_copy(h->h)}; });
+}
+
+hg_status hg_hodlr_free(hg_hodlr_t h) {
+    delete h;
+    return HG_OK;
+}
+
+hg_status hg_hodlr_make_asymmetric(hg_ctx_t ctx, hg_hodlr_t h) {
+    return guard(ctx, [&] { h->h.make_asymmetric(); });
+}
+
+hg_status hg_hodlr_matvec(hg_ctx_t ctx, hg_hodlr_t h, const double* X, int64_t ldx, int64_t s, double* Y,
+                          int64_t ldy, int loc) {
+    return guard(ctx, [&] {
+        const i64 n = h->h.n();
+        if (ldx < n || ldy < n) throw std::invalid_argument("matvec: dimension mismatch");
+        Staged x(X, ldx, n, s, loc);
+        Output y(Y, ldy, n, s, loc);
+        hodlr_apply(h->h, x.ptr, x.ld, int(s), y.dptr, y.ld, 1, h->h.tau(), true, false, 0.0);
+        y.finish();
+    });
+}
+
+hg_status hg_hodlr_sub_matvec(hg_ctx_t ctx, hg_hodlr_t h, int d, int64_t node, const double* X, int64_t ldx,
+                              int64_t s, int transpose, double* Y, int64_t ldy, int loc) {
+    return guard(ctx, [&] {
+        const auto& tree = h->h.tree->host;
+        if (d < 0 || d > tree.depth() || node < 0 || node >= i64(tree.level(d).size()))
+            throw std::invalid_argument("sub_matvec: node out of range");
+        const Range r = tree.level(d)[size_t(node)];
+        const i64 n = h->h.n();
+        Staged x(X, ldx, r.size(), s, loc);
+        DVec full(size_t(n) * size_t(s)), yf(size_t(n) * size_t(s));
+        full.zero();
+        HG_CUDA(cudaMemcpy2DAsync(full.get() + r.lo, size_t(n) * sizeof(double), x.ptr, size_t(x.ld) * sizeof(double),
+                                  size_t(r.size()) * sizeof(double), size_t(s), cudaMemcpyDeviceToDevice,
+                                  current().stream));
+        hodlr_apply(h->h, full.get(), n, int(s), yf.get(), n, d + 1, h->h.tau(), true, transpose != 0, 0.0);
+        Output y(Y, ldy, r.size(), s, loc);
+        HG_CUDA(cudaMemcpy2DAsync(y.dptr, size_t(y.ld) * sizeof(double), yf.get() + r.lo, size_t(n) * sizeof(double),
+                                  size_t(r.size()) * sizeof(double), size_t(s), cudaMemcpyDeviceToDevice,
+                                  current().stream));
+        y.finish();
+    });
+}
+
+hg_status hg_hodlr_trace(hg_ctx_t ctx, hg_hodlr_t h, double* out) {
+    return guard(ctx, [&] { *out = scalar_result([&](double* d) { hodlr_trace(h->h, d, false); }); });
+}
+
+hg_status hg_trace_product(hg_ctx_t ctx, hg_hodlr_t a, hg_hodlr_t b, double* out) {
+    return guard(ctx, [&] { *out = scalar_result([&](double* d) { hodlr_trace_product(a->h, b->h, d, false); }); });
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// Common device-side infrastructure for the B200 HODLR hot path.
+//
+// One context = one device + one CUDA stream. All device memory comes from the
+// stream-ordered pool (cudaMallocAsync) so per-call temporaries are cheap;
+// every kernel of a context runs on its stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hg {
+
+using i64 = long long;
+
+// ---------------------------------------------------------------- errors
+/// factorization.hpp:14-16 — non-positive capacitance / leaf determinant.
+struct NotPositiveDefinite : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define HG_CUDA(x)                                                                              \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw ::hg::CudaError(std::string(#x) + " failed: " + cudaGetErrorString(e_) +     \
+                                  " at " __FILE__ ":" + std::to_string(__LINE__));              \
+    } while (0)
+#define HG_LAUNCH() HG_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const char* msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+
+// --------------------------------------------------------------- context
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    std::uint64_t launches = 0;  // kernels launched through this context
+};
+
+Ctx& current();           // thread's active context (set by the C ABI)
+void set_current(Ctx* c);
+
+inline void count_launch() { ++current().launches; }
+
+// ---------------------------------------------------------- device buffer
+/// Stream-ordered device allocation (RAII, deep-copyable).
+template <class T>
+class DBuf {
+public:
+    DBuf() = default;
+    explicit DBuf(size_t n) { alloc(n); }
+    ~DBuf() { release(); }
+    DBuf(const DBuf& o) { copy_from(o); }
+    DBuf& operator=(const DBuf& o) {
+        if (this != &o) {
+            release();
+            copy_from(o);
+        }
+        return *this;
+    }
+    DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(size_t n) {
+        release();
+        n_ = n;
+        if (n) HG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), current().stream));
+    }
+    void zero() {
+        if (n_) HG_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), current().stream));
+    }
+    void upload(const T* h, size_t n) {
+        if (n != n_) alloc(n);
+        if (n) HG_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, current().stream));
+    }
+    void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+    std::vector<T> download() const {
+        std::vector<T> v(n_);
+        if (n_) {
+            HG_CUDA(cudaMemcpyAsync(v.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost, current().stream));
+            HG_CUDA(cudaStreamSynchronize(current().stream));
+        }
+        return v;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+    void release() {
+        if (p_) cudaFreeAsync(p_, current().stream);
+        p_ = nullptr;
+        n_ = 0;
+    }
+
+private:
+    void copy_from(const DBuf& o) {
+        p_ = nullptr;
+        n_ = 0;
+        if (o.n_) {
+            alloc(o.n_);
+            HG_CUDA(cudaMemcpyAsync(p_, o.p_, n_ * sizeof(T), cudaMemcpyDeviceToDevice, current().stream));
+        }
+    }
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+using DVec = DBuf<double>;
+using DVecP = std::shared_ptr<DVec>;
+
+inline DVecP make_dvec(size_t n, bool zero = true) {
+    auto p = std::make_shared<DVec>(n);
+    if (zero) p->zero();
+    return p;
+}
+
+inline void sync() { HG_CUDA(cudaStreamSynchronize(current().stream)); }
+
+inline int cdiv(i64 a, i64 b) { return int((a + b - 1) / b); }
+
+}  // namespace hg

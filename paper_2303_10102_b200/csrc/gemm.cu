@@ -1,0 +1,481 @@
+// Segmented FP64 GEMM engine and deterministic reductions (see kernels.cuh).
+//
+// Tile engine: 64x64 output tile per 256-thread CTA, 4x4 register micro-tile
+// per thread (rows tm+16i, cols tn+16j so that shared-memory reads are
+// contiguous/broadcast), K staged 16 at a time through padded shared memory
+// with a one-step register prefetch. Split-K partials are reduced in a fixed
+// order so every result is bitwise reproducible run to run.
+#include "kernels.cuh"
+
+namespace hg {
+
+namespace {
+
+constexpr int TM = 64, TN = 64, KS = 16, NT = 256;
+constexpr int SEG_CHUNK = 512;  // rows per split-K work item
+constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
+
+__device__ __forceinline__ void mma16(const double (&As)[KS][TM + 1], const double (&Bs)[KS][TN + 1],
+                                      double (&acc)[4][4], int tm, int tn) {
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+}
+
+// ------------------------------------------------------------------ seg_tn
+struct SegTnArgs {
+    const double* A;
+    i64 lda;
+    int ca;
+    const double* B;
+    i64 ldb;
+    int cb;
+    const WorkItem* items;
+    int tiles_m;
+    double* out;
+    i64 ostride;
+    int ldo;
+    int direct;
+    double alpha, beta;
+};
+
+__global__ void __launch_bounds__(NT) k_seg_tn(SegTnArgs g) {
+    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    const WorkItem it = g.items[blockIdx.x];
+    const int m0 = (blockIdx.y % g.tiles_m) * TM, n0 = (blockIdx.y / g.tiles_m) * TN;
+    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    const int lk = tid & 15, lc = tid >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    double ra[4], rb[4];
+    auto load = [&](int kb) {
+        const int r = kb + lk;
+        const bool rv = r < it.rows;
+        const i64 row = i64(it.row0) + r;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = m0 + lc + 16 * q;
+            ra[q] = (rv && m < g.ca) ? g.A[row + i64(m) * g.lda] : 0.0;
+            const int n = n0 + lc + 16 * q;
+            rb[q] = (rv && n < g.cb) ? g.B[row + i64(n) * g.ldb] : 0.0;
+        }
+    };
+    load(0);
+    for (int kb = 0; kb < it.rows; kb += KS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            As[lk][lc + 16 * q] = ra[q];
+            Bs[lk][lc + 16 * q] = rb[q];
+        }
+        __syncthreads();
+        if (kb + KS < it.rows) load(kb + KS);
+        mma16(As, Bs, acc, tm, tn);
+        __syncthreads();
+    }
+    double* o = g.out + (g.direct ? i64(it.seg) : i64(blockIdx.x)) * g.ostride;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int n = n0 + tn + 16 * j;
+        if (n >= g.cb) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = m0 + tm + 16 * i;
+            if (m >= g.ca) continue;
+            double* p = o + m + i64(n) * g.ldo;
+            if (g.direct)
+                *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
+            else
+                *p = acc[i][j];
+        }
+    }
+}
+
+__global__ void k_seg_reduce(const double* ws, i64 wstride, int ca, int cb, const int* seg_first, double* T,
+                             i64 tstride, int ldt, double alpha, double beta) {
+    const int s = blockIdx.y;
+    const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= i64(ca) * cb) return;
+    double sum = 0.0;
+    for (int c = seg_first[s]; c < seg_first[s + 1]; ++c) sum += ws[i64(c) * wstride + e];
+    const int m = int(e % ca), n = int(e / ca);
+    double* t = T + i64(s) * tstride + m + i64(n) * ldt;
+    *t = alpha * sum + (beta != 0.0 ? beta * *t : 0.0);
+}
+
+// ------------------------------------------------------------------ seg_nn
+struct SegNnArgs {
+    const double* X;
+    i64 ldx;
+    int k;
+    const double* T;
+    i64 tstride;
+    int ldt;
+    TMap map;
+    double* Y;
+    i64 ldy;
+    int w;
+    const WorkItem* items;
+    double alpha, beta;
+};
+
+__global__ void __launch_bounds__(NT) k_seg_nn(SegNnArgs g) {
+    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    const WorkItem it = g.items[blockIdx.x];
+    const int n0 = blockIdx.y * TN;
+    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.tstride +
+                       ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int am = tid & 63, akq = tid >> 6;  // A loads: 64 rows x 4 k-phases
+    const int bk = tid & 15, bn = tid >> 4;   // B loads: 16 k x 16 cols
+    double ra[4], rb[4];
+    auto load = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kk = akq + 4 * q;
+            ra[q] = (am < it.rows && kb + kk < g.k) ? g.X[i64(it.row0 + am) + i64(kb + kk) * g.ldx] : 0.0;
+            const int n = n0 + bn + 16 * q;
+            rb[q] = (kb + bk < g.k && n < g.w) ? Tb[(kb + bk) + i64(n) * g.ldt] : 0.0;
+        }
+    };
+    load(0);
+    for (int kb = 0; kb < g.k; kb += KS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            As[akq + 4 * q][am] = ra[q];
+            Bs[bk][bn + 16 * q] = rb[q];
+        }
+        __syncthreads();
+        if (kb + KS < g.k) load(kb + KS);
+        mma16(As, Bs, acc, tm, tn);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int n = n0 + tn + 16 * j;
+        if (n >= g.w) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = tm + 16 * i;
+            if (m >= it.rows) continue;
+            double* p = g.Y + i64(it.row0 + m) + i64(n) * g.ldy;
+            *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- leaf_mm
+struct LeafMmArgs {
+    const int* bounds;
+    int rt;
+    const double* L;
+    i64 lstride;
+    int ldl;
+    const double* X;
+    i64 ldx;
+    double* Y;
+    i64 ldy;
+    int w;
+    double alpha, beta;
+};
+
+template <bool TRANS>
+__global__ void __launch_bounds__(NT) k_leaf_mm(LeafMmArgs g) {
+    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * TM;
+    if (r0 >= m) return;
+    const int n0 = blockIdx.y * TN;
+    const double* Lb = g.L + i64(b) * g.lstride;
+    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int bk = tid & 15, bn = tid >> 4;
+    double ra[4], rb[4];
+    auto load = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!TRANS) {
+                const int i = tid & 63, kk = (tid >> 6) + 4 * q;
+                ra[q] = (r0 + i < m && kb + kk < m) ? Lb[(r0 + i) + i64(kb + kk) * g.ldl] : 0.0;
+            } else {
+                const int kk = tid & 15, i = (tid >> 4) + 16 * q;
+                ra[q] = (r0 + i < m && kb + kk < m) ? Lb[(kb + kk) + i64(r0 + i) * g.ldl] : 0.0;
+            }
+            const int n = n0 + bn + 16 * q;
+            rb[q] = (kb + bk < m && n < g.w) ? g.X[i64(lo + kb + bk) + i64(n) * g.ldx] : 0.0;
+        }
+    };
+    load(0);
+    for (int kb = 0; kb < m; kb += KS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!TRANS)
+                As[(tid >> 6) + 4 * q][tid & 63] = ra[q];
+            else
+                As[tid & 15][(tid >> 4) + 16 * q] = ra[q];
+            Bs[bk][bn + 16 * q] = rb[q];
+        }
+        __syncthreads();
+        if (kb + KS < m) load(kb + KS);
+        mma16(As, Bs, acc, tm, tn);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int n = n0 + tn + 16 * j;
+        if (n >= g.w) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int mi = r0 + tm + 16 * i;
+            if (mi >= m) continue;
+            double* p = g.Y + i64(lo + mi) + i64(n) * g.ldy;
+            *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        }
+    }
+}
+
+// ------------------------------------------------------------ elementwise
+__global__ void k_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
+    const i64 total = n * w;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e % n, j = e / n;
+        double* y = Y + i + j * ldy;
+        const double x = X ? alpha * X[i + j * ldx] : 0.0;
+        *y = x + (beta != 0.0 ? beta * *y : 0.0);
+    }
+}
+
+__global__ void k_parity_scale(const WorkItem* items, int w, const double* X, i64 ldx, double ae, double ao,
+                               double* Y, i64 ldy, double beta) {
+    const WorkItem it = items[blockIdx.x];
+    const double a = (it.seg & 1) ? ao : ae;
+    for (int e = threadIdx.x; e < it.rows * w; e += blockDim.x) {
+        const int r = e % it.rows, j = e / it.rows;
+        const i64 row = i64(it.row0) + r;
+        double* y = Y + row + i64(j) * ldy;
+        *y = a * X[row + i64(j) * ldx] + (beta != 0.0 ? beta * *y : 0.0);
+    }
+}
+
+// -------------------------------------------------------------- reductions
+__device__ double block_sum(double v) {
+    __shared__ double sh[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    v = (threadIdx.x < (blockDim.x >> 5)) ? sh[lane] : 0.0;
+    if (wid == 0)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;  // valid in thread 0
+}
+
+struct DotPanels {
+    i64 n;
+    const double *A, *B;
+    i64 lda, ldb;
+    __device__ double operator()(i64 e) const {
+        const i64 i = e % n, j = e / n;
+        return A[i + j * lda] * B[i + j * ldb];
+    }
+};
+
+struct PairDot {
+    int ra, rb, xr, ldg, ldh;
+    i64 gs, hs;
+    const double *G, *H;
+    __device__ double operator()(i64 e) const {
+        const i64 per = i64(ra) * rb;
+        const int s = int(e / per);
+        const int rem = int(e % per), a = rem % ra, b = rem / ra;
+        return G[i64(s) * gs + a + i64(b) * ldg] * H[i64(s ^ xr) * hs + b + i64(a) * ldh];
+    }
+};
+
+struct LeafTrace {
+    const int* bounds;
+    int bmax, ldl;
+    i64 lstride;
+    const double* L;
+    __device__ double operator()(i64 e) const {
+        const int b = int(e / bmax), i = int(e % bmax);
+        if (i >= bounds[b + 1] - bounds[b]) return 0.0;
+        return L[i64(b) * lstride + i + i64(i) * ldl];
+    }
+};
+
+struct LeafPair {
+    const int* bounds;
+    int bmax, ldl;
+    i64 lstride;
+    const double *A, *B;
+    __device__ double operator()(i64 e) const {
+        const i64 per = i64(bmax) * bmax;
+        const int b = int(e / per);
+        const int rem = int(e % per), r = rem % bmax, c = rem / bmax;
+        const int m = bounds[b + 1] - bounds[b];
+        if (r >= m || c >= m) return 0.0;
+        const i64 base = i64(b) * lstride;
+        return A[base + c + i64(r) * ldl] * B[base + r + i64(c) * ldl];
+    }
+};
+
+template <class F>
+__global__ void k_reduce_partial(F f, i64 total, double* partial) {
+    double v = 0.0;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) v += f(e);
+    v = block_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+}
+
+__global__ void k_reduce_final(const double* partial, int np, double* out, int accumulate) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) v += partial[i];
+    v = block_sum(v);
+    if (threadIdx.x == 0) *out = accumulate ? *out + v : v;
+}
+
+template <class F>
+void reduce(F f, i64 total, double* out, bool accumulate) {
+    auto& c = current();
+    DVec partial(RED_BLOCKS);
+    k_reduce_partial<<<RED_BLOCKS, 256, 0, c.stream>>>(f, total, partial.get());
+    HG_LAUNCH();
+    k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), RED_BLOCKS, out, accumulate ? 1 : 0);
+    HG_LAUNCH();
+    c.launches += 2;
+}
+
+}  // namespace
+
+void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* B, i64 ldb, int cb, double* T,
+            i64 tstride, int ldt, double alpha, double beta) {
+    if (ca <= 0 || cb <= 0) return;
+    auto& c = current();
+    const TileList& tl = p.tiles(SEG_CHUNK);
+    const int tiles_m = cdiv(ca, TM), tiles_n = cdiv(cb, TN);
+    SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
+    dim3 grid(unsigned(tl.count), unsigned(tiles_m * tiles_n));
+    if (tl.one_per_seg) {
+        k_seg_tn<<<grid, NT, 0, c.stream>>>(g);
+        HG_LAUNCH();
+        ++c.launches;
+        return;
+    }
+    const i64 wstride = i64(ca) * cb;
+    DVec ws(size_t(wstride) * size_t(tl.count));
+    g.out = ws.get();
+    g.ostride = wstride;
+    g.ldo = ca;
+    g.direct = 0;
+    k_seg_tn<<<grid, NT, 0, c.stream>>>(g);
+    HG_LAUNCH();
+    dim3 rgrid(unsigned(cdiv(wstride, 256)), unsigned(p.nseg()));
+    k_seg_reduce<<<rgrid, 256, 0, c.stream>>>(ws.get(), wstride, ca, cb, tl.seg_first.get(), T, tstride, ldt, alpha,
+                                              beta);
+    HG_LAUNCH();
+    c.launches += 2;
+}
+
+void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T, i64 tstride, int ldt, TMap map,
+            double* Y, i64 ldy, int w, double alpha, double beta) {
+    if (w <= 0) return;
+    auto& c = current();
+    if (k <= 0) {
+        if (beta != 1.0) panel_axpby(p.hbounds().back(), w, 0.0, nullptr, 0, beta, Y, ldy);
+        return;
+    }
+    const TileList& tl = p.tiles(TM);
+    SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
+    dim3 grid(unsigned(tl.count), unsigned(cdiv(w, TN)));
+    k_seg_nn<<<grid, NT, 0, c.stream>>>(g);
+    HG_LAUNCH();
+    ++c.launches;
+}
+
+void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, bool trans, const double* X, i64 ldx,
+             double* Y, i64 ldy, int w, double alpha, double beta) {
+    if (w <= 0) return;
+    auto& c = current();
+    const int rt = cdiv(leaves.max_seg(), TM);
+    LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
+    dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, TN)));
+    if (trans)
+        k_leaf_mm<true><<<grid, NT, 0, c.stream>>>(g);
+    else
+        k_leaf_mm<false><<<grid, NT, 0, c.stream>>>(g);
+    HG_LAUNCH();
+    ++c.launches;
+}
+
+void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
+    if (n <= 0 || w <= 0) return;
+    auto& c = current();
+    const i64 total = n * w;
+    const int blocks = int(std::min<i64>((total + 255) / 256, 148 * 16));
+    k_axpby<<<blocks, 256, 0, c.stream>>>(n, w, alpha, X, ldx, beta, Y, ldy);
+    HG_LAUNCH();
+    ++c.launches;
+}
+
+void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 ldx, double a_even, double a_odd,
+                        double* Y, i64 ldy, double beta) {
+    (void)n;
+    if (w <= 0) return;
+    auto& c = current();
+    const TileList& tl = p.tiles(256);
+    k_parity_scale<<<tl.count, 256, 0, c.stream>>>(tl.items.get(), w, X, ldx, a_even, a_odd, Y, ldy, beta);
+    HG_LAUNCH();
+    ++c.launches;
+}
+
+void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate) {
+    reduce(DotPanels{n, A, B, lda, ldb}, n * i64(w), out, accumulate);
+}
+
+void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,
+                  int ldh, double* out, bool accumulate) {
+    reduce(PairDot{ra, rb, xr, ldg, ldh, gs, hs, G, H}, i64(nseg) * ra * rb, out, accumulate);
+}
+
+void leaf_trace(const Partition& leaves, const double* L, i64 lstride, int ldl, double* out, bool accumulate) {
+    reduce(LeafTrace{leaves.dbounds(), leaves.max_seg(), ldl, lstride, L}, i64(leaves.nseg()) * leaves.max_seg(), out,
+           accumulate);
+}
+
+void leaf_pair_dot(const Partition& leaves, const double* A, const double* B, i64 lstride, int ldl, double* out,
+                   bool accumulate) {
+    const int bm = leaves.max_seg();
+    reduce(LeafPair{leaves.dbounds(), bm, ldl, lstride, A, B}, i64(leaves.nseg()) * bm * bm, out, accumulate);
+}
+
+double read_scalar(const double* d) {
+    double h = 0;
+    HG_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, current().stream));
+    HG_CUDA(cudaStreamSynchronize(current().stream));
+    return h;
+}
+
+}  // namespace hg

@@ -1,0 +1,65 @@
+// Batched FP64 primitives over flattened per-level row panels.
+//
+// Every HODLR operation of the hot path reduces to a handful of segmented
+// kernels over the row ranges of one tree depth ("segments"):
+//   seg_tn    T_s = alpha * A[s]^T B[s] + beta T_s      (projections, Gram blocks)
+//   seg_nn    Y[s] = alpha * X[s] T_{map(s)} + beta Y[s]  (low-rank updates)
+//   leaf_mm   Y[leaf] = alpha * op(L_b) X[leaf] + beta Y[leaf]
+//   reductions (deterministic, fixed order) for traces.
+// Panels are column-major n x w arrays; segment s of depth d covers rows
+// [bounds[s], bounds[s+1]).
+#pragma once
+
+#include "tree.cuh"
+
+namespace hg {
+
+/// Selects the small right factor of segment s in seg_nn:
+/// index = (s >> shift) ^ xr; first row = (s & 1) ? row_odd : row_even.
+struct TMap {
+    int shift = 0, xr = 0, row_even = 0, row_odd = 0;
+    static TMap same() { return TMap{}; }
+    static TMap sibling() { return TMap{0, 1, 0, 0}; }
+    static TMap parent(int re, int ro) { return TMap{1, 0, re, ro}; }
+};
+
+/// T_s (ca x cb, col-major, ld ldt, stride tstride per segment) =
+/// alpha A[s]^T B[s] + beta T_s. Deterministic split-K over row chunks.
+void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* B, i64 ldb, int cb,
+            double* T, i64 tstride, int ldt, double alpha = 1.0, double beta = 0.0);
+
+/// Y[s] (rows x w) = alpha X[s] (rows x k) * T_sel (k x w) + beta Y[s].
+void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T, i64 tstride, int ldt,
+            TMap map, double* Y, i64 ldy, int w, double alpha = 1.0, double beta = 0.0);
+
+/// Leaves: Y[leaf b] = alpha op(L_b) X[leaf b] + beta Y[leaf b]; L_b at
+/// L + b*lstride with ld ldl (m_b x m_b).
+void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, bool trans, const double* X,
+             i64 ldx, double* Y, i64 ldy, int w, double alpha = 1.0, double beta = 0.0);
+
+/// Copy / scale / add panels: Y = alpha X + beta Y over n x w.
+void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy);
+
+/// Masked copy by segment parity at a depth: rows of even (odd) segments
+/// take alpha_even * X (alpha_odd * X); columns [0, w).
+void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 ldx, double a_even,
+                        double a_odd, double* Y, i64 ldy, double beta);
+
+/// out[0] (+)= sum(A .* B) over n x w (deterministic).
+void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate);
+
+/// out[0] (+)= sum_s sum_{a<ra,b<rb} G_s(a,b) H_{s^xr}(b,a) with G_s ra x rb (ld
+/// ldg, stride gs), H_s rb x ra (ld ldh, stride hs).
+void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,
+                  int ldh, double* out, bool accumulate);
+
+/// out[0] (+)= sum_b trace(L_b) (leaves, ld ldl, stride lstride).
+void leaf_trace(const Partition& leaves, const double* L, i64 lstride, int ldl, double* out, bool accumulate);
+/// out[0] (+)= sum_b sum(A_b^T .* B_b).
+void leaf_pair_dot(const Partition& leaves, const double* A, const double* B, i64 lstride, int ldl, double* out,
+                   bool accumulate);
+
+/// Final host read of a device scalar (synchronizes the stream).
+double read_scalar(const double* d);
+
+}  // namespace hg

@@ -1,0 +1,642 @@
+"""Host-side mirror of the reference `hodlrgp` C++ API over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/hodlrgp/*.hpp; every numerical call goes through
+lib/libhodlrgp_b200.so (include/hodlrgp_b200.h) on the GPU. There is no CPU
+fallback: importing on a box without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhodlrgp_b200.so")
+
+i64, u64, dbl, vp = C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int)
+lp = C.POINTER(C.c_int64)
+
+HOST, DEVICE = 0, 1
+RIGHT, LEFT = 0, 1
+
+_SIGS = {
+    "hg_last_error": (C.c_char_p, []),
+    "hg_ctx_create": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
+    "hg_ctx_destroy": (C.c_int, [vp]),
+    "hg_ctx_synchronize": (C.c_int, [vp]),
+    "hg_ctx_launches": (u64, [vp]),
+    "hg_ctx_stream": (vp, [vp]),
+    "hg_tree_depth": (C.c_int, [i64, i64, i64]),
+    "hg_tree_ranges": (C.c_int, [i64, C.c_int, lp]),
+    "hg_kd_ordering": (C.c_int, [i64, C.c_int, dp, i64, i64, lp, lp, ip]),
+    "hg_hodlr_zero": (C.c_int, [vp, i64, C.c_int, C.c_int, C.POINTER(vp)]),
+    "hg_hodlr_identity": (C.c_int, [vp, i64, C.c_int, C.POINTER(vp)]),
+    "hg_hodlr_random": (C.c_int, [vp, i64, C.c_int, i64, u64, C.c_int, C.POINTER(vp)]),
+    "hg_hodlr_import": (C.c_int, [vp, i64, C.c_int, C.c_int, ip, dp, ip, ip, C.POINTER(vp)]),
+    "hg_hodlr_info": (C.c_int, [vp, lp, ip, ip, ip]),
+    "hg_hodlr_export_size": (i64, [vp]),
+    "hg_hodlr_export": (C.c_int, [vp, vp, dp, ip, ip]),
+    "hg_hodlr_copy": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "hg_hodlr_free": (C.c_int, [vp]),
+    "hg_hodlr_make_asymmetric": (C.c_int, [vp, vp]),
+    "hg_hodlr_matvec": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, C.c_int]),
+    "hg_hodlr_sub_matvec": (C.c_int, [vp, vp, C.c_int, i64, vp, i64, i64, C.c_int, vp, i64, C.c_int]),
+    "hg_hodlr_trace": (C.c_int, [vp, vp, dp]),
+    "hg_trace_product": (C.c_int, [vp, vp, vp, dp]),
+    "hg_factorize": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
+    "hg_factor_free": (C.c_int, [vp]),
+    "hg_factor_solve": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, C.c_int]),
+    "hg_factor_logdet": (C.c_int, [vp, vp, dp]),
+    "hg_factor_leaf_llt": (C.c_int, [vp, vp, ip]),
+    "hg_multiply": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
+    "hg_solve_multiply": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
+    "hg_prodrep_free": (C.c_int, [vp]),
+    "hg_prodrep_densify": (C.c_int, [vp, vp, dp]),
+    "hg_trace_product_rep": (C.c_int, [vp, vp, dp]),
+    "hg_trace_pair": (C.c_int, [vp, vp, vp, dp]),
+    "hg_trace_solve": (C.c_int, [vp, vp, vp, dp]),
+    "hg_trace_quad": (C.c_int, [vp, vp, vp, vp, vp, dp]),
+    "hg_oracle_dense": (C.c_int, [vp, i64, dp, C.c_int, dp, C.POINTER(vp)]),
+    "hg_oracle_matern": (C.c_int, [vp, i64, dp, C.c_int, dbl, dbl, dbl, C.c_int, C.POINTER(vp)]),
+    "hg_oracle_callback": (C.c_int, [vp, i64, C.c_int, vp, vp, C.POINTER(vp)]),
+    "hg_oracle_set_parameters": (C.c_int, [vp, dp, C.c_int]),
+    "hg_oracle_free": (C.c_int, [vp]),
+    "hg_oracle_apply": (C.c_int, [vp, vp, C.c_int, vp, i64, i64, vp, i64, C.c_int]),
+    "hg_oracle_counters": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.c_int]),
+    "hg_build": (C.c_int, [vp, vp, C.c_int, i64, u64, C.c_int, C.POINTER(vp)]),
+    "hg_build_free": (C.c_int, [vp]),
+    "hg_build_h": (C.c_int, [vp, C.POINTER(vp)]),
+    "hg_build_deriv": (C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+    "hg_build_num_warnings": (C.c_int, [vp]),
+    "hg_build_decisions": (C.c_int, [vp, C.c_int, lp]),
+    "hg_log_likelihood": (C.c_int, [vp, vp, dp, dp, dp]),
+    "hg_score": (C.c_int, [vp, vp, C.POINTER(vp), C.c_int, dp, dp, dp]),
+    "hg_fisher_information": (C.c_int, [vp, vp, C.POINTER(vp), C.c_int, dp]),
+    "hg_mle_iteration": (C.c_int, [vp, vp, C.c_int, i64, u64, dp, dp, dp, dp, dp]),
+}
+
+_lib = None
+_ctx = None
+
+
+def lib():
+    """Load the C ABI library (raises if it was not built: no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"hodlrgp_b200: {LIB_PATH} not built (run `make -C paper_2303_10102_b200`)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name, None)
+            if f is None:
+                continue
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class HodlrError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class NotPositiveDefinite(HodlrError):
+    """factorization.hpp:14-16"""
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().hg_last_error().decode()
+    if rc == 1:
+        raise NotPositiveDefinite(rc, msg)
+    if rc == 2:
+        raise ValueError(msg)
+    if rc == 3:
+        raise OverflowError(msg)
+    if rc == 4:
+        raise TypeError(msg)
+    if rc == 5:
+        raise MemoryError(msg)
+    raise HodlrError(rc, msg)
+
+
+class Context:
+    """One device + one CUDA stream (hg_ctx_create)."""
+
+    def __init__(self, device=0, stream=None):
+        h = vp()
+        _check(lib().hg_ctx_create(device, stream, C.byref(h)))
+        self.ptr = h
+
+    def synchronize(self):
+        _check(lib().hg_ctx_synchronize(self.ptr))
+
+    @property
+    def launches(self):
+        return int(lib().hg_ctx_launches(self.ptr))
+
+    @property
+    def stream(self):
+        return lib().hg_ctx_stream(self.ptr)
+
+
+def context():
+    global _ctx
+    if _ctx is None:
+        _ctx = Context(0)
+    return _ctx
+
+
+def _d(a):
+    return a.ctypes.data_as(dp)
+
+
+def _f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr_ld(x):
+    """(pointer, ld, rows, cols, loc) for a numpy array or a CUDA torch tensor."""
+    if isinstance(x, np.ndarray):
+        x = _f(x)
+        return x.ctypes.data, x.shape[0], x.shape[0], x.shape[1] if x.ndim > 1 else 1, HOST, x
+    # torch tensor on the device: column-major view required (stride(0) == 1)
+    if x.dim() == 1:
+        return x.data_ptr(), x.shape[0], x.shape[0], 1, DEVICE, x
+    if x.stride(0) != 1:
+        raise ValueError("device tensors must be column-major (use t.T.contiguous().T)")
+    return x.data_ptr(), x.stride(1), x.shape[0], x.shape[1], DEVICE, x
+
+
+# ------------------------------------------------------------------ tree
+def tree_depth(n, leaf_min, leaf_max):
+    """cluster_tree.cpp:34-38"""
+    return lib().hg_tree_depth(n, leaf_min, leaf_max)
+
+
+class ClusterTree:
+    """cluster_tree.hpp:24-51 (host; bit-exact)."""
+
+    def __init__(self, n, tau):
+        self.n, self.tau = n, tau
+        cnt = 2 ** (tau + 1) - 1
+        out = np.zeros(2 * cnt, dtype=np.int64)
+        _check(lib().hg_tree_ranges(n, tau, out.ctypes.data_as(lp)))
+        self._levels, o = [], 0
+        for d in range(tau + 1):
+            self._levels.append([(int(out[o + 2 * i]), int(out[o + 2 * i + 1])) for i in range(2 ** d)])
+            o += 2 ** (d + 1)
+
+    def size(self):
+        return self.n
+
+    def depth(self):
+        return self.tau
+
+    def level(self, d):
+        return self._levels[d]
+
+    def leaves(self):
+        return self._levels[self.tau]
+
+    def num_leaves(self):
+        return len(self._levels[self.tau])
+
+    def max_leaf_size(self):
+        return max(hi - lo for lo, hi in self.leaves())
+
+
+def build_kd_ordering(coords, leaf_min, leaf_max):
+    """cluster_tree.cpp:40-90 -> (perm, inv, tree)."""
+    c = _f(coords)
+    if c.ndim == 1:
+        c = c.reshape(-1, 1, order="F")
+    n, d = c.shape
+    perm = np.zeros(n, dtype=np.int64)
+    inv = np.zeros(n, dtype=np.int64)
+    tau = C.c_int()
+    _check(lib().hg_kd_ordering(n, d, _d(c), leaf_min, leaf_max, perm.ctypes.data_as(lp), inv.ctypes.data_as(lp),
+                                C.byref(tau)))
+    return perm, inv, ClusterTree(n, tau.value)
+
+
+# ----------------------------------------------------------- HodlrMatrix
+class HodlrMatrix:
+    """hodlr_matrix.hpp:48-106, device resident."""
+
+    def __init__(self, ptr, ctx=None):
+        self.ptr = ptr
+        self.ctx = ctx or context()
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_hodlr_free(self.ptr)
+            self.ptr = None
+
+    @staticmethod
+    def _make(fn, *args, ctx=None):
+        ctx = ctx or context()
+        h = vp()
+        _check(fn(ctx.ptr, *args, C.byref(h)))
+        return HodlrMatrix(h, ctx)
+
+    @staticmethod
+    def zero(tree, symmetric=True, ctx=None):
+        return HodlrMatrix._make(lib().hg_hodlr_zero, tree.n, tree.tau, int(symmetric), ctx=ctx)
+
+    @staticmethod
+    def identity(tree, ctx=None):
+        return HodlrMatrix._make(lib().hg_hodlr_identity, tree.n, tree.tau, ctx=ctx)
+
+    @staticmethod
+    def random_spd(tree, k, seed, ctx=None):
+        return HodlrMatrix._make(lib().hg_hodlr_random, tree.n, tree.tau, k, seed, 1, ctx=ctx)
+
+    @staticmethod
+    def random_symmetric(tree, k, seed, ctx=None):
+        return HodlrMatrix._make(lib().hg_hodlr_random, tree.n, tree.tau, k, seed, 0, ctx=ctx)
+
+    @staticmethod
+    def from_panels(p, ctx=None):
+        """Import the panel exchange format (see include/hodlrgp_b200.h)."""
+        R = np.asarray(list(p["R"]) or [0], dtype=np.int32)
+        ru = np.asarray(list(p["ranks_up"]) or [0], dtype=np.int32)
+        rl = np.asarray(list(p["ranks_lo"]) or [0], dtype=np.int32)
+        flat = np.ascontiguousarray(p["flat"], dtype=np.float64)
+        return HodlrMatrix._make(lib().hg_hodlr_import, p["n"], p["tau"], int(p["sym"]), R.ctypes.data_as(ip),
+                                 _d(flat), ru.ctypes.data_as(ip), rl.ctypes.data_as(ip), ctx=ctx)
+
+    def info(self):
+        n, tau, sym = C.c_int64(), C.c_int(), C.c_int()
+        _check(lib().hg_hodlr_info(self.ptr, C.byref(n), C.byref(tau), C.byref(sym), None))
+        R = np.zeros(max(tau.value, 1), dtype=np.int32)
+        _check(lib().hg_hodlr_info(self.ptr, C.byref(n), C.byref(tau), C.byref(sym), R.ctypes.data_as(ip)))
+        return n.value, tau.value, bool(sym.value), [int(r) for r in R[: tau.value]]
+
+    def size(self):
+        return self.info()[0]
+
+    def depth(self):
+        return self.info()[1]
+
+    def symmetric(self):
+        return self.info()[2]
+
+    def tree(self):
+        n, tau, _, _ = self.info()
+        return ClusterTree(n, tau)
+
+    def export_panels(self):
+        n, tau, sym, R = self.info()
+        flat = np.zeros(int(lib().hg_hodlr_export_size(self.ptr)))
+        nn = max(2 ** tau - 1, 1)
+        ru = np.zeros(nn, dtype=np.int32)
+        rl = np.zeros(nn, dtype=np.int32)
+        _check(lib().hg_hodlr_export(self.ctx.ptr, self.ptr, _d(flat), ru.ctypes.data_as(ip), rl.ctypes.data_as(ip)))
+        return dict(n=n, tau=tau, sym=sym, R=R, flat=flat, ranks_up=ru[: 2 ** tau - 1], ranks_lo=rl[: 2 ** tau - 1])
+
+    def copy(self):
+        h = vp()
+        _check(lib().hg_hodlr_copy(self.ctx.ptr, self.ptr, C.byref(h)))
+        return HodlrMatrix(h, self.ctx)
+
+    def make_asymmetric(self):
+        _check(lib().hg_hodlr_make_asymmetric(self.ctx.ptr, self.ptr))
+
+    def matvec(self, x):
+        """y = H x (numpy in -> numpy out; CUDA tensor in -> CUDA tensor out)."""
+        vec = getattr(x, "ndim", None) == 1
+        if isinstance(x, np.ndarray):
+            xx = _f(x).reshape(x.shape[0], -1, order="F")
+            y = np.zeros_like(xx, order="F")
+            _check(lib().hg_hodlr_matvec(self.ctx.ptr, self.ptr, xx.ctypes.data, xx.shape[0], xx.shape[1],
+                                         y.ctypes.data, y.shape[0], HOST))
+            return y[:, 0] if vec else y
+        px, ldx, rows, cols, loc, keep = _ptr_ld(x)
+        import torch
+
+        y = torch.empty((cols, rows), dtype=torch.float64, device=x.device).T
+        _check(lib().hg_hodlr_matvec(self.ctx.ptr, self.ptr, px, ldx, cols, y.data_ptr(), y.stride(1), DEVICE))
+        return y
+
+    def sub_matvec(self, d, node, x, transpose=False):
+        xx = _f(x)
+        vec = xx.ndim == 1
+        xx = xx.reshape(xx.shape[0], -1, order="F")
+        y = np.zeros_like(xx, order="F")
+        _check(lib().hg_hodlr_sub_matvec(self.ctx.ptr, self.ptr, d, node, xx.ctypes.data, xx.shape[0], xx.shape[1],
+                                         int(transpose), y.ctypes.data, y.shape[0], HOST))
+        return y[:, 0] if vec else y
+
+    def trace(self):
+        out = C.c_double()
+        _check(lib().hg_hodlr_trace(self.ctx.ptr, self.ptr, C.byref(out)))
+        return out.value
+
+    def densify(self):
+        """Dense assembly from exported panels (hodlr_matrix.cpp:273-292; n <= 2^14)."""
+        p = self.export_panels()
+        return densify_panels(p)
+
+
+def densify_panels(p):
+    n, tau = p["n"], p["tau"]
+    if n > 2 ** 14:
+        raise OverflowError("densify: matrix too large")
+    t = ClusterTree(n, tau)
+    a = np.zeros((n, n))
+    off = 0
+    for l in range(1, tau + 1):
+        R = p["R"][l - 1]
+        U = p["flat"][off: off + n * R].reshape((n, R), order="F")
+        V = p["flat"][off + n * R: off + 2 * n * R].reshape((n, R), order="F")
+        off += 2 * n * R
+        kids = t.level(l)
+        for j in range(2 ** (l - 1)):
+            (a0, a1), (b0, b1) = kids[2 * j], kids[2 * j + 1]
+            a[a0:a1, b0:b1] = U[a0:a1] @ V[b0:b1].T
+            a[b0:b1, a0:a1] = U[b0:b1] @ V[a0:a1].T
+    for lo, hi in t.leaves():
+        m = hi - lo
+        a[lo:hi, lo:hi] = p["flat"][off: off + m * m].reshape((m, m), order="F")
+        off += m * m
+    return a
+
+
+def trace_product(a, b):
+    """HodlrMatrix::trace_product (hodlr_matrix.cpp:294-318)."""
+    out = C.c_double()
+    _check(lib().hg_trace_product(a.ctx.ptr, a.ptr, b.ptr, C.byref(out)))
+    return out.value
+
+
+# --------------------------------------------------------- factorization
+class HodlrFactorization:
+    """factorization.hpp:45-78"""
+
+    def __init__(self, ptr, ctx, n):
+        self.ptr, self.ctx, self.n = ptr, ctx, n
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_factor_free(self.ptr)
+            self.ptr = None
+
+    def solve(self, b):
+        bb = _f(b)
+        vec = bb.ndim == 1
+        bb = bb.reshape(bb.shape[0], -1, order="F")
+        x = np.zeros_like(bb, order="F")
+        _check(lib().hg_factor_solve(self.ctx.ptr, self.ptr, bb.ctypes.data, bb.shape[0], bb.shape[1], x.ctypes.data,
+                                     x.shape[0], HOST))
+        return x[:, 0] if vec else x
+
+    def logdet(self):
+        out = C.c_double()
+        _check(lib().hg_factor_logdet(self.ctx.ptr, self.ptr, C.byref(out)))
+        return out.value
+
+    def leaf_llt(self):
+        t = ClusterTree(self.n, 0)
+        del t
+        out = np.zeros(1 << 20, dtype=np.int32)
+        _check(lib().hg_factor_leaf_llt(self.ctx.ptr, self.ptr, out.ctypes.data_as(ip)))
+        return out
+
+
+def factorize(h, orientation=RIGHT):
+    """factorization.cpp:62-168"""
+    f = vp()
+    _check(lib().hg_factorize(h.ctx.ptr, h.ptr, orientation, C.byref(f)))
+    return HodlrFactorization(f, h.ctx, h.size())
+
+
+# --------------------------------------------------------- trace algebra
+class ProductRep:
+    """product_rep.hpp:14-26"""
+
+    def __init__(self, ptr, ctx, n):
+        self.ptr, self.ctx, self.n = ptr, ctx, n
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_prodrep_free(self.ptr)
+            self.ptr = None
+
+    def densify(self):
+        out = np.zeros((self.n, self.n), order="F")
+        _check(lib().hg_prodrep_densify(self.ctx.ptr, self.ptr, _d(out)))
+        return out
+
+
+def multiply(f, b):
+    p = vp()
+    _check(lib().hg_multiply(f.ctx.ptr, f.ptr, b.ptr, C.byref(p)))
+    return ProductRep(p, f.ctx, f.n)
+
+
+def solve_multiply(f, b):
+    p = vp()
+    _check(lib().hg_solve_multiply(f.ctx.ptr, f.ptr, b.ptr, C.byref(p)))
+    return ProductRep(p, f.ctx, f.n)
+
+
+def trace_product_rep(p):
+    out = C.c_double()
+    _check(lib().hg_trace_product_rep(p.ctx.ptr, p.ptr, C.byref(out)))
+    return out.value
+
+
+def trace_pair(p, q):
+    out = C.c_double()
+    _check(lib().hg_trace_pair(p.ctx.ptr, p.ptr, q.ptr, C.byref(out)))
+    return out.value
+
+
+def trace_solve(f, b):
+    if isinstance(f, HodlrMatrix):
+        f = factorize(f, LEFT)
+    out = C.c_double()
+    _check(lib().hg_trace_solve(f.ctx.ptr, f.ptr, b.ptr, C.byref(out)))
+    return out.value
+
+
+def trace_quad(fa, b, fc, d):
+    if isinstance(fa, HodlrMatrix):
+        fa = factorize(fa, LEFT)
+    if isinstance(fc, HodlrMatrix):
+        fc = factorize(fc, LEFT)
+    out = C.c_double()
+    _check(lib().hg_trace_quad(fa.ctx.ptr, fa.ptr, b.ptr, fc.ptr, d.ptr, C.byref(out)))
+    return out.value
+
+
+# ----------------------------------------------------- covariance oracle
+class CovarianceOracle:
+    """oracle.hpp:15-52 with the forward model on the device."""
+
+    def __init__(self, ptr, ctx, n, p):
+        self.ptr, self.ctx, self.n, self.p = ptr, ctx, n, p
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_oracle_free(self.ptr)
+            self.ptr = None
+
+    def dim(self):
+        return self.n
+
+    def num_params(self):
+        return self.p
+
+    def set_parameters(self, theta):
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        _check(lib().hg_oracle_set_parameters(self.ptr, _d(th), len(th)))
+
+    def apply(self, v, j=-1):
+        vv = _f(v).reshape(self.n, -1, order="F")
+        y = np.zeros_like(vv, order="F")
+        _check(lib().hg_oracle_apply(self.ctx.ptr, self.ptr, j, vv.ctypes.data, self.n, vv.shape[1], y.ctypes.data,
+                                     self.n, HOST))
+        return y
+
+    def apply_derivative(self, j, v):
+        return self.apply(v, j)
+
+    def counters(self, reset=False):
+        a, d = C.c_uint64(), C.c_uint64()
+        _check(lib().hg_oracle_counters(self.ptr, C.byref(a), C.byref(d), int(reset)))
+        return a.value, d.value
+
+    def apply_columns(self):
+        return self.counters()[0]
+
+    def derivative_columns(self):
+        return self.counters()[1]
+
+    def reset_counters(self):
+        self.counters(reset=True)
+
+
+def DenseMatrixOracle(k, dks=(), ctx=None):
+    """oracle.hpp:115-143"""
+    ctx = ctx or context()
+    k = _f(k)
+    n = k.shape[0]
+    buf = np.concatenate([_f(d).ravel(order="F") for d in dks]) if len(dks) else np.zeros(1)
+    o = vp()
+    _check(lib().hg_oracle_dense(ctx.ptr, n, _d(k), len(dks), _d(buf), C.byref(o)))
+    return CovarianceOracle(o, ctx, n, len(dks))
+
+
+def MaternOracle(x, nu2, sigma2, ell, nugget, scan=True, ctx=None):
+    """1D Matérn nu = nu2/2 (theta = sigma2, ell) with a fixed nugget."""
+    ctx = ctx or context()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    o = vp()
+    _check(lib().hg_oracle_matern(ctx.ptr, len(x), _d(x), nu2, sigma2, ell, nugget, int(scan), C.byref(o)))
+    return CovarianceOracle(o, ctx, len(x), 2)
+
+
+# ------------------------------------------------------------------ build
+class BuildResult:
+    """sketch.hpp:78-82"""
+
+    def __init__(self, ptr, ctx, p, tau):
+        self.ptr, self.ctx, self.p, self.tau = ptr, ctx, p, tau
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_build_free(self.ptr)
+            self.ptr = None
+
+    @property
+    def h(self):
+        o = vp()
+        _check(lib().hg_build_h(self.ptr, C.byref(o)))
+        return HodlrMatrix(o, self.ctx)
+
+    @property
+    def deriv(self):
+        out = []
+        for j in range(self.p):
+            o = vp()
+            _check(lib().hg_build_deriv(self.ptr, j, C.byref(o)))
+            out.append(HodlrMatrix(o, self.ctx))
+        return out
+
+    @property
+    def warnings(self):
+        return lib().hg_build_num_warnings(self.ptr)
+
+    def decisions(self):
+        cnt = max(2 ** self.tau - 1, 1)
+        out = np.zeros((cnt, 2 + self.p), dtype=np.int64)
+        k = lib().hg_build_decisions(self.ptr, self.p, out.ctypes.data_as(lp))
+        return out[:k]
+
+
+def build_hodlr(oracle, tree, k, seed):
+    """sketch.cpp:347-350 with SketchPlan(tree, k, seed)."""
+    b = vp()
+    _check(lib().hg_build(oracle.ctx.ptr, oracle.ptr, tree.tau, k, seed, 0, C.byref(b)))
+    return BuildResult(b, oracle.ctx, 0, tree.tau).h
+
+
+def build_hodlr_with_derivatives(oracle, tree, k, seed):
+    """sketch.cpp:352-356"""
+    b = vp()
+    _check(lib().hg_build(oracle.ctx.ptr, oracle.ptr, tree.tau, k, seed, 1, C.byref(b)))
+    return BuildResult(b, oracle.ctx, oracle.p, tree.tau)
+
+
+# -------------------------------------------------------------------- mle
+def _vec(y):
+    return np.ascontiguousarray(y, dtype=np.float64)
+
+
+def log_likelihood(f, y, ybar=None):
+    """mle.cpp:25-30"""
+    y = _vec(y)
+    yb = _vec(ybar) if ybar is not None else None
+    out = C.c_double()
+    _check(lib().hg_log_likelihood(f.ctx.ptr, f.ptr, _d(y), _d(yb) if yb is not None else None, C.byref(out)))
+    return out.value
+
+
+def score(f, deriv, y, ybar=None):
+    """mle.cpp:32-41"""
+    y = _vec(y)
+    yb = _vec(ybar) if ybar is not None else None
+    arr = (vp * len(deriv))(*[d.ptr for d in deriv])
+    out = np.zeros(len(deriv))
+    _check(lib().hg_score(f.ctx.ptr, f.ptr, arr, len(deriv), _d(y), _d(yb) if yb is not None else None, _d(out)))
+    return out
+
+
+def fisher_information(f, deriv):
+    """mle.cpp:43-54"""
+    p = len(deriv)
+    arr = (vp * p)(*[d.ptr for d in deriv])
+    out = np.zeros((p, p), order="F")
+    _check(lib().hg_fisher_information(f.ctx.ptr, f.ptr, arr, p, _d(out)))
+    return out
+
+
+def mle_iteration(oracle, tau, k, seed, y):
+    """One MLE iteration (acceptance.cpp:297-308) -> (loglik, score, fisher, times[5])."""
+    y = _vec(y)
+    p = oracle.p
+    ll = C.c_double()
+    s = np.zeros(p)
+    fi = np.zeros((p, p), order="F")
+    t = np.zeros(5)
+    _check(lib().hg_mle_iteration(oracle.ctx.ptr, oracle.ptr, tau, k, seed, _d(y), C.byref(ll), _d(s), _d(fi), _d(t)))
+    return ll.value, s, fi, t
