@@ -291,4 +291,92 @@ hg_status hg_trace_product(hg_ctx_t ctx, hg_hodlr_t a, hg_hodlr_t b, double* out
     return guard(ctx, [&] { *out = scalar_result([&](double* d) { hodlr_trace_product(a->h, b->h, d, false); }); });
 }
 
+// ---------------------------------------------------------- factorization
+hg_status hg_factorize(hg_ctx_t ctx, hg_hodlr_t h, int orientation, hg_factor_t* out) {
+    return guard(ctx, [&] {
+        if (orientation != HG_RIGHT && orientation != HG_LEFT) throw std::invalid_argument("factorize: orientation");
+        *out = new hg_factor_s{factorize(h->h, orientation)};
+    });
+}
+
+hg_status hg_factor_free(hg_factor_t f) {
+    delete f;
+    return HG_OK;
+}
+
+hg_status hg_factor_solve(hg_ctx_t ctx, hg_factor_t f, const double* B, int64_t ldb, int64_t s, double* X,
+                          int64_t ldx, int loc) {
+    return guard(ctx, [&] {
+        const i64 n = f->f.n();
+        if (ldb < n || ldx < n) throw std::invalid_argument("solve: dimension mismatch");
+        Output y(X, ldx, n, s, loc);
+        if (!(loc == HG_DEVICE && B == X && ldb == ldx))
+            HG_CUDA(cudaMemcpy2DAsync(y.dptr, size_t(y.ld) * sizeof(double), B, size_t(ldb) * sizeof(double),
+                                      size_t(n) * sizeof(double), size_t(s),
+                                      loc == HG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                      current().stream));
+        factor_solve(f->f, y.dptr, y.ld, int(s));
+        y.finish();
+    });
+}
+
+hg_status hg_factor_logdet(hg_ctx_t ctx, hg_factor_t f, double* out) {
+    return guard(ctx, [&] { *out = factor_logdet(f->f); });
+}
+
+hg_status hg_factor_leaf_llt(hg_ctx_t ctx, hg_factor_t f, int* out) {
+    return guard(ctx, [&] {
+        auto k = leaf_kinds(f->f);
+        for (size_t i = 0; i < k.size(); ++i) out[i] = k[i];
+    });
+}
+
+// ---------------------------------------------------------- trace algebra
+hg_status hg_multiply(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, hg_prodrep_t* out) {
+    return guard(ctx, [&] { *out = new hg_prodrep_s{pipeline(f->f, b->h, false)}; });
+}
+
+hg_status hg_solve_multiply(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, hg_prodrep_t* out) {
+    return guard(ctx, [&] { *out = new hg_prodrep_s{pipeline(f->f, b->h, true)}; });
+}
+
+hg_status hg_prodrep_free(hg_prodrep_t p) {
+    delete p;
+    return HG_OK;
+}
+
+hg_status hg_prodrep_densify(hg_ctx_t ctx, hg_prodrep_t p, double* out) {
+    return guard(ctx, [&] {
+        auto a = prodrep_densify(p->p);
+        std::memcpy(out, a.data(), a.size() * sizeof(double));
+    });
+}
+
+hg_status hg_trace_product_rep(hg_ctx_t ctx, hg_prodrep_t p, double* out) {
+    return guard(ctx, [&] { *out = scalar_result([&](double* d) { trace_product_rep(p->p, d, false); }); });
+}
+
+hg_status hg_trace_pair(hg_ctx_t ctx, hg_prodrep_t p, hg_prodrep_t q, double* out) {
+    return guard(ctx, [&] {
+        if (!p->p.base.tree->host.same_structure(q->p.base.tree->host))
+            throw std::invalid_argument("trace_pair: tree mismatch");
+        *out = scalar_result([&](double* d) { trace_pair(p->p, q->p, d, false); });
+    });
+}
+
+hg_status hg_trace_solve(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, double* out) {
+    return guard(ctx, [&] {
+        DProductRep r = pipeline(f->f, b->h, true);
+        *out = scalar_result([&](double* d) { trace_product_rep(r, d, false); });
+    });
+}
+
+hg_status hg_trace_quad(hg_ctx_t ctx, hg_factor_t fa, hg_hodlr_t b, hg_factor_t fc, hg_hodlr_t d, double* out) {
+    return guard(ctx, [&] {
+        DProductRep p = pipeline(fa->f, b->h, true);
+        DProductRep q = pipeline(fc->f, d->h, true);
+        *out = scalar_result([&](double* x) { trace_pair(p, q, x, false); });
+    });
+}
+
 }  // extern "C"
