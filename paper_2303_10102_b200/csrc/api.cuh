@@ -1,16 +1,22 @@
 // Aggregate header of the device hot path (used by the C ABI).
 #pragma once
 
+#include "build.cuh"
 #include "prodrep.cuh"
 
 namespace hg {
 
 DHodlr hodlr_deep_copy(const DHodlr& h);
 
-// Filled in by oracle.cu / build.cu.
-struct DOracle {
-    virtual ~DOracle() = default;
-};
-struct DBuildResult {};
+/// mle.cpp:25-30 — r is the residual y - ybar (device, length n).
+double log_likelihood(const DFactor& f, const double* r);
+
+/// mle.cpp:32-41 with the p ProductReps K^-1 K_j kept in `reps` for reuse by
+/// the Fisher matrix (the same arithmetic the reference repeats per pair).
+std::vector<double> score(const DFactor& f, const std::vector<const DHodlr*>& deriv, const double* r,
+                          std::vector<DProductRep>* reps);
+
+/// mle.cpp:43-54 (p x p, column-major) from the cached ProductReps.
+std::vector<double> fisher_from_reps(const std::vector<DProductRep>& reps);
 
 }  // namespace hg

@@ -1,0 +1,606 @@
+// Sketch construction of H and dH/dtheta_j on the device (sketch.cpp:128-356).
+//
+// Level l is processed for all of its 2^(l-1) nodes at once: oracle applies
+// and peeling matvecs act on full n x k panels, the per-node range finders
+// are one batched (TSQR + column-pivoted Householder) QR, and the per-node
+// small algebra (sign fix, numeric rank, completion, diff_qr, q2 width,
+// recompression) runs one CTA per node.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <mutex>
+#include <random>
+
+#include "build.cuh"
+
+namespace hg {
+
+namespace {
+
+__global__ void k_leaf_identity(const int* bounds, double* P, i64 ldp) {
+    const int b = blockIdx.x;
+    const int lo = bounds[b], m = bounds[b + 1] - lo;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) P[i64(lo + i) + i64(i) * ldp] = 1.0;
+}
+
+/// Node arrays from the batched QR (or the full-width shortcut, sketch.cpp:159-170):
+/// R (k x k, sign-fixed, rows >= numeric rank zeroed), perm, sign, numeric rank.
+__global__ void k_range_post(int k, const int* qmap, const double* qR, const int* qperm, double* R, int* perm,
+                             double* sign, int* nr) {
+    const int j = blockIdx.x;
+    const int q = qmap[j];
+    double* Rj = R + i64(j) * k * k;
+    if (q < 0) {  // full width: q = I, r = 0
+        for (int e = threadIdx.x; e < k * k; e += blockDim.x) Rj[e] = 0.0;
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            perm[j * k + i] = i;
+            sign[j * k + i] = 1.0;
+        }
+        if (threadIdx.x == 0) nr[j] = k;
+        return;
+    }
+    const double* Q = qR + i64(q) * k * k;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int r = e % k;
+        const double s = Q[r + r * k] < 0 ? -1.0 : 1.0;
+        Rj[e] = s * Q[e];
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        perm[j * k + i] = qperm[q * k + i];
+        sign[j * k + i] = Q[i + i * k] < 0 ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    __shared__ int s_nr;
+    if (threadIdx.x == 0) {
+        const double d0 = fabs(Rj[0]);
+        int r = 0;
+        while (r < k && fabs(Rj[r + r * k]) > 64 * DBL_EPSILON * d0) ++r;
+        s_nr = r;
+        nr[j] = r;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x)
+        if (e % k >= s_nr) Rj[e] = 0.0;
+}
+
+/// S[cl] = Q * diag(sign) (or the identity for full-width nodes).
+__global__ void k_q_sign(const int* bounds, int k, const int* qmap, const double* sign, double* S, i64 lds) {
+    const int j = blockIdx.x;
+    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
+    const bool full = qmap[j] < 0;
+    for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
+        const int r = e % m, c = e / m;
+        double* p = S + i64(lo + r) + i64(c) * lds;
+        if (full)
+            *p = r == c ? 1.0 : 0.0;
+        else
+            *p *= sign[j * k + c];
+    }
+}
+
+__device__ double cta_sum(double v) {
+    __shared__ double sh[32];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
+    return t;
+}
+
+/// sketch.cpp:60-74: complete deficient columns with canonical basis vectors
+/// orthogonalised twice against the kept ones (skipping norms below 0.5).
+__global__ void k_complete(const int* bounds, int k, const int* nr, double* S, i64 lds, double* scratch) {
+    const int j = blockIdx.x;
+    int filled = nr[j];
+    if (filled >= k) return;
+    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
+    double* Q = S + lo;
+    double* v = scratch + lo;
+    __shared__ double g[512];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int e = 0; e < m && filled < k; ++e) {
+        // pass 1: v = e_e - Q_f Q_f[e,:]^T
+        for (int c = tid; c < filled; c += blockDim.x) g[c] = Q[e + i64(c) * lds];
+        __syncthreads();
+        for (int i = tid; i < m; i += blockDim.x) {
+            double s = (i == e) ? 1.0 : 0.0;
+            for (int c = 0; c < filled; ++c) s -= Q[i + i64(c) * lds] * g[c];
+            v[i] = s;
+        }
+        __syncthreads();
+        // pass 2: g = Q_f^T v ; v -= Q_f g
+        for (int c = warp; c < filled; c += nw) {
+            double s = 0.0;
+            for (int i = lane; i < m; i += 32) s += Q[i + i64(c) * lds] * v[i];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) g[c] = s;
+        }
+        __syncthreads();
+        double part = 0.0;
+        for (int i = tid; i < m; i += blockDim.x) {
+            double s = v[i];
+            for (int c = 0; c < filled; ++c) s -= Q[i + i64(c) * lds] * g[c];
+            v[i] = s;
+            part += s * s;
+        }
+        const double nv = sqrt(cta_sum(part));
+        if (nv < 0.5) {
+            __syncthreads();
+            continue;
+        }
+        for (int i = tid; i < m; i += blockDim.x) Q[i + i64(filled) * lds] = v[i] / nv;
+        ++filled;
+        __syncthreads();
+    }
+}
+
+/// presc (sketch.cpp:203-206): max over params of ||dY_param[cl]||_F.
+__global__ void k_presc(const int* bounds, int k, int p, const double* dY, i64 ld, double* presc) {
+    const int j = blockIdx.x;
+    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
+    double best = 0.0;
+    for (int q = 0; q < p; ++q) {
+        double part = 0.0;
+        for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
+            const int r = e % m, c = e / m;
+            const double v = dY[i64(lo + r) + i64(q * k + c) * ld];
+            part += v * v;
+        }
+        best = fmax(best, sqrt(cta_sum(part)));
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) presc[j] = best;
+}
+
+/// q2 width (sketch.cpp:214-221).
+__global__ void k_w2_nodes(int nodes, const int* bounds, int k, int kp, const int* qmap, const double* R2,
+                           const double* presc, int* w2out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nodes) return;
+    const int q = qmap[j];
+    if (q < 0) {
+        w2out[j] = 0;
+        return;
+    }
+    const int m = bounds[2 * j + 1] - bounds[2 * j];
+    const double* R = R2 + i64(q) * kp * kp;
+    const double d0 = fabs(R[0]);
+    const double fl = fmax(1e-10 * d0, 1e-12 * presc[j]);
+    const int cap = min(kp, m - k);
+    int w2 = 0;
+    while (w2 < cap && fabs(R[w2 + w2 * kp]) > fl) ++w2;
+    w2out[j] = w2;
+}
+
+/// Zero columns [w_j, wtot) of the rows of one child (odd = right) of node j.
+__global__ void k_mask_cols(const int* bounds, int odd, const int* wj, int wtot, double* P, i64 ldp) {
+    const int j = blockIdx.x;
+    const int c = 2 * j + odd;
+    const int lo = bounds[c], m = bounds[c + 1] - lo;
+    const int w0 = wj[j];
+    for (int e = threadIdx.x; e < m * (wtot - w0); e += blockDim.x) {
+        const int r = e % m, col = w0 + e / m;
+        P[i64(lo + r) + i64(col) * ldp] = 0.0;
+    }
+}
+
+/// diff_qr restricted to the in-span rotation (sketch.cpp:78-111,245-268):
+/// y = (Q_rw^T dY[:, perm[:rw]]) R_rw^{-1}; Omega = skew(strict lower of y).
+/// G holds Q^T dY (k x k) per child; one thread per row of y.
+__global__ void k_diffqr(int k, const double* G, const double* R, const int* perm, const int* nr, const int* qmap,
+                         double* Om, int* rw_out, int* ill) {
+    const int j = blockIdx.x;
+    const double* Gj = G + i64(2 * j) * k * k;  // left child block
+    const double* Rj = R + i64(j) * k * k;
+    double* O = Om + i64(j) * k * k;
+    __shared__ int s_rw;
+    __shared__ double y[64 * 65];
+    if (threadIdx.x == 0) {
+        int rw = 0;
+        const int r = nr[j];
+        if (qmap[j] >= 0 && r > 0) {
+            const double r00 = fabs(Rj[0]);
+            while (rw < r && fabs(Rj[rw + rw * k]) > 1e-6 * r00) ++rw;
+        }
+        s_rw = rw;
+        rw_out[j] = rw;
+        double dmax = 0.0, dmin = INFINITY;
+        for (int i = 0; i < rw; ++i) {
+            dmax = fmax(dmax, fabs(Rj[i + i * k]));
+            dmin = fmin(dmin, fabs(Rj[i + i * k]));
+        }
+        ill[j] = (rw > 0 && (!(dmin > 0) || dmax / dmin > 1e12)) ? 1 : 0;
+    }
+    __syncthreads();
+    const int rw = s_rw;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) O[e] = 0.0;
+    const int a = threadIdx.x;
+    if (a < rw) {
+        for (int c = 0; c < rw; ++c) {  // y(a,:) R_rw = y0(a,:), column by column
+            double s = Gj[a + perm[j * k + c] * k];
+            for (int i = 0; i < c; ++i) s -= y[a * 65 + i] * Rj[i + c * k];
+            y[a * 65 + c] = s / Rj[c + c * k];
+        }
+    }
+    __syncthreads();
+    if (a < rw)
+        for (int c = 0; c < a; ++c) {
+            O[a + c * k] = y[a * 65 + c];
+            O[c + a * k] = -y[a * 65 + c];
+        }
+}
+
+// ------------------------------------------------------------ recompression
+/// M_j = T_L T_R^T (W x W, zero outside wl x wr) from the per-child R factors.
+__global__ void k_core(int W, const double* Rc, double* M) {
+    const int j = blockIdx.x;
+    const double* L = Rc + i64(2 * j) * W * W;
+    const double* Rr = Rc + i64(2 * j + 1) * W * W;
+    double* Mj = M + i64(j) * W * W;
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+        const int a = e % W, b = e / W;
+        double s = 0.0;
+        for (int c = max(a, b); c < W; ++c) s += L[a + c * W] * Rr[b + c * W];
+        Mj[e] = s;
+    }
+}
+
+/// Truncation rank at rtol relative to the leading pivoted diagonal.
+__global__ void k_trunc_rank(int nodes, int W, const double* RM, const int* wmin, double rtol, int* r_out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nodes) return;
+    const double* R = RM + i64(j) * W * W;
+    const double d0 = fabs(R[0]);
+    int r = 0;
+    while (r < wmin[j] && fabs(R[r + r * W]) > rtol * d0) ++r;
+    r_out[j] = r;
+}
+
+/// TinL = Q_M[:, :r] (columns >= r zeroed, in place); TinR[perm[i], a] = R_M[a, i], a < r.
+__global__ void k_tins(int W, int rmax, const int* r, const double* RM, const int* permM, double* Tin) {
+    const int j = blockIdx.x;
+    const int rj = r[j];
+    double* TL = Tin + i64(2 * j) * W * rmax;
+    double* TR = Tin + i64(2 * j + 1) * W * rmax;
+    const double* R = RM + i64(j) * W * W;
+    for (int e = threadIdx.x; e < W * rmax; e += blockDim.x) {
+        const int i = e % W, a = e / W;
+        if (a >= rj) TL[e] = 0.0;
+        TR[e] = 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < W * rmax; e += blockDim.x) {
+        const int i = e % W, a = e / W;
+        if (a < rj) TR[permM[j * W + i] + i64(a) * W] = R[a + i64(i) * W];
+    }
+}
+
+std::vector<int> dl_int(const DBuf<int>& d) { return d.download(); }
+
+/// Recompress the derivative level panel D (n x W, symmetric storage) in
+/// place of `out` (hodlr_matrix.cpp:42-66 via sketch.cpp:331-341).
+void compress_level(DHodlr& D, int l, double rtol) {
+    const int W = D.Rl(l);
+    if (W == 0) return;
+    const DTree& t = *D.tree;
+    const i64 n = t.n();
+    const Partition& pc = t.part(l);
+    const int nodes = 1 << (l - 1);
+    const auto& hb = pc.hbounds();
+    double* P = D.Ul(l);
+    // Unpivoted QR of every child block (both factors of every node).
+    std::vector<BatchedQR::Block> blocks;
+    for (int c = 0; c < 2 * nodes; ++c) blocks.push_back({P + hb[static_cast<size_t>(c)], n, hb[static_cast<size_t>(c + 1)] - hb[static_cast<size_t>(c)]});
+    BatchedQR qr(blocks, W, false);
+    // Core M = T_L T_R^T and its rank-revealing pivoted QR.
+    DVec M(static_cast<size_t>(nodes) * W * W);
+    k_core<<<nodes, 256, 0, current().stream>>>(W, qr.R(), M.get());
+    HG_LAUNCH();
+    count_launch();
+    std::vector<BatchedQR::Block> mb;
+    for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * W * W, W, W});
+    BatchedQR mq(mb, W, true);
+    std::vector<int> wmin(static_cast<size_t>(nodes));
+    for (int j = 0; j < nodes; ++j) {
+        const int cl = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)], cr = hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)];
+        wmin[static_cast<size_t>(j)] = std::min({cl, cr, W});
+    }
+    DBuf<int> dwmin, dr(static_cast<size_t>(nodes));
+    dwmin.upload(wmin);
+    k_trunc_rank<<<cdiv(nodes, 128), 128, 0, current().stream>>>(nodes, W, mq.R(), dwmin.get(), rtol, dr.get());
+    HG_LAUNCH();
+    count_launch();
+    std::vector<int> r = dl_int(dr);
+    int rmax = 0;
+    for (int x : r) rmax = std::max(rmax, x);
+    auto Pn = rmax ? make_dvec(static_cast<size_t>(n) * static_cast<size_t>(rmax), true) : nullptr;
+    if (rmax) {
+        // Per child c: Tin_c = Q_M[:, :r] (left child) or P R_M[:r, :]^T (right child).
+        DVec Tin(static_cast<size_t>(2 * nodes) * W * rmax);
+        std::vector<double*> qo;
+        std::vector<i64> ql;
+        for (int j = 0; j < nodes; ++j) {
+            qo.push_back(Tin.get() + i64(2 * j) * W * rmax);
+            ql.push_back(W);
+        }
+        mq.form_q(rmax, nullptr, 0, 0, qo, ql);
+        k_tins<<<nodes, 256, 0, current().stream>>>(W, rmax, dr.get(), mq.R(), mq.perm(), Tin.get());
+        HG_LAUNCH();
+        count_launch();
+        std::vector<double*> out;
+        std::vector<i64> ld;
+        for (int c = 0; c < 2 * nodes; ++c) {
+            out.push_back(Pn->get() + hb[static_cast<size_t>(c)]);
+            ld.push_back(n);
+        }
+        qr.form_q(rmax, Tin.get(), i64(W) * rmax, W, out, ld);
+    }
+    D.R[static_cast<size_t>(l - 1)] = rmax;
+    D.U[static_cast<size_t>(l - 1)] = Pn;
+    D.V[static_cast<size_t>(l - 1)] = Pn;
+    for (int j = 0; j < nodes; ++j) {
+        D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+        D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+    }
+}
+
+/// Y = K X - H X with H restricted to levels < l (peeling), full n x s panels.
+void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y) {
+    const i64 n = H.n();
+    o.apply(j, X, n, s, Y, n);
+    hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0);
+}
+
+}  // namespace
+
+DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
+    static std::mutex mu;
+    static std::map<std::tuple<const DTree*, i64, std::uint64_t>, std::weak_ptr<const DSketchPlan>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(tree.get(), k, seed);
+    auto it = cache.find(key);
+    if (it != cache.end())
+        if (auto sp = it->second.lock()) return sp;
+    auto plan = std::make_shared<DSketchPlan>();
+    plan->tree = tree;
+    plan->k = k;
+    plan->seed = seed;
+    const ClusterTree& t = tree->host;
+    const i64 n = t.size();
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::vector<double> buf(static_cast<size_t>(n) * static_cast<size_t>(k));
+    for (int l = 1; l <= t.depth(); ++l) {
+        std::fill(buf.begin(), buf.end(), 0.0);
+        const auto& kids = t.level(l);
+        for (size_t j = 0; j < t.level(l - 1).size(); ++j) {
+            const Range cr = kids[2 * j + 1];
+            for (i64 i = cr.lo; i < cr.hi; ++i)
+                for (i64 c = 0; c < k; ++c) buf[static_cast<size_t>(i + c * n)] = gauss(rng);
+        }
+        auto d = make_dvec(buf.size(), false);
+        d->upload(buf);
+        sync();  // the host buffer is reused for the next level
+        plan->level.push_back(d);
+    }
+    plan->leaf = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(tree->bmax), true);
+    k_leaf_identity<<<tree->leaves().nseg(), 128, 0, current().stream>>>(tree->leaves().dbounds(), plan->leaf->get(),
+                                                                         n);
+    HG_LAUNCH();
+    count_launch();
+    cache[key] = plan;
+    return plan;
+}
+
+DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& plan, bool with_deriv) {
+    const ClusterTree& T = tree->host;
+    const i64 n = T.size();
+    const int tau = T.depth();
+    const int k = int(kk);
+    if (o.dim() != n) throw std::invalid_argument("build_hodlr: oracle dimension mismatch");
+    if (plan.tree.get() != tree.get() || plan.k != kk)
+        throw std::invalid_argument("build_hodlr: sketch plan not dimensioned for tree");
+    for (int l = 1; l <= tau; ++l) {  // sketch.cpp:115-126
+        const auto& kids = T.level(l);
+        for (size_t j = 0; j < T.level(l - 1).size(); ++j)
+            if (kk > std::min(kids[2 * j].size(), kids[2 * j + 1].size()))
+                throw std::invalid_argument("build_hodlr: rank " + std::to_string(kk) +
+                                            " exceeds block dimension at level " + std::to_string(l));
+    }
+    if (k > 64) throw std::length_error("build_hodlr: rank above 64 not supported");
+    const int p = with_deriv ? o.num_params() : 0;
+    const int kp = k * p;
+    DBuildResult out;
+    out.p = p;
+    out.h = DHodlr::zero(tree);
+    for (int q = 0; q < p; ++q) out.deriv.push_back(DHodlr::zero(tree));
+    auto& ctx = current();
+
+    for (int l = 1; l <= tau; ++l) {
+        const Partition& pc = tree->part(l);
+        const auto& hb = pc.hbounds();
+        const int nodes = 1 << (l - 1);
+        const double* Rs = plan.level[static_cast<size_t>(l - 1)]->get();
+        // Pass 1: Y = K R - H R, dY_j = K_j R - D_j R (sketch.cpp:151-154).
+        DVec Y(static_cast<size_t>(n) * k), dY(static_cast<size_t>(n) * std::max(kp, 1));
+        peel(o, -1, out.h, l - 1, Rs, k, Y.get());
+        for (int q = 0; q < p; ++q) peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, Rs, k, dY.get() + i64(q) * k * n);
+        // Range finder per node (sketch.cpp:156-175).
+        std::vector<int> qmap(static_cast<size_t>(nodes), -1);
+        std::vector<BatchedQR::Block> blocks;
+        for (int j = 0; j < nodes; ++j) {
+            const int m = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
+            if (m == k) continue;
+            qmap[static_cast<size_t>(j)] = int(blocks.size());
+            blocks.push_back({Y.get() + hb[static_cast<size_t>(2 * j)], n, m});
+        }
+        DBuf<int> dqmap;
+        dqmap.upload(qmap);
+        DVec Rn(static_cast<size_t>(nodes) * k * k), sign(static_cast<size_t>(nodes) * k);
+        DBuf<int> perm(static_cast<size_t>(nodes) * k), nr(static_cast<size_t>(nodes));
+        DVec S(static_cast<size_t>(n) * k);
+        S.zero();
+        {
+            std::unique_ptr<BatchedQR> qr;
+            if (!blocks.empty()) {
+                qr = std::make_unique<BatchedQR>(blocks, k, true);
+                std::vector<double*> qo;
+                std::vector<i64> ql;
+                for (int j = 0; j < nodes; ++j)
+                    if (qmap[static_cast<size_t>(j)] >= 0) {
+                        qo.push_back(S.get() + hb[static_cast<size_t>(2 * j)]);
+                        ql.push_back(n);
+                    }
+                qr->form_q(k, nullptr, 0, 0, qo, ql);
+            }
+            DVec dummyR(1);
+            DBuf<int> dummyP(1);
+            k_range_post<<<nodes, 128, 0, ctx.stream>>>(k, dqmap.get(), qr ? qr->R() : dummyR.get(),
+                                                        qr ? qr->perm() : dummyP.get(), Rn.get(), perm.get(),
+                                                        sign.get(), nr.get());
+            HG_LAUNCH();
+            k_q_sign<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, dqmap.get(), sign.get(), S.get(), n);
+            HG_LAUNCH();
+            DVec scratch(static_cast<size_t>(n));
+            k_complete<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, nr.get(), S.get(), n, scratch.get());
+            HG_LAUNCH();
+            ctx.launches += 3;
+        }
+        // Pass 2: Z = K S - H S (sketch.cpp:177-183).
+        DVec Z(static_cast<size_t>(n) * k);
+        peel(o, -1, out.h, l - 1, S.get(), k, Z.get());
+
+        // q2 residual bases (sketch.cpp:194-233).
+        std::vector<int> w2(static_cast<size_t>(nodes), 0);
+        int w2max = 0;
+        DVec S2;
+        DBuf<int> dw2(static_cast<size_t>(nodes));
+        dw2.zero();
+        if (p > 0) {
+            DVec resid(static_cast<size_t>(n) * kp), presc(static_cast<size_t>(nodes)), G(static_cast<size_t>(2 * nodes) * k * kp);
+            panel_axpby(n, kp, 1.0, dY.get(), n, 0.0, resid.get(), n);
+            k_presc<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, p, dY.get(), n, presc.get());
+            HG_LAUNCH();
+            ++ctx.launches;
+            for (int pass = 0; pass < 2; ++pass) {
+                seg_tn(pc, S.get(), n, k, resid.get(), n, kp, G.get(), i64(k) * kp, k);
+                seg_nn(pc, S.get(), n, k, G.get(), i64(k) * kp, k, TMap::same(), resid.get(), n, kp, -1.0, 1.0);
+            }
+            std::vector<BatchedQR::Block> b2;
+            for (int j = 0; j < nodes; ++j)
+                if (qmap[static_cast<size_t>(j)] >= 0)
+                    b2.push_back({resid.get() + hb[static_cast<size_t>(2 * j)], n, hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)]});
+            std::unique_ptr<BatchedQR> qr2;
+            if (!b2.empty()) {
+                qr2 = std::make_unique<BatchedQR>(b2, kp, true);
+                k_w2_nodes<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, pc.dbounds(), k, kp, dqmap.get(), qr2->R(),
+                                                                    presc.get(), dw2.get());
+                HG_LAUNCH();
+                ++ctx.launches;
+                w2 = dw2.download();
+                for (int x : w2) w2max = std::max(w2max, x);
+            }
+            if (w2max > 0) {
+                S2.alloc(static_cast<size_t>(n) * w2max);
+                S2.zero();
+                std::vector<double*> qo;
+                std::vector<i64> ql;
+                for (int j = 0; j < nodes; ++j)
+                    if (qmap[static_cast<size_t>(j)] >= 0) {
+                        qo.push_back(S2.get() + hb[static_cast<size_t>(2 * j)]);
+                        ql.push_back(n);
+                    }
+                qr2->form_q(w2max, nullptr, 0, 0, qo, ql);
+                k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dw2.get(), w2max, S2.get(), n);
+                HG_LAUNCH();
+                ++ctx.launches;
+            }
+        }
+
+        // Differentiated passes (sketch.cpp:236-295) and the commit (:297-311).
+        std::vector<std::vector<int>> rws(static_cast<size_t>(p));
+        for (int q = 0; q < p; ++q) {
+            DVec G(static_cast<size_t>(2 * nodes) * k * k), Om(static_cast<size_t>(nodes) * k * k), ds(static_cast<size_t>(n) * k);
+            DBuf<int> rw(static_cast<size_t>(nodes)), ill(static_cast<size_t>(nodes));
+            const double* dYq = dY.get() + i64(q) * k * n;
+            seg_tn(pc, S.get(), n, k, dYq, n, k, G.get(), i64(k) * k, k);
+            k_diffqr<<<nodes, 64, 0, ctx.stream>>>(k, G.get(), Rn.get(), perm.get(), nr.get(), dqmap.get(), Om.get(),
+                                                   rw.get(), ill.get());
+            HG_LAUNCH();
+            ++ctx.launches;
+            seg_nn(pc, S.get(), n, k, Om.get(), i64(k) * k, k, TMap::parent(0, 0), ds.get(), n, k, 1.0, 0.0);
+            // dZ = K_q S - D_q S + K ds - H ds
+            DVec dZ(static_cast<size_t>(n) * k), tmp(static_cast<size_t>(n) * k);
+            peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S.get(), k, dZ.get());
+            peel(o, -1, out.h, l - 1, ds.get(), k, tmp.get());
+            panel_axpby(n, k, 1.0, tmp.get(), n, 1.0, dZ.get(), n);
+            DVec dZ2;
+            if (w2max > 0) {
+                dZ2.alloc(static_cast<size_t>(n) * w2max);
+                peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S2.get(), w2max, dZ2.get());
+                k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 1, dw2.get(), w2max, dZ2.get(), n);
+                HG_LAUNCH();
+                ++ctx.launches;
+            }
+            // Derivative level panel: [dqc | q | q2] on left rows, [t | dt | dt2] on right rows.
+            const int Wd = 2 * k + w2max;
+            DHodlr& D = out.deriv[static_cast<size_t>(q)];
+            D.set_level(l, Wd, true);
+            double* Pd = D.Ul(l);
+            panel_parity_scale(pc, n, k, ds.get(), n, 1.0, 0.0, Pd, n, 0.0);
+            panel_parity_scale(pc, n, k, Z.get(), n, 0.0, 1.0, Pd, n, 1.0);
+            panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, Pd + i64(k) * n, n, 0.0);
+            panel_parity_scale(pc, n, k, dZ.get(), n, 0.0, 1.0, Pd + i64(k) * n, n, 1.0);
+            if (w2max > 0) {
+                panel_parity_scale(pc, n, w2max, S2.get(), n, 1.0, 0.0, Pd + i64(2 * k) * n, n, 0.0);
+                panel_parity_scale(pc, n, w2max, dZ2.get(), n, 0.0, 1.0, Pd + i64(2 * k) * n, n, 1.0);
+            }
+            for (int j = 0; j < nodes; ++j) {
+                D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
+                D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
+            }
+            rws[static_cast<size_t>(q)] = rw.download();
+            std::vector<int> ic = ill.download();
+            for (int x : ic) out.warnings += x;
+        }
+        // Value level panel: q on left rows, t = Z on right rows.
+        out.h.set_level(l, k, true);
+        panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, out.h.Ul(l), n, 0.0);
+        panel_parity_scale(pc, n, k, Z.get(), n, 0.0, 1.0, out.h.Ul(l), n, 1.0);
+        for (int j = 0; j < nodes; ++j) {
+            out.h.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;
+            out.h.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;
+        }
+        std::vector<int> nrh = nr.download();
+        for (int j = 0; j < nodes; ++j) {
+            out.decisions.push_back(nrh[static_cast<size_t>(j)]);
+            out.decisions.push_back(w2[static_cast<size_t>(j)]);
+            for (int q = 0; q < p; ++q) out.decisions.push_back(rws[static_cast<size_t>(q)][static_cast<size_t>(j)]);
+        }
+    }
+
+    // Leaves (sketch.cpp:314-329): identity-concatenation sampler.
+    {
+        const int bm = tree->bmax;
+        DVec Yl(static_cast<size_t>(n) * bm);
+        peel(o, -1, out.h, tau, plan.leaf->get(), bm, Yl.get());
+        auto to_leaves = [&](DHodlr& h, double* P) {
+            leaves_panel(*tree, h.leaves->get(), P, false);
+            h.leaves_zero = false;
+        };
+        to_leaves(out.h, Yl.get());
+        for (int q = 0; q < p; ++q) {
+            peel(o, q, out.deriv[static_cast<size_t>(q)], tau, plan.leaf->get(), bm, Yl.get());
+            to_leaves(out.deriv[static_cast<size_t>(q)], Yl.get());
+        }
+    }
+    // Recompress every derivative off-diagonal block (sketch.cpp:331-341).
+    for (int q = 0; q < p; ++q)
+        for (int l = 1; l <= tau; ++l) compress_level(out.deriv[static_cast<size_t>(q)], l, 1e-13);
+    return out;
+}
+
+}  // namespace hg

@@ -25,6 +25,7 @@ struct hg_prodrep_s {
 struct hg_oracle_s {
     std::unique_ptr<DOracle> o;
 };
+static_assert(sizeof(hg_apply_fn) == sizeof(ApplyFn), "callback ABI");
 struct hg_build_s {
     DBuildResult r;
 };
@@ -85,10 +86,10 @@ struct Staged {
             ld = ldp;
             return;
         }
-        buf.alloc(size_t(rows) * size_t(s));
+        buf.alloc(static_cast<size_t>(rows) * static_cast<size_t>(s));
         if (rows * s)
-            HG_CUDA(cudaMemcpy2DAsync(buf.get(), size_t(rows) * sizeof(double), p, size_t(ldp) * sizeof(double),
-                                      size_t(rows) * sizeof(double), size_t(s), cudaMemcpyHostToDevice,
+            HG_CUDA(cudaMemcpy2DAsync(buf.get(), static_cast<size_t>(rows) * sizeof(double), p, static_cast<size_t>(ldp) * sizeof(double),
+                                      static_cast<size_t>(rows) * sizeof(double), static_cast<size_t>(s), cudaMemcpyHostToDevice,
                                       current().stream));
         ptr = buf.get();
         ld = rows;
@@ -107,15 +108,15 @@ struct Output {
             ld = ldp;
             return;
         }
-        buf.alloc(size_t(r) * size_t(cols));
+        buf.alloc(static_cast<size_t>(r) * static_cast<size_t>(cols));
         dptr = buf.get();
         ld = r;
         host = p;
     }
     void finish() {
         if (host && rows * s)
-            HG_CUDA(cudaMemcpy2DAsync(host, size_t(ldh) * sizeof(double), dptr, size_t(rows) * sizeof(double),
-                                      size_t(rows) * sizeof(double), size_t(s), cudaMemcpyDeviceToHost,
+            HG_CUDA(cudaMemcpy2DAsync(host, static_cast<size_t>(ldh) * sizeof(double), dptr, static_cast<size_t>(rows) * sizeof(double),
+                                      static_cast<size_t>(rows) * sizeof(double), static_cast<size_t>(s), cudaMemcpyDeviceToHost,
                                       current().stream));
         sync();
     }
@@ -192,8 +193,8 @@ hg_status hg_kd_ordering(int64_t n, int d, const double* coords, int64_t leaf_mi
     return guard(nullptr, [&] {
         KdOrdering kd = build_kd_ordering(coords, n, d, leaf_min, leaf_max);
         for (int64_t i = 0; i < n; ++i) {
-            perm[i] = kd.perm[size_t(i)];
-            inv[i] = kd.inv[size_t(i)];
+            perm[i] = kd.perm[static_cast<size_t>(i)];
+            inv[i] = kd.inv[static_cast<size_t>(i)];
         }
         *tau = kd.tree.depth();
     });
@@ -266,18 +267,18 @@ hg_status hg_hodlr_sub_matvec(hg_ctx_t ctx, hg_hodlr_t h, int d, int64_t node, c
         const auto& tree = h->h.tree->host;
         if (d < 0 || d > tree.depth() || node < 0 || node >= i64(tree.level(d).size()))
             throw std::invalid_argument("sub_matvec: node out of range");
-        const Range r = tree.level(d)[size_t(node)];
+        const Range r = tree.level(d)[static_cast<size_t>(node)];
         const i64 n = h->h.n();
         Staged x(X, ldx, r.size(), s, loc);
-        DVec full(size_t(n) * size_t(s)), yf(size_t(n) * size_t(s));
+        DVec full(static_cast<size_t>(n) * static_cast<size_t>(s)), yf(static_cast<size_t>(n) * static_cast<size_t>(s));
         full.zero();
-        HG_CUDA(cudaMemcpy2DAsync(full.get() + r.lo, size_t(n) * sizeof(double), x.ptr, size_t(x.ld) * sizeof(double),
-                                  size_t(r.size()) * sizeof(double), size_t(s), cudaMemcpyDeviceToDevice,
+        HG_CUDA(cudaMemcpy2DAsync(full.get() + r.lo, static_cast<size_t>(n) * sizeof(double), x.ptr, static_cast<size_t>(x.ld) * sizeof(double),
+                                  static_cast<size_t>(r.size()) * sizeof(double), static_cast<size_t>(s), cudaMemcpyDeviceToDevice,
                                   current().stream));
         hodlr_apply(h->h, full.get(), n, int(s), yf.get(), n, d + 1, h->h.tau(), true, transpose != 0, 0.0);
         Output y(Y, ldy, r.size(), s, loc);
-        HG_CUDA(cudaMemcpy2DAsync(y.dptr, size_t(y.ld) * sizeof(double), yf.get() + r.lo, size_t(n) * sizeof(double),
-                                  size_t(r.size()) * sizeof(double), size_t(s), cudaMemcpyDeviceToDevice,
+        HG_CUDA(cudaMemcpy2DAsync(y.dptr, static_cast<size_t>(y.ld) * sizeof(double), yf.get() + r.lo, static_cast<size_t>(n) * sizeof(double),
+                                  static_cast<size_t>(r.size()) * sizeof(double), static_cast<size_t>(s), cudaMemcpyDeviceToDevice,
                                   current().stream));
         y.finish();
     });
@@ -311,8 +312,8 @@ hg_status hg_factor_solve(hg_ctx_t ctx, hg_factor_t f, const double* B, int64_t 
         if (ldb < n || ldx < n) throw std::invalid_argument("solve: dimension mismatch");
         Output y(X, ldx, n, s, loc);
         if (!(loc == HG_DEVICE && B == X && ldb == ldx))
-            HG_CUDA(cudaMemcpy2DAsync(y.dptr, size_t(y.ld) * sizeof(double), B, size_t(ldb) * sizeof(double),
-                                      size_t(n) * sizeof(double), size_t(s),
+            HG_CUDA(cudaMemcpy2DAsync(y.dptr, static_cast<size_t>(y.ld) * sizeof(double), B, static_cast<size_t>(ldb) * sizeof(double),
+                                      static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(s),
                                       loc == HG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                       current().stream));
         factor_solve(f->f, y.dptr, y.ld, int(s));
@@ -376,6 +377,165 @@ hg_status hg_trace_quad(hg_ctx_t ctx, hg_factor_t fa, hg_hodlr_t b, hg_factor_t 
         DProductRep p = pipeline(fa->f, b->h, true);
         DProductRep q = pipeline(fc->f, d->h, true);
         *out = scalar_result([&](double* x) { trace_pair(p, q, x, false); });
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// ------------------------------------------------------------------ oracle
+hg_status hg_oracle_dense(hg_ctx_t ctx, int64_t n, const double* K, int p, const double* dK, hg_oracle_t* out) {
+    return guard(ctx, [&] { *out = new hg_oracle_s{make_dense_oracle(n, K, p, dK)}; });
+}
+
+hg_status hg_oracle_matern(hg_ctx_t ctx, int64_t n, const double* x, int nu2, double sigma2, double ell,
+                           double nugget, int scan, hg_oracle_t* out) {
+    return guard(ctx, [&] { *out = new hg_oracle_s{make_matern_oracle(n, x, nu2, sigma2, ell, nugget, scan != 0)}; });
+}
+
+hg_status hg_oracle_callback(hg_ctx_t ctx, int64_t n, int p, hg_apply_fn fn, void* user, hg_oracle_t* out) {
+    return guard(ctx, [&] { *out = new hg_oracle_s{make_callback_oracle(n, p, reinterpret_cast<ApplyFn>(fn), user)}; });
+}
+
+hg_status hg_oracle_set_parameters(hg_oracle_t o, const double* theta, int p) {
+    return guard(nullptr, [&] { o->o->set_parameters(theta, p); });
+}
+
+hg_status hg_oracle_free(hg_oracle_t o) {
+    delete o;
+    return HG_OK;
+}
+
+hg_status hg_oracle_apply(hg_ctx_t ctx, hg_oracle_t o, int j, const double* V, int64_t ldv, int64_t s, double* Y,
+                          int64_t ldy, int loc) {
+    return guard(ctx, [&] {
+        const i64 n = o->o->dim();
+        if (ldv < n || ldy < n) throw std::invalid_argument("oracle apply: dimension mismatch");
+        Staged v(V, ldv, n, s, loc);
+        Output y(Y, ldy, n, s, loc);
+        o->o->apply(j, v.ptr, v.ld, int(s), y.dptr, y.ld);
+        y.finish();
+    });
+}
+
+hg_status hg_oracle_counters(hg_oracle_t o, uint64_t* apply_columns, uint64_t* derivative_columns, int reset) {
+    *apply_columns = o->o->apply_columns();
+    *derivative_columns = o->o->derivative_columns();
+    if (reset) o->o->reset_counters();
+    return HG_OK;
+}
+
+// ------------------------------------------------------------------- build
+hg_status hg_build(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, int with_derivatives,
+                   hg_build_t* out) {
+    return guard(ctx, [&] {
+        DTreeP tree = get_tree(o->o->dim(), tau);
+        DSketchPlanP plan = get_plan(tree, k, seed);
+        *out = new hg_build_s{build(*o->o, tree, k, *plan, with_derivatives != 0)};
+        sync();
+    });
+}
+
+hg_status hg_build_free(hg_build_t b) {
+    delete b;
+    return HG_OK;
+}
+
+hg_status hg_build_h(hg_build_t b, hg_hodlr_t* out) {
+    return guard(nullptr, [&] { *out = new hg_hodlr_s{b->r.h}; });
+}
+
+hg_status hg_build_deriv(hg_build_t b, int j, hg_hodlr_t* out) {
+    return guard(nullptr, [&] {
+        if (j < 0 || j >= int(b->r.deriv.size())) throw std::invalid_argument("build_deriv: index");
+        *out = new hg_hodlr_s{b->r.deriv[static_cast<size_t>(j)]};
+    });
+}
+
+int hg_build_num_warnings(hg_build_t b) { return b->r.warnings; }
+
+int hg_build_decisions(hg_build_t b, int p, int64_t* out) {
+    const int stride = 2 + b->r.p;
+    const size_t cnt = b->r.decisions.size() / static_cast<size_t>(stride);
+    for (size_t i = 0; i < cnt; ++i)
+        for (int c = 0; c < 2 + p; ++c)
+            out[i * static_cast<size_t>(2 + p) + static_cast<size_t>(c)] = c < stride ? b->r.decisions[i * static_cast<size_t>(stride) + static_cast<size_t>(c)] : 0;
+    return int(cnt);
+}
+
+// --------------------------------------------------------------------- mle
+namespace {
+DVec residual(const double* y, const double* ybar, i64 n) {
+    std::vector<double> r(y, y + n);
+    if (ybar)
+        for (i64 i = 0; i < n; ++i) r[static_cast<size_t>(i)] -= ybar[i];
+    DVec d;
+    d.upload(r);
+    return d;
+}
+}  // namespace
+
+hg_status hg_log_likelihood(hg_ctx_t ctx, hg_factor_t f, const double* y, const double* ybar, double* out) {
+    return guard(ctx, [&] {
+        DVec r = residual(y, ybar, f->f.n());
+        *out = log_likelihood(f->f, r.get());
+    });
+}
+
+hg_status hg_score(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, const double* y, const double* ybar,
+                   double* out) {
+    return guard(ctx, [&] {
+        DVec r = residual(y, ybar, f->f.n());
+        std::vector<const DHodlr*> d;
+        for (int j = 0; j < p; ++j) d.push_back(&deriv[j]->h);
+        auto s = score(f->f, d, r.get(), nullptr);
+        for (int j = 0; j < p; ++j) out[j] = s[static_cast<size_t>(j)];
+    });
+}
+
+hg_status hg_fisher_information(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, double* out) {
+    return guard(ctx, [&] {
+        std::vector<DProductRep> reps;
+        for (int j = 0; j < p; ++j) reps.push_back(pipeline(f->f, deriv[j]->h, true));
+        auto fi = fisher_from_reps(reps);
+        for (size_t i = 0; i < fi.size(); ++i) out[i] = fi[i];
+    });
+}
+
+hg_status hg_mle_iteration(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
+                           double* loglik, double* score_out, double* fisher, double* times) {
+    return guard(ctx, [&] {
+        auto& c = current();
+        const i64 n = o->o->dim();
+        DTreeP tree = get_tree(n, tau);
+        DSketchPlanP plan = get_plan(tree, k, seed);
+        cudaEvent_t ev[6];
+        for (auto& e : ev) HG_CUDA(cudaEventCreate(&e));
+        DVec r = residual(y, nullptr, n);
+        HG_CUDA(cudaEventRecord(ev[0], c.stream));
+        DBuildResult br = build(*o->o, tree, k, *plan, true);
+        HG_CUDA(cudaEventRecord(ev[1], c.stream));
+        DFactor f = factorize(br.h, HG_LEFT);
+        HG_CUDA(cudaEventRecord(ev[2], c.stream));
+        *loglik = log_likelihood(f, r.get());
+        HG_CUDA(cudaEventRecord(ev[3], c.stream));
+        std::vector<const DHodlr*> d;
+        for (auto& x : br.deriv) d.push_back(&x);
+        std::vector<DProductRep> reps;
+        auto s = score(f, d, r.get(), &reps);
+        for (size_t j = 0; j < s.size(); ++j) score_out[j] = s[j];
+        HG_CUDA(cudaEventRecord(ev[4], c.stream));
+        auto fi = fisher_from_reps(reps);
+        for (size_t i = 0; i < fi.size(); ++i) fisher[i] = fi[i];
+        HG_CUDA(cudaEventRecord(ev[5], c.stream));
+        HG_CUDA(cudaEventSynchronize(ev[5]));
+        for (int i = 0; i < 5; ++i) {
+            float ms = 0;
+            HG_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            times[i] = ms * 1e-3;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 

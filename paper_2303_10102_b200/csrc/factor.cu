@@ -447,11 +447,11 @@ void cap_solve(const DFactor& f, int i, const double* Q, bool top_odd, bool tran
     const int R = f.Rl(i), m = 2 * R;
     const int nodes = 1 << (i - 1);
     int thr = 64;
-    while (thr > 8 && size_t(m) * thr * sizeof(double) > SMEM_CAP) thr >>= 1;
-    const size_t smem = size_t(m) * thr * sizeof(double);
+    while (thr > 8 && static_cast<size_t>(m) * thr * sizeof(double) > SMEM_CAP) thr >>= 1;
+    const size_t smem = static_cast<size_t>(m) * thr * sizeof(double);
     if (smem > SMEM_CAP) throw std::length_error("cap_solve: capacitance too large for shared memory");
     set_smem(reinterpret_cast<const void*>(k_cap_solve), smem);
-    CapSolveArgs g{R, w, f.cap[size_t(i - 1)]->get(), f.cap_piv[size_t(i - 1)]->get(), Q, top_odd ? 1 : 0,
+    CapSolveArgs g{R, w, f.cap[static_cast<size_t>(i - 1)]->get(), f.cap_piv[static_cast<size_t>(i - 1)]->get(), Q, top_odd ? 1 : 0,
                    trans ? 1 : 0, T};
     dim3 grid(unsigned(nodes), unsigned(cdiv(w, thr)));
     k_cap_solve<<<grid, thr, smem, current().stream>>>(g);
@@ -465,7 +465,7 @@ void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) {
     if (w <= 0) return;
     const Partition& lv = f.tree->leaves();
     const int m = lv.max_seg();
-    const size_t smem = (size_t(m) * (SOLVE_COLS + 1) + 16 * size_t(m + 1)) * sizeof(double);
+    const size_t smem = (static_cast<size_t>(m) * (SOLVE_COLS + 1) + 16 * static_cast<size_t>(m + 1)) * sizeof(double);
     set_smem(reinterpret_cast<const void*>(k_leaf_solve), smem);
     LeafSolveArgs g{lv.dbounds(), f.bmax(), f.leaf_fac->get(), f.leaf_kind->get(), f.leaf_piv->get(), Y, ldy, w};
     dim3 grid(unsigned(lv.nseg()), unsigned(cdiv(w, SOLVE_COLS)));
@@ -479,8 +479,8 @@ void level_inverse(const DFactor& f, int i, bool transposed, double* Y, i64 ldy,
     if (R == 0 || w <= 0) return;
     const Partition& p = f.tree->part(i);
     const i64 n = f.n();
-    DVec Q(size_t(p.nseg()) * size_t(R) * size_t(w));
-    DVec T(size_t(p.nseg() / 2) * size_t(2 * R) * size_t(w));
+    DVec Q(static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(w));
+    DVec T(static_cast<size_t>(p.nseg() / 2) * static_cast<size_t>(2 * R) * static_cast<size_t>(w));
     if (!transposed) {
         seg_tn(p, f.Fl(i), n, R, Y, ldy, w, Q.get(), i64(R) * w, R);
         cap_solve(f, i, Q.get(), true, false, T.get(), w);
@@ -505,25 +505,25 @@ DFactor factorize(const DHodlr& h, int orient) {
     const int tau = h.tau();
     const i64 n = h.n();
     f.R = h.R;
-    f.off.assign(size_t(tau), 0);
+    f.off.assign(static_cast<size_t>(tau), 0);
     for (int l = 1; l <= tau; ++l) {
-        f.off[size_t(l - 1)] = f.sumR;
-        f.sumR += f.R[size_t(l - 1)];
+        f.off[static_cast<size_t>(l - 1)] = f.sumR;
+        f.sumR += f.R[static_cast<size_t>(l - 1)];
     }
     // Source factors (factorization.cpp:75-96): w = upper.left on left-child
     // rows, x = upper.right on right-child rows.
-    f.F.assign(size_t(tau), nullptr);
+    f.F.assign(static_cast<size_t>(tau), nullptr);
     for (int l = 1; l <= tau; ++l) {
         const int R = f.Rl(l);
         if (!R) continue;
         if (h.sym) {
-            f.F[size_t(l - 1)] = h.U[size_t(l - 1)];
+            f.F[static_cast<size_t>(l - 1)] = h.U[static_cast<size_t>(l - 1)];
         } else {
-            auto P = make_dvec(size_t(n) * size_t(R), false);
+            auto P = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(R), false);
             const Partition& p = h.tree->part(l);
             panel_parity_scale(p, n, R, h.Ul(l), n, 1.0, 0.0, P->get(), n, 0.0);
             panel_parity_scale(p, n, R, h.Vl(l), n, 0.0, 1.0, P->get(), n, 1.0);
-            f.F[size_t(l - 1)] = P;
+            f.F[static_cast<size_t>(l - 1)] = P;
         }
     }
     // Leaves (factorization.cpp:68-72).
@@ -532,12 +532,12 @@ DFactor factorize(const DHodlr& h, int orient) {
     if (bm > MAX_LEAF) throw std::length_error("factorize: leaf size above 320 not supported");
     f.leaf_mat = h.leaves;
     f.leaf_fac = make_dvec(h.leaves->size(), true);
-    f.leaf_kind = std::make_shared<DBuf<int>>(size_t(nl));
-    f.leaf_piv = std::make_shared<DBuf<int>>(size_t(nl) * size_t(bm));
-    f.leaf_ld = make_dvec(size_t(nl), false);
-    f.leaf_sign = std::make_shared<DBuf<int>>(size_t(nl));
+    f.leaf_kind = std::make_shared<DBuf<int>>(static_cast<size_t>(nl));
+    f.leaf_piv = std::make_shared<DBuf<int>>(static_cast<size_t>(nl) * static_cast<size_t>(bm));
+    f.leaf_ld = make_dvec(static_cast<size_t>(nl), false);
+    f.leaf_sign = std::make_shared<DBuf<int>>(static_cast<size_t>(nl));
     {
-        const size_t smem = size_t(bm) * bm * sizeof(double);
+        const size_t smem = static_cast<size_t>(bm) * bm * sizeof(double);
         const int use = smem <= SMEM_CAP ? 1 : 0;
         if (use) set_smem(reinterpret_cast<const void*>(k_leaf_factor), smem);
         LeafFacArgs g{lv.dbounds(), bm, h.leaves->get(), f.leaf_fac->get(), h.sym ? 1 : 0, use,
@@ -547,34 +547,34 @@ DFactor factorize(const DHodlr& h, int orient) {
         count_launch();
     }
     // Working left factors (factorization.cpp:75-119): Wbar = Abar^{-1} F.
-    f.Wbar = make_dvec(size_t(n) * size_t(std::max(f.sumR, 1)), false);
+    f.Wbar = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(f.sumR, 1)), false);
     for (int l = 1; l <= tau; ++l)
         if (f.Rl(l)) panel_axpby(n, f.Rl(l), 1.0, f.Fl(l), n, 0.0, f.Wl(l), n);
     leaf_solve(f, f.Wbar->get(), n, f.sumR);
     // Levels tau..1 (factorization.cpp:121-166).
-    f.cap.assign(size_t(tau), nullptr);
-    f.cap_piv.assign(size_t(tau), nullptr);
-    f.cap_ld.assign(size_t(tau), nullptr);
-    f.cap_sign.assign(size_t(tau), nullptr);
+    f.cap.assign(static_cast<size_t>(tau), nullptr);
+    f.cap_piv.assign(static_cast<size_t>(tau), nullptr);
+    f.cap_ld.assign(static_cast<size_t>(tau), nullptr);
+    f.cap_sign.assign(static_cast<size_t>(tau), nullptr);
     for (int i = tau; i >= 1; --i) {
         const int R = f.Rl(i), m = 2 * R, nodes = 1 << (i - 1);
         if (R == 0) continue;
         const Partition& p = h.tree->part(i);
-        DVec P(size_t(p.nseg()) * size_t(R) * size_t(R));
+        DVec P(static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(R));
         seg_tn(p, f.Fl(i), n, R, f.Wl(i), n, R, P.get(), i64(R) * R, R);
-        f.cap[size_t(i - 1)] = make_dvec(size_t(nodes) * size_t(m) * size_t(m), false);
-        f.cap_piv[size_t(i - 1)] = std::make_shared<DBuf<int>>(size_t(nodes) * size_t(m));
-        f.cap_ld[size_t(i - 1)] = make_dvec(size_t(nodes), false);
-        f.cap_sign[size_t(i - 1)] = std::make_shared<DBuf<int>>(size_t(nodes));
-        const size_t smem = size_t(m) * m * sizeof(double);
+        f.cap[static_cast<size_t>(i - 1)] = make_dvec(static_cast<size_t>(nodes) * static_cast<size_t>(m) * static_cast<size_t>(m), false);
+        f.cap_piv[static_cast<size_t>(i - 1)] = std::make_shared<DBuf<int>>(static_cast<size_t>(nodes) * static_cast<size_t>(m));
+        f.cap_ld[static_cast<size_t>(i - 1)] = make_dvec(static_cast<size_t>(nodes), false);
+        f.cap_sign[static_cast<size_t>(i - 1)] = std::make_shared<DBuf<int>>(static_cast<size_t>(nodes));
+        const size_t smem = static_cast<size_t>(m) * m * sizeof(double);
         const int use = smem <= SMEM_CAP ? 1 : 0;
         if (use) set_smem(reinterpret_cast<const void*>(k_cap_lu), smem);
-        CapLuArgs g{R, P.get(), f.cap[size_t(i - 1)]->get(), f.cap_piv[size_t(i - 1)]->get(),
-                    f.cap_ld[size_t(i - 1)]->get(), f.cap_sign[size_t(i - 1)]->get(), use};
+        CapLuArgs g{R, P.get(), f.cap[static_cast<size_t>(i - 1)]->get(), f.cap_piv[static_cast<size_t>(i - 1)]->get(),
+                    f.cap_ld[static_cast<size_t>(i - 1)]->get(), f.cap_sign[static_cast<size_t>(i - 1)]->get(), use};
         k_cap_lu<<<unsigned(nodes), FNT, use ? smem : 0, current().stream>>>(g);
         HG_LAUNCH();
         count_launch();
-        if (i > 1 && f.off[size_t(i - 1)] > 0) level_inverse(f, i, false, f.Wbar->get(), n, f.off[size_t(i - 1)]);
+        if (i > 1 && f.off[static_cast<size_t>(i - 1)] > 0) level_inverse(f, i, false, f.Wbar->get(), n, f.off[static_cast<size_t>(i - 1)]);
     }
     return f;
 }
@@ -598,9 +598,9 @@ double factor_logdet(const DFactor& f) {
         ld += lld[b];
     }
     for (int i = 1; i <= f.tau(); ++i) {
-        if (!f.cap[size_t(i - 1)]) continue;
-        std::vector<double> cl = f.cap_ld[size_t(i - 1)]->download();
-        std::vector<int> cs = f.cap_sign[size_t(i - 1)]->download();
+        if (!f.cap[static_cast<size_t>(i - 1)]) continue;
+        std::vector<double> cl = f.cap_ld[static_cast<size_t>(i - 1)]->download();
+        std::vector<int> cs = f.cap_sign[static_cast<size_t>(i - 1)]->download();
         for (size_t j = 0; j < cl.size(); ++j) {
             if (cs[j] <= 0) throw NotPositiveDefinite("capacitance has non-positive determinant");
             ld += cl[j];

@@ -35,9 +35,9 @@ struct DFactor {
     int tau() const { return tree->tau(); }
     int bmax() const { return tree->bmax; }
     i64 lstride() const { return i64(bmax()) * bmax(); }
-    double* Fl(int l) const { return F[size_t(l - 1)] ? F[size_t(l - 1)]->get() : nullptr; }
-    double* Wl(int l) const { return Wbar->get() + i64(off[size_t(l - 1)]) * n(); }
-    int Rl(int l) const { return R[size_t(l - 1)]; }
+    double* Fl(int l) const { return F[static_cast<size_t>(l - 1)] ? F[static_cast<size_t>(l - 1)]->get() : nullptr; }
+    double* Wl(int l) const { return Wbar->get() + i64(off[static_cast<size_t>(l - 1)]) * n(); }
+    int Rl(int l) const { return R[static_cast<size_t>(l - 1)]; }
 };
 
 /// factorization.cpp:62-168

@@ -6,30 +6,19 @@
 // with a one-step register prefetch. Split-K partials are reduced in a fixed
 // order so every result is bitwise reproducible run to run.
 #include "kernels.cuh"
+#include "tile.cuh"
 
 namespace hg {
 
 namespace {
 
-constexpr int TM = 64, TN = 64, KS = 16, NT = 256;
+using tile::KS;
+using tile::NT;
+using tile::TM;
+using tile::TN;
+using tile::mma16;
 constexpr int SEG_CHUNK = 512;  // rows per split-K work item
 constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
-
-__device__ __forceinline__ void mma16(const double (&As)[KS][TM + 1], const double (&Bs)[KS][TN + 1],
-                                      double (&acc)[4][4], int tm, int tn) {
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-}
 
 // ------------------------------------------------------------------ seg_tn
 struct SegTnArgs {
@@ -385,7 +374,7 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
         return;
     }
     const i64 wstride = i64(ca) * cb;
-    DVec ws(size_t(wstride) * size_t(tl.count));
+    DVec ws(static_cast<size_t>(wstride) * static_cast<size_t>(tl.count));
     g.out = ws.get();
     g.ostride = wstride;
     g.ldo = ca;

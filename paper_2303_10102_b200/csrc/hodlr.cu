@@ -29,23 +29,44 @@ __global__ void k_leaf_ggt(const int* bounds, int bmax, const double* g, double*
     }
 }
 
+__global__ void k_leaves_panel(const int* bounds, int bmax, double* leaves, double* P, i64 ldp, int to_panel) {
+    const int b = blockIdx.x;
+    const int lo = bounds[b], m = bounds[b + 1] - lo;
+    double* L = leaves + i64(b) * bmax * bmax;
+    for (int e = threadIdx.x; e < m * bmax; e += blockDim.x) {
+        const int r = e % m, c = e / m;
+        if (to_panel)
+            P[i64(lo + r) + i64(c) * ldp] = c < m ? L[r + i64(c) * bmax] : 0.0;
+        else if (c < m)
+            L[r + i64(c) * bmax] = P[i64(lo + r) + i64(c) * ldp];
+    }
+}
+
 }  // namespace
+
+void leaves_panel(const DTree& t, double* leaves, double* P, bool to_panel) {
+    const Partition& lv = t.leaves();
+    k_leaves_panel<<<unsigned(lv.nseg()), 256, 0, current().stream>>>(lv.dbounds(), t.bmax, leaves, P, t.n(),
+                                                                       to_panel ? 1 : 0);
+    HG_LAUNCH();
+    count_launch();
+}
 
 DHodlr DHodlr::zero(DTreeP t, bool symmetric) {
     DHodlr h;
     h.tree = t;
     h.sym = symmetric;
     const int tau = t->tau();
-    h.R.assign(size_t(tau), 0);
-    h.U.assign(size_t(tau), nullptr);
-    h.V.assign(size_t(tau), nullptr);
-    h.rank_up.resize(size_t(tau));
-    h.rank_lo.resize(size_t(tau));
+    h.R.assign(static_cast<size_t>(tau), 0);
+    h.U.assign(static_cast<size_t>(tau), nullptr);
+    h.V.assign(static_cast<size_t>(tau), nullptr);
+    h.rank_up.resize(static_cast<size_t>(tau));
+    h.rank_lo.resize(static_cast<size_t>(tau));
     for (int l = 1; l <= tau; ++l) {
-        h.rank_up[size_t(l - 1)].assign(size_t(1) << (l - 1), 0);
-        h.rank_lo[size_t(l - 1)].assign(size_t(1) << (l - 1), 0);
+        h.rank_up[static_cast<size_t>(l - 1)].assign(static_cast<size_t>(1) << (l - 1), 0);
+        h.rank_lo[static_cast<size_t>(l - 1)].assign(static_cast<size_t>(1) << (l - 1), 0);
     }
-    h.leaves = make_dvec(size_t(t->leaves().nseg()) * size_t(h.lstride()), true);
+    h.leaves = make_dvec(static_cast<size_t>(t->leaves().nseg()) * static_cast<size_t>(h.lstride()), true);
     h.leaves_zero = true;
     return h;
 }
@@ -55,17 +76,17 @@ DHodlr DHodlr::identity(DTreeP t) {
     std::vector<double> lv(h.leaves->size(), 0.0);
     const auto& hb = t->leaves().hbounds();
     for (int b = 0; b < t->leaves().nseg(); ++b)
-        for (int i = 0; i < hb[size_t(b + 1)] - hb[size_t(b)]; ++i)
-            lv[size_t(b) * size_t(h.lstride()) + size_t(i) * size_t(h.bmax() + 1)] = 1.0;
+        for (int i = 0; i < hb[static_cast<size_t>(b + 1)] - hb[static_cast<size_t>(b)]; ++i)
+            lv[static_cast<size_t>(b) * static_cast<size_t>(h.lstride()) + static_cast<size_t>(i) * static_cast<size_t>(h.bmax() + 1)] = 1.0;
     h.leaves->upload(lv);
     h.leaves_zero = false;
     return h;
 }
 
 void DHodlr::set_level(int l, int r, bool symmetric_panel) {
-    R[size_t(l - 1)] = r;
-    U[size_t(l - 1)] = r ? make_dvec(size_t(n()) * size_t(r), true) : nullptr;
-    V[size_t(l - 1)] = symmetric_panel ? U[size_t(l - 1)] : (r ? make_dvec(size_t(n()) * size_t(r), true) : nullptr);
+    R[static_cast<size_t>(l - 1)] = r;
+    U[static_cast<size_t>(l - 1)] = r ? make_dvec(static_cast<size_t>(n()) * static_cast<size_t>(r), true) : nullptr;
+    V[static_cast<size_t>(l - 1)] = symmetric_panel ? U[static_cast<size_t>(l - 1)] : (r ? make_dvec(static_cast<size_t>(n()) * static_cast<size_t>(r), true) : nullptr);
 }
 
 // hodlr_matrix.cpp:126-172
@@ -81,28 +102,28 @@ DHodlr DHodlr::random(DTreeP t, i64 k, std::uint64_t seed, bool spd) {
         int Rl = 0;
         for (size_t j = 0; j < nodes; ++j)
             Rl = std::max<int>(Rl, int(std::min({k, kids[2 * j].size(), kids[2 * j + 1].size()})));
-        std::vector<double> P(size_t(n) * size_t(Rl), 0.0);
+        std::vector<double> P(static_cast<size_t>(n) * static_cast<size_t>(Rl), 0.0);
         for (size_t j = 0; j < nodes; ++j) {
             const Range cl = kids[2 * j], cr = kids[2 * j + 1];
             const i64 r = std::min({k, cl.size(), cr.size()});
             const double s1 = std::sqrt(double(cl.size())), s2 = std::sqrt(double(cr.size()));
             for (i64 i = 0; i < cl.size(); ++i)
-                for (i64 c = 0; c < r; ++c) P[size_t(cl.lo + i + c * n)] = gauss(rng) / s1;
+                for (i64 c = 0; c < r; ++c) P[static_cast<size_t>(cl.lo + i + c * n)] = gauss(rng) / s1;
             for (i64 i = 0; i < cr.size(); ++i)
-                for (i64 c = 0; c < r; ++c) P[size_t(cr.lo + i + c * n)] = gauss(rng) / s2;
-            h.rank_up[size_t(l - 1)][j] = int(r);
-            h.rank_lo[size_t(l - 1)][j] = int(r);
+                for (i64 c = 0; c < r; ++c) P[static_cast<size_t>(cr.lo + i + c * n)] = gauss(rng) / s2;
+            h.rank_up[static_cast<size_t>(l - 1)][j] = int(r);
+            h.rank_lo[static_cast<size_t>(l - 1)][j] = int(r);
         }
         h.set_level(l, Rl, true);
-        if (Rl) h.U[size_t(l - 1)]->upload(P);
+        if (Rl) h.U[static_cast<size_t>(l - 1)]->upload(P);
     }
     const int bmax = h.bmax();
     std::vector<double> G(h.leaves->size(), 0.0);
     for (i64 b = 0; b < tree.num_leaves(); ++b) {
-        const i64 m = tree.leaves()[size_t(b)].size();
+        const i64 m = tree.leaves()[static_cast<size_t>(b)].size();
         const double sm = std::sqrt(double(m));
         for (i64 i = 0; i < m; ++i)
-            for (i64 j = 0; j < m; ++j) G[size_t(b * h.lstride() + i + j * bmax)] = gauss(rng) / sm;
+            for (i64 j = 0; j < m; ++j) G[static_cast<size_t>(b * h.lstride() + i + j * bmax)] = gauss(rng) / sm;
     }
     DVec g;
     g.upload(G);
@@ -124,27 +145,27 @@ DHodlr DHodlr::import_panels(DTreeP t, bool symmetric, const int* R, const doubl
         const int Rl = R[l - 1];
         h.set_level(l, Rl, symmetric);
         if (Rl) {
-            h.U[size_t(l - 1)]->upload(flat + off, size_t(n) * size_t(Rl));
-            if (!symmetric) h.V[size_t(l - 1)]->upload(flat + off + size_t(n) * size_t(Rl), size_t(n) * size_t(Rl));
+            h.U[static_cast<size_t>(l - 1)]->upload(flat + off, static_cast<size_t>(n) * static_cast<size_t>(Rl));
+            if (!symmetric) h.V[static_cast<size_t>(l - 1)]->upload(flat + off + static_cast<size_t>(n) * static_cast<size_t>(Rl), static_cast<size_t>(n) * static_cast<size_t>(Rl));
         }
-        off += 2 * size_t(n) * size_t(Rl);
-        for (size_t j = 0; j < h.rank_up[size_t(l - 1)].size(); ++j, ++node) {
-            h.rank_up[size_t(l - 1)][j] = ranks_up[node];
-            h.rank_lo[size_t(l - 1)][j] = symmetric ? ranks_up[node] : ranks_lo[node];
+        off += 2 * static_cast<size_t>(n) * static_cast<size_t>(Rl);
+        for (size_t j = 0; j < h.rank_up[static_cast<size_t>(l - 1)].size(); ++j, ++node) {
+            h.rank_up[static_cast<size_t>(l - 1)][j] = ranks_up[node];
+            h.rank_lo[static_cast<size_t>(l - 1)][j] = symmetric ? ranks_up[node] : ranks_lo[node];
         }
     }
     const auto& hb = t->leaves().hbounds();
     std::vector<double> lv(h.leaves->size(), 0.0);
     bool allzero = true;
     for (int b = 0; b < t->leaves().nseg(); ++b) {
-        const int m = hb[size_t(b + 1)] - hb[size_t(b)];
+        const int m = hb[static_cast<size_t>(b + 1)] - hb[static_cast<size_t>(b)];
         for (int j = 0; j < m; ++j)
             for (int i = 0; i < m; ++i) {
-                double v = flat[off + size_t(i) + size_t(j) * size_t(m)];
-                lv[size_t(b) * size_t(h.lstride()) + size_t(i) + size_t(j) * size_t(h.bmax())] = v;
+                double v = flat[off + static_cast<size_t>(i) + static_cast<size_t>(j) * static_cast<size_t>(m)];
+                lv[static_cast<size_t>(b) * static_cast<size_t>(h.lstride()) + static_cast<size_t>(i) + static_cast<size_t>(j) * static_cast<size_t>(h.bmax())] = v;
                 if (v != 0.0) allzero = false;
             }
-        off += size_t(m) * size_t(m);
+        off += static_cast<size_t>(m) * static_cast<size_t>(m);
     }
     h.leaves->upload(lv);
     h.leaves_zero = allzero;
@@ -153,10 +174,10 @@ DHodlr DHodlr::import_panels(DTreeP t, bool symmetric, const int* R, const doubl
 
 size_t DHodlr::export_size() const {
     size_t s = 0;
-    for (int r : R) s += 2 * size_t(n()) * size_t(r);
+    for (int r : R) s += 2 * static_cast<size_t>(n()) * static_cast<size_t>(r);
     const auto& hb = tree->leaves().hbounds();
     for (int b = 0; b < tree->leaves().nseg(); ++b) {
-        size_t m = size_t(hb[size_t(b + 1)] - hb[size_t(b)]);
+        size_t m = static_cast<size_t>(hb[static_cast<size_t>(b + 1)] - hb[static_cast<size_t>(b)]);
         s += m * m;
     }
     return s;
@@ -167,27 +188,27 @@ void DHodlr::export_panels(double* flat, int* ranks_up, int* ranks_lo) const {
     size_t off = 0, node = 0;
     for (int l = 1; l <= tau(); ++l) {
         const int Rl = this->Rl(l);
-        const size_t cnt = size_t(n) * size_t(Rl);
+        const size_t cnt = static_cast<size_t>(n) * static_cast<size_t>(Rl);
         if (Rl) {
             HG_CUDA(cudaMemcpyAsync(flat + off, Ul(l), cnt * sizeof(double), cudaMemcpyDeviceToHost, current().stream));
             HG_CUDA(cudaMemcpyAsync(flat + off + cnt, Vl(l), cnt * sizeof(double), cudaMemcpyDeviceToHost,
                                     current().stream));
         }
         off += 2 * cnt;
-        for (size_t j = 0; j < rank_up[size_t(l - 1)].size(); ++j, ++node) {
-            ranks_up[node] = rank_up[size_t(l - 1)][j];
-            ranks_lo[node] = rank_lo[size_t(l - 1)][j];
+        for (size_t j = 0; j < rank_up[static_cast<size_t>(l - 1)].size(); ++j, ++node) {
+            ranks_up[node] = rank_up[static_cast<size_t>(l - 1)][j];
+            ranks_lo[node] = rank_lo[static_cast<size_t>(l - 1)][j];
         }
     }
     std::vector<double> lv = leaves->download();  // synchronizes
     const auto& hb = tree->leaves().hbounds();
     for (int b = 0; b < tree->leaves().nseg(); ++b) {
-        const int m = hb[size_t(b + 1)] - hb[size_t(b)];
+        const int m = hb[static_cast<size_t>(b + 1)] - hb[static_cast<size_t>(b)];
         for (int j = 0; j < m; ++j)
             for (int i = 0; i < m; ++i)
-                flat[off + size_t(i) + size_t(j) * size_t(m)] =
-                    lv[size_t(b) * size_t(lstride()) + size_t(i) + size_t(j) * size_t(bmax())];
-        off += size_t(m) * size_t(m);
+                flat[off + static_cast<size_t>(i) + static_cast<size_t>(j) * static_cast<size_t>(m)] =
+                    lv[static_cast<size_t>(b) * static_cast<size_t>(lstride()) + static_cast<size_t>(i) + static_cast<size_t>(j) * static_cast<size_t>(bmax())];
+        off += static_cast<size_t>(m) * static_cast<size_t>(m);
     }
 }
 
@@ -195,17 +216,17 @@ void DHodlr::make_asymmetric() {
     if (!sym) return;
     sym = false;
     for (int l = 1; l <= tau(); ++l) {
-        V[size_t(l - 1)] = U[size_t(l - 1)];
-        rank_lo[size_t(l - 1)] = rank_up[size_t(l - 1)];
+        V[static_cast<size_t>(l - 1)] = U[static_cast<size_t>(l - 1)];
+        rank_lo[static_cast<size_t>(l - 1)] = rank_up[static_cast<size_t>(l - 1)];
     }
 }
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
-                 bool with_leaves, bool transpose, double beta) {
+                 bool with_leaves, bool transpose, double beta, double alpha) {
     if (s <= 0) return;
     const i64 n = h.n();
     if (with_leaves && !h.leaves_zero) {
-        leaf_mm(h.tree->leaves(), h.leaves->get(), h.lstride(), h.bmax(), transpose, X, ldx, Y, ldy, s, 1.0, beta);
+        leaf_mm(h.tree->leaves(), h.leaves->get(), h.lstride(), h.bmax(), transpose, X, ldx, Y, ldy, s, alpha, beta);
     } else if (beta != 1.0) {
         panel_axpby(n, s, 0.0, nullptr, 0, beta, Y, ldy);
     }
@@ -217,9 +238,9 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         const Partition& p = h.tree->part(l);
         const double* A = transpose ? h.Ul(l) : h.Vl(l);
         const double* B = transpose ? h.Vl(l) : h.Ul(l);
-        DVec T(size_t(p.nseg()) * size_t(R) * size_t(s));
+        DVec T(static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(s));
         seg_tn(p, A, n, R, X, ldx, s, T.get(), i64(R) * s, R);
-        seg_nn(p, B, n, R, T.get(), i64(R) * s, R, TMap::sibling(), Y, ldy, s, 1.0, 1.0);
+        seg_nn(p, B, n, R, T.get(), i64(R) * s, R, TMap::sibling(), Y, ldy, s, alpha, 1.0);
     }
 }
 
@@ -235,7 +256,7 @@ void hodlr_trace_product(const DHodlr& a, const DHodlr& b, double* out, bool acc
         const int RA = a.Rl(l), RB = b.Rl(l);
         if (RA == 0 || RB == 0) continue;
         const Partition& p = a.tree->part(l);
-        DVec G(size_t(p.nseg()) * size_t(RA) * size_t(RB)), H(size_t(p.nseg()) * size_t(RA) * size_t(RB));
+        DVec G(static_cast<size_t>(p.nseg()) * static_cast<size_t>(RA) * static_cast<size_t>(RB)), H(static_cast<size_t>(p.nseg()) * static_cast<size_t>(RA) * static_cast<size_t>(RB));
         seg_tn(p, b.Vl(l), n, RB, a.Ul(l), n, RA, G.get(), i64(RB) * RA, RB);
         seg_tn(p, a.Vl(l), n, RA, b.Ul(l), n, RB, H.get(), i64(RA) * RB, RA);
         seg_pair_dot(p.nseg(), 1, G.get(), i64(RB) * RA, RB, RB, RA, H.get(), i64(RA) * RB, RA, out, true);

@@ -29,9 +29,9 @@ struct DHodlr {
     int tau() const { return tree->tau(); }
     int bmax() const { return tree->bmax; }
     i64 lstride() const { return i64(bmax()) * bmax(); }
-    double* Ul(int l) const { return U[size_t(l - 1)] ? U[size_t(l - 1)]->get() : nullptr; }
-    double* Vl(int l) const { return V[size_t(l - 1)] ? V[size_t(l - 1)]->get() : nullptr; }
-    int Rl(int l) const { return R[size_t(l - 1)]; }
+    double* Ul(int l) const { return U[static_cast<size_t>(l - 1)] ? U[static_cast<size_t>(l - 1)]->get() : nullptr; }
+    double* Vl(int l) const { return V[static_cast<size_t>(l - 1)] ? V[static_cast<size_t>(l - 1)]->get() : nullptr; }
+    int Rl(int l) const { return R[static_cast<size_t>(l - 1)]; }
 
     /// hodlr_matrix.cpp:68-81 (empty off-diagonal blocks, zero leaves).
     static DHodlr zero(DTreeP t, bool symmetric = true);
@@ -54,12 +54,15 @@ struct DHodlr {
     void set_level(int l, int r, bool symmetric_panel);
 };
 
-/// Y = beta Y + H_sel X over an n x s block, where H_sel keeps levels
+/// Y = beta Y + alpha H_sel X over an n x s block, where H_sel keeps levels
 /// [lmin, lmax] (and the leaves when with_leaves). lmin = d+1 gives the
 /// block-diagonal of all depth-d sub-blocks at once (sub_matvec,
 /// hodlr_matrix.cpp:228-265); lmin = 1 is the full matvec (:198-222).
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
-                 bool with_leaves, bool transpose, double beta = 0.0);
+                 bool with_leaves, bool transpose, double beta = 0.0, double alpha = 1.0);
+
+/// Leaves <-> n x bmax panel (leaf b occupies its rows, columns [0, m_b)).
+void leaves_panel(const DTree& t, double* leaves, double* P, bool to_panel);
 
 /// out (+)= trace(H) (hodlr_matrix.cpp:267-271).
 void hodlr_trace(const DHodlr& h, double* out, bool accumulate);

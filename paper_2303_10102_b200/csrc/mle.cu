@@ -1,0 +1,63 @@
+// Statistics glue of one MLE iteration (mle.cpp:25-54) on the device.
+#include <cmath>
+
+#include "api.cuh"
+
+namespace hg {
+
+namespace {
+constexpr double kLog2Pi = 1.8378770664093454836;
+}
+
+double log_likelihood(const DFactor& f, const double* r) {
+    const i64 n = f.n();
+    DVec w(static_cast<size_t>(n)), d(1);
+    panel_axpby(n, 1, 1.0, r, n, 0.0, w.get(), n);
+    factor_solve(f, w.get(), n, 1);
+    dot_panels(n, 1, r, n, w.get(), n, d.get(), false);
+    const double ld = factor_logdet(f);
+    return -0.5 * double(n) * kLog2Pi - 0.5 * ld - 0.5 * read_scalar(d.get());
+}
+
+std::vector<double> score(const DFactor& f, const std::vector<const DHodlr*>& deriv, const double* r,
+                          std::vector<DProductRep>* reps) {
+    const i64 n = f.n();
+    const size_t p = deriv.size();
+    DVec w(static_cast<size_t>(n)), kw(static_cast<size_t>(n)), acc(2 * std::max<size_t>(p, 1));
+    panel_axpby(n, 1, 1.0, r, n, 0.0, w.get(), n);
+    factor_solve(f, w.get(), n, 1);
+    std::vector<DProductRep> local;
+    std::vector<DProductRep>& rp = reps ? *reps : local;
+    rp.clear();
+    for (size_t j = 0; j < p; ++j) {
+        rp.push_back(pipeline(f, *deriv[j], true));
+        trace_product_rep(rp.back(), acc.get() + 2 * j, false);
+        hodlr_apply(*deriv[j], w.get(), n, 1, kw.get(), n, 1, deriv[j]->tau(), true, false, 0.0);
+        dot_panels(n, 1, w.get(), n, kw.get(), n, acc.get() + 2 * j + 1, false);
+    }
+    std::vector<double> h = acc.download();
+    std::vector<double> s(p);
+    for (size_t j = 0; j < p; ++j) s[j] = -0.5 * h[2 * j] + 0.5 * h[2 * j + 1];
+    return s;
+}
+
+std::vector<double> fisher_from_reps(const std::vector<DProductRep>& reps) {
+    const size_t p = reps.size();
+    DVec acc(std::max<size_t>(p * p, 1));
+    acc.zero();
+    for (size_t i = 0; i < p; ++i)
+        for (size_t j = i; j < p; ++j) trace_pair(reps[i], reps[j], acc.get() + i + j * p, false);
+    std::vector<double> t = acc.download();
+    std::vector<double> info(p * p), out(p * p);
+    for (size_t i = 0; i < p; ++i)
+        for (size_t j = i; j < p; ++j) {
+            const double v = 0.5 * t[i + j * p];
+            info[i + j * p] = v;
+            info[j + i * p] = v;
+        }
+    for (size_t i = 0; i < p; ++i)
+        for (size_t j = 0; j < p; ++j) out[i + j * p] = 0.5 * (info[i + j * p] + info[j + i * p]);
+    return out;
+}
+
+}  // namespace hg

@@ -1,0 +1,328 @@
+// Device covariance oracles: dense matrices, 1D Matérn (dense on-the-fly and
+// O(n) scan), user callbacks. Reference interface: oracle.hpp:15-143.
+#include <cmath>
+
+#include "oracle.cuh"
+#include "tile.cuh"
+
+namespace hg {
+
+void gemm_nn(i64 m, int n, int k, const double* A, i64 lda, const double* B, i64 ldb, double* C, i64 ldc,
+             double alpha, double beta) {
+    const Partition& p = get_tree(m, 0)->part(0);
+    seg_nn(p, A, lda, k, B, 0, int(ldb), TMap::same(), C, ldc, n, alpha, beta);
+}
+
+namespace {
+
+// ------------------------------------------------------------------ dense
+class DenseOracle : public DOracle {
+public:
+    DenseOracle(i64 n, const double* K, int p, const double* dK) : DOracle(n, p) {
+        k_.upload(K, static_cast<size_t>(n) * static_cast<size_t>(n));
+        if (p) dk_.upload(dK, static_cast<size_t>(p) * static_cast<size_t>(n) * static_cast<size_t>(n));
+    }
+
+protected:
+    void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {
+        if (j >= p_) throw std::invalid_argument("apply_derivative: parameter index");
+        if (j >= 0 && p_ == 0) {
+            panel_axpby(n_, s, 0.0, nullptr, 0, 0.0, Y, ldy);
+            return;
+        }
+        const double* M = j < 0 ? k_.get() : dk_.get() + i64(j) * n_ * n_;
+        gemm_nn(n_, s, int(n_), M, n_, V, ldv, Y, ldy, 1.0, 0.0);
+    }
+
+private:
+    DVec k_, dk_;
+};
+
+// ----------------------------------------------------------------- Matérn
+/// exp(-lambda d) * sum_m c[m] d^m (same table as oracle/hodlr.cpp).
+struct Poly {
+    double lambda;
+    double c[4];
+    int nt;
+};
+
+Poly matern_poly(int nu2, int which, double sigma2, double ell) {
+    Poly P{};
+    const double cnu = nu2 == 1 ? 1.0 : (nu2 == 3 ? std::sqrt(3.0) : std::sqrt(5.0));
+    P.lambda = cnu / ell;
+    const double L = P.lambda, s = which == 0 ? 1.0 : sigma2;
+    if (which <= 0) {
+        P.c[0] = s;
+        if (nu2 >= 3) P.c[1] = s * L;
+        if (nu2 == 5) P.c[2] = s * L * L / 3.0;
+        P.nt = nu2 == 1 ? 1 : (nu2 == 3 ? 2 : 3);
+    } else if (nu2 == 1) {
+        P.c[1] = s * L / ell;
+        P.nt = 2;
+    } else if (nu2 == 3) {
+        P.c[2] = s * L * L / ell;
+        P.nt = 3;
+    } else {
+        P.c[2] = s * L * L / (3.0 * ell);
+        P.c[3] = s * L * L * L / (3.0 * ell);
+        P.nt = 4;
+    }
+    return P;
+}
+
+__device__ __forceinline__ double poly_eval(const Poly& P, double d) {
+    double p = 0.0, dm = 1.0;
+    for (int m = 0; m < P.nt; ++m) {
+        p += P.c[m] * dm;
+        dm *= d;
+    }
+    return p * exp(-P.lambda * d);
+}
+
+using tile::KS;
+using tile::NT;
+using tile::TM;
+using tile::TN;
+
+/// Y = K V with K(i,j) = k(|x_i - x_j|) formed tile by tile in shared memory.
+__global__ void __launch_bounds__(NT) k_matern_dense(const double* x, int n, Poly P, const double* V, i64 ldv,
+                                                       int s, double* Y, i64 ldy) {
+    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    const int r0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    double acc[4][4] = {};
+    const int am = tid & 63, akq = tid >> 6, bk = tid & 15, bn = tid >> 4;
+    const double xr = r0 + am < n ? x[r0 + am] : 0.0;
+    for (int kb = 0; kb < n; kb += KS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kk = akq + 4 * q;
+            As[kk][am] = (r0 + am < n && kb + kk < n) ? poly_eval(P, fabs(xr - x[kb + kk])) : 0.0;
+            const int c = n0 + bn + 16 * q;
+            Bs[bk][bn + 16 * q] = (kb + bk < n && c < s) ? V[i64(kb + bk) + i64(c) * ldv] : 0.0;
+        }
+        __syncthreads();
+        tile::mma16(As, Bs, acc, tm, tn);
+        __syncthreads();
+    }
+    for (int j = 0; j < 4; ++j) {
+        const int c = n0 + tn + 16 * j;
+        if (c >= s) continue;
+        for (int i = 0; i < 4; ++i) {
+            const int r = r0 + tm + 16 * i;
+            if (r < n) Y[i64(r) + i64(c) * ldy] = acc[i][j];
+        }
+    }
+}
+
+__device__ __forceinline__ void propagate(double* st, int nt, double d, double rho) {
+    // st_m <- rho * sum_{q<=m} C(m,q) d^{m-q} st_q
+    double ns[4];
+    const double d2 = d * d;
+    ns[0] = st[0];
+    if (nt > 1) ns[1] = st[1] + d * st[0];
+    if (nt > 2) ns[2] = st[2] + 2.0 * d * st[1] + d2 * st[0];
+    if (nt > 3) ns[3] = st[3] + 3.0 * d * st[2] + 3.0 * d2 * st[1] + d2 * d * st[0];
+    for (int m = 0; m < nt; ++m) st[m] = rho * ns[m];
+}
+
+__global__ void k_steps(const double* x, int n, double lambda, double* dx, double* rho) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double d = i > 0 ? x[i] - x[i - 1] : 0.0;
+        dx[i] = d;
+        rho[i] = exp(-lambda * d);
+    }
+}
+
+struct ScanArgs {
+    const double* dx;   // dx[i] = x_i - x_{i-1}
+    const double* rho;  // exp(-lambda dx[i])
+    const double* x;
+    int n, ch, nch, s, nt;
+    const double* V;
+    i64 ldv;
+    double* Y;
+    i64 ldy;
+    double* locF;  // [col][chunk][4]
+    double* locB;
+    double c[4];
+    double diag;  // added to the diagonal: nugget (value) - c0 (double-counted self term)
+};
+
+__global__ void k_scan_local(ScanArgs g) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.nch * g.s) return;
+    const int chunk = t % g.nch, col = t / g.nch;
+    const int lo = chunk * g.ch, hi = min(g.n, lo + g.ch);
+    const double* v = g.V + i64(col) * g.ldv;
+    double st[4] = {0, 0, 0, 0};
+    for (int i = lo; i < hi; ++i) {
+        if (i > lo) propagate(st, g.nt, g.dx[i], g.rho[i]);
+        st[0] += v[i];
+    }
+    double* o = g.locF + (i64(col) * g.nch + chunk) * 4;
+    for (int m = 0; m < 4; ++m) o[m] = st[m];
+    for (int m = 0; m < 4; ++m) st[m] = 0.0;
+    for (int i = hi - 1; i >= lo; --i) {
+        if (i < hi - 1) propagate(st, g.nt, g.dx[i + 1], g.rho[i + 1]);
+        st[0] += v[i];
+    }
+    o = g.locB + (i64(col) * g.nch + chunk) * 4;
+    for (int m = 0; m < 4; ++m) o[m] = st[m];
+}
+
+/// Carries: locF[c] becomes the full forward state at the chunk's last point,
+/// locB[c] the full backward state at its first point (sequential per column;
+/// the chunk-to-chunk transfer exp(-lambda dx) is recomputed from x).
+__global__ void k_scan_carry(ScanArgs g, double lambda) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= g.s) return;
+    double* F = g.locF + i64(col) * g.nch * 4;
+    double* B = g.locB + i64(col) * g.nch * 4;
+    double st[4];
+    for (int m = 0; m < 4; ++m) st[m] = F[m];
+    for (int c = 1; c < g.nch; ++c) {
+        const int e_prev = c * g.ch - 1, e_cur = min(g.n, (c + 1) * g.ch) - 1;
+        const double d = g.x[e_cur] - g.x[e_prev];
+        propagate(st, g.nt, d, exp(-lambda * d));
+        for (int m = 0; m < 4; ++m) {
+            st[m] += F[c * 4 + m];
+            F[c * 4 + m] = st[m];
+        }
+    }
+    for (int m = 0; m < 4; ++m) st[m] = B[(g.nch - 1) * 4 + m];
+    for (int c = g.nch - 2; c >= 0; --c) {
+        const double d = g.x[(c + 1) * g.ch] - g.x[c * g.ch];
+        propagate(st, g.nt, d, exp(-lambda * d));
+        for (int m = 0; m < 4; ++m) {
+            st[m] += B[c * 4 + m];
+            B[c * 4 + m] = st[m];
+        }
+    }
+}
+
+__global__ void k_scan_final(ScanArgs g) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.nch * g.s) return;
+    const int chunk = t % g.nch, col = t / g.nch;
+    const int lo = chunk * g.ch, hi = min(g.n, lo + g.ch);
+    const double* v = g.V + i64(col) * g.ldv;
+    double* y = g.Y + i64(col) * g.ldy;
+    double st[4] = {0, 0, 0, 0};
+    if (chunk > 0) {
+        const double* c = g.locF + (i64(col) * g.nch + chunk - 1) * 4;
+        for (int m = 0; m < 4; ++m) st[m] = c[m];
+    }
+    for (int i = lo; i < hi; ++i) {
+        if (i > 0) propagate(st, g.nt, g.dx[i], g.rho[i]);
+        st[0] += v[i];
+        double a = 0.0;
+        for (int m = 0; m < g.nt; ++m) a += g.c[m] * st[m];
+        y[i] = a;
+    }
+    for (int m = 0; m < 4; ++m) st[m] = 0.0;
+    if (chunk < g.nch - 1) {
+        const double* c = g.locB + (i64(col) * g.nch + chunk + 1) * 4;
+        for (int m = 0; m < 4; ++m) st[m] = c[m];
+    }
+    for (int i = hi - 1; i >= lo; --i) {
+        if (i < g.n - 1) propagate(st, g.nt, g.dx[i + 1], g.rho[i + 1]);
+        st[0] += v[i];
+        double a = 0.0;
+        for (int m = 0; m < g.nt; ++m) a += g.c[m] * st[m];
+        y[i] += a + g.diag * v[i];
+    }
+}
+
+class MaternOracle : public DOracle {
+public:
+    MaternOracle(i64 n, const double* x, int nu2, double sigma2, double ell, double nugget, bool scan)
+        : DOracle(n, 2), nu2_(nu2), sigma2_(sigma2), ell_(ell), nugget_(nugget), scan_(scan) {
+        if (nu2 != 1 && nu2 != 3 && nu2 != 5) throw std::invalid_argument("Matern: nu in {1/2, 3/2, 5/2}");
+        for (i64 i = 1; i < n; ++i)
+            if (x[i] < x[i - 1]) throw std::invalid_argument("Matern: points must be sorted");
+        x_.upload(x, static_cast<size_t>(n));
+        dx_.alloc(static_cast<size_t>(n));
+        rho_.alloc(static_cast<size_t>(n));
+    }
+    void set_parameters(const double* th, int p) override {
+        if (p != 2) throw std::invalid_argument("Matern: theta = (sigma2, ell)");
+        sigma2_ = th[0];
+        ell_ = th[1];
+        cached_lambda_ = -1.0;
+    }
+
+protected:
+    void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {
+        if (j >= 2) throw std::invalid_argument("apply_derivative: parameter index");
+        const Poly P = matern_poly(nu2_, j, sigma2_, ell_);
+        auto& c = current();
+        if (!scan_) {
+            dim3 grid(unsigned(cdiv(n_, TM)), unsigned(cdiv(s, TN)));
+            k_matern_dense<<<grid, NT, 0, c.stream>>>(x_.get(), int(n_), P, V, ldv, s, Y, ldy);
+            HG_LAUNCH();
+            ++c.launches;
+            if (j < 0 && nugget_ != 0.0) panel_axpby(n_, s, nugget_, V, ldv, 1.0, Y, ldy);
+            return;
+        }
+        if (cached_lambda_ != P.lambda) {
+            k_steps<<<cdiv(n_, 256), 256, 0, c.stream>>>(x_.get(), int(n_), P.lambda, dx_.get(), rho_.get());
+            HG_LAUNCH();
+            ++c.launches;
+            cached_lambda_ = P.lambda;
+        }
+        const int ch = int(std::max<i64>(64, (n_ + 4095) / 4096));
+        const int nch = cdiv(n_, ch);
+        DVec locF(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4), locB(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4);
+        ScanArgs g{dx_.get(), rho_.get(), x_.get(), int(n_), ch, nch, s, P.nt, V, ldv, Y, ldy, locF.get(),
+                   locB.get(), {P.c[0], P.c[1], P.c[2], P.c[3]}, (j < 0 ? nugget_ : 0.0) - P.c[0]};
+        const int threads = nch * s;
+        k_scan_local<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
+        HG_LAUNCH();
+        k_scan_carry<<<cdiv(s, 32), 32, 0, c.stream>>>(g, P.lambda);
+        HG_LAUNCH();
+        k_scan_final<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
+        HG_LAUNCH();
+        c.launches += 3;
+    }
+
+private:
+    int nu2_;
+    double sigma2_, ell_, nugget_;
+    bool scan_;
+    DVec x_;
+    mutable DVec dx_, rho_;
+    mutable double cached_lambda_ = -1.0;
+};
+
+class CallbackOracle : public DOracle {
+public:
+    CallbackOracle(i64 n, int p, ApplyFn fn, void* user) : DOracle(n, p), fn_(fn), user_(user) {}
+
+protected:
+    void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {
+        if (fn_(user_, j, V, ldv, s, Y, ldy, current().stream) != 0)
+            throw std::runtime_error("oracle callback failed");
+    }
+
+private:
+    ApplyFn fn_;
+    void* user_;
+};
+
+}  // namespace
+
+std::unique_ptr<DOracle> make_dense_oracle(i64 n, const double* K, int p, const double* dK) {
+    return std::make_unique<DenseOracle>(n, K, p, dK);
+}
+
+std::unique_ptr<DOracle> make_matern_oracle(i64 n, const double* x, int nu2, double sigma2, double ell,
+                                            double nugget, bool scan) {
+    return std::make_unique<MaternOracle>(n, x, nu2, sigma2, ell, nugget, scan);
+}
+
+std::unique_ptr<DOracle> make_callback_oracle(i64 n, int p, ApplyFn fn, void* user) {
+    return std::make_unique<CallbackOracle>(n, p, fn, user);
+}
+
+}  // namespace hg

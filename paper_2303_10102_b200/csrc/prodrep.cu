@@ -7,34 +7,13 @@ namespace hg {
 
 namespace {
 
-__global__ void k_leaves_panel(const int* bounds, int bmax, double* leaves, double* P, i64 ldp, int to_panel) {
-    const int b = blockIdx.x;
-    const int lo = bounds[b], m = bounds[b + 1] - lo;
-    double* L = leaves + i64(b) * bmax * bmax;
-    for (int e = threadIdx.x; e < m * bmax; e += blockDim.x) {
-        const int r = e % m, c = e / m;
-        if (to_panel)
-            P[i64(lo + r) + i64(c) * ldp] = c < m ? L[r + i64(c) * bmax] : 0.0;
-        else if (c < m)
-            L[r + i64(c) * bmax] = P[i64(lo + r) + i64(c) * ldp];
-    }
-}
-
-void leaves_panel(const DTree& t, double* leaves, double* P, bool to_panel) {
-    const Partition& lv = t.leaves();
-    k_leaves_panel<<<unsigned(lv.nseg()), 256, 0, current().stream>>>(lv.dbounds(), t.bmax, leaves, P, t.n(),
-                                                                       to_panel ? 1 : 0);
-    HG_LAUNCH();
-    count_launch();
-}
-
 /// Y <- Abar^{-1} Y (inverse) or Abar Y on an n x w panel.
 void leaf_step(const DFactor& f, bool inverse, double* Y, int w) {
     if (w <= 0) return;
     if (inverse) {
         leaf_solve(f, Y, f.n(), w);
     } else {
-        DVec tmp(size_t(f.n()) * size_t(w));
+        DVec tmp(static_cast<size_t>(f.n()) * static_cast<size_t>(w));
         panel_axpby(f.n(), w, 1.0, Y, f.n(), 0.0, tmp.get(), f.n());
         leaf_mm(f.tree->leaves(), f.leaf_mat->get(), f.lstride(), f.bmax(), false, tmp.get(), f.n(), Y, f.n(), w,
                 1.0, 0.0);
@@ -56,7 +35,7 @@ void level_multiply(const DFactor& f, int i, double* Y, i64 ldy, int w) {
     const int R = f.Rl(i);
     if (R == 0 || w <= 0) return;
     const Partition& p = f.tree->part(i);
-    DVec Q(size_t(p.nseg()) * size_t(R) * size_t(w));
+    DVec Q(static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(w));
     // v^T Y = [x^T Y_cr ; w^T Y_cl]; Y_cl += wbar (x^T Y_cr), Y_cr += xbar (w^T Y_cl)
     seg_tn(p, f.Fl(i), f.n(), R, Y, ldy, w, Q.get(), i64(R) * w, R);
     seg_nn(p, f.Wl(i), f.n(), R, Q.get(), i64(R) * w, R, TMap::sibling(), Y, ldy, w, 1.0, 1.0);
@@ -74,23 +53,23 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
     rep.base.make_asymmetric();
     // Left factors are rewritten: give the base its own copies (right factors stay aliased).
     for (int l = 1; l <= tau; ++l)
-        if (rep.base.Rl(l)) rep.base.U[size_t(l - 1)] = std::make_shared<DVec>(*b.U[size_t(l - 1)]);
+        if (rep.base.Rl(l)) rep.base.U[static_cast<size_t>(l - 1)] = std::make_shared<DVec>(*b.U[static_cast<size_t>(l - 1)]);
     rep.base.leaves = std::make_shared<DVec>(*b.leaves);
-    rep.C.assign(size_t(tau), 0);
-    rep.coff.assign(size_t(tau), 0);
+    rep.C.assign(static_cast<size_t>(tau), 0);
+    rep.coff.assign(static_cast<size_t>(tau), 0);
     for (int i = 1; i <= tau; ++i) {
-        rep.coff[size_t(i - 1)] = rep.sumC;
-        rep.C[size_t(i - 1)] = 2 * f.Rl(i);
-        rep.sumC += rep.C[size_t(i - 1)];
+        rep.coff[static_cast<size_t>(i - 1)] = rep.sumC;
+        rep.C[static_cast<size_t>(i - 1)] = 2 * f.Rl(i);
+        rep.sumC += rep.C[static_cast<size_t>(i - 1)];
     }
-    rep.Cu = make_dvec(size_t(n) * size_t(std::max(rep.sumC, 1)), true);
-    rep.Cv = make_dvec(size_t(n) * size_t(std::max(rep.sumC, 1)), true);
+    rep.Cu = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(rep.sumC, 1)), true);
+    rep.Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(rep.sumC, 1)), true);
 
     for (int i = 1; i <= tau; ++i) {
         const int R = f.Rl(i);
         if (R == 0) continue;
         // product_rep.cpp:84-90: older corrections' left factors.
-        level_op(f, i, inverse, rep.Cu->get(), rep.coff[size_t(i - 1)]);
+        level_op(f, i, inverse, rep.Cu->get(), rep.coff[static_cast<size_t>(i - 1)]);
         // product_rep.cpp:92-104: the running base's coarser left factors.
         for (int m = 1; m < i; ++m)
             if (rep.base.Rl(m)) level_op(f, i, inverse, rep.base.Ul(m), rep.base.Rl(m));
@@ -98,10 +77,10 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         const Partition& p = f.tree->part(i);
         const int C2 = 2 * R;
         double* cu = rep.Cul(i);
-        DVec Q(size_t(n) * size_t(C2));
+        DVec Q(static_cast<size_t>(n) * static_cast<size_t>(C2));
         if (inverse) {
             // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
-            DVec E(size_t(1 << (i - 1)) * size_t(C2) * size_t(C2));
+            DVec E(static_cast<size_t>(1 << (i - 1)) * static_cast<size_t>(C2) * static_cast<size_t>(C2));
             cap_inverse_transpose(f, i, E.get());
             seg_nn(p, f.Fl(i), n, R, E.get(), i64(C2) * C2, C2, TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
             // q = u = [wbar 0; 0 xbar]
@@ -123,7 +102,7 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         if (rep.base.Rl(m)) leaf_step(f, inverse, rep.base.Ul(m), rep.base.Rl(m));
     {
         const int bm = f.bmax();
-        DVec P(size_t(n) * size_t(bm));
+        DVec P(static_cast<size_t>(n) * static_cast<size_t>(bm));
         leaves_panel(*f.tree, rep.base.leaves->get(), P.get(), true);
         leaf_step(f, inverse, P.get(), bm);
         leaves_panel(*f.tree, rep.base.leaves->get(), P.get(), false);
@@ -145,9 +124,9 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
     // Cross terms sum(v .* (base_sub u)) (product_rep.cpp:212-224).
     auto cross = [&](const DHodlr& h, const DProductRep& corr) {
         for (int i = 1; i <= tau; ++i) {
-            const int Ci = corr.C[size_t(i - 1)];
+            const int Ci = corr.C[static_cast<size_t>(i - 1)];
             if (!Ci) continue;
-            DVec Y(size_t(n) * size_t(Ci));
+            DVec Y(static_cast<size_t>(n) * static_cast<size_t>(Ci));
             hodlr_apply(h, corr.Cul(i), n, Ci, Y.get(), n, i, tau, true, false, 0.0);
             dot_panels(n, Ci, corr.Cvl(i), n, Y.get(), n, out, true);
         }
@@ -157,17 +136,17 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
     // Correction pairs aligned by the finer level (product_rep.cpp:159-176,227-233):
     // all coarse levels of one operand against fine level f of the other at once.
     auto pairs = [&](const DProductRep& coarse, int W, const DProductRep& fine, int f) {
-        const int Cf = fine.C[size_t(f - 1)];
+        const int Cf = fine.C[static_cast<size_t>(f - 1)];
         if (!W || !Cf) return;
         const Partition& p = t.part(f - 1);
-        DVec G1(size_t(p.nseg()) * size_t(W) * size_t(Cf)), G2(size_t(p.nseg()) * size_t(W) * size_t(Cf));
+        DVec G1(static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf)), G2(static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf));
         seg_tn(p, coarse.Cv->get(), n, W, fine.Cul(f), n, Cf, G1.get(), i64(W) * Cf, W);
         seg_tn(p, fine.Cvl(f), n, Cf, coarse.Cu->get(), n, W, G2.get(), i64(W) * Cf, Cf);
         seg_pair_dot(p.nseg(), 0, G1.get(), i64(W) * Cf, W, W, Cf, G2.get(), i64(W) * Cf, Cf, out, true);
     };
     for (int f = 1; f <= tau; ++f) {
-        pairs(pb, pb.coff[size_t(f - 1)] + pb.C[size_t(f - 1)], pd, f);  // i <= j: coarse from pb
-        pairs(pd, pd.coff[size_t(f - 1)], pb, f);                         // i > j: coarse from pd
+        pairs(pb, pb.coff[static_cast<size_t>(f - 1)] + pb.C[static_cast<size_t>(f - 1)], pd, f);  // i <= j: coarse from pb
+        pairs(pd, pd.coff[static_cast<size_t>(f - 1)], pb, f);                         // i > j: coarse from pd
     }
 }
 
@@ -175,16 +154,16 @@ std::vector<double> prodrep_densify(const DProductRep& p) {
     const i64 n = p.n();
     if (n > (i64(1) << 14)) throw std::length_error("densify: matrix too large");
     std::vector<double> flat(p.base.export_size());
-    std::vector<int> ru(size_t(std::max<i64>((i64(1) << p.tau()) - 1, 1))), rl(ru.size());
+    std::vector<int> ru(static_cast<size_t>(std::max<i64>((i64(1) << p.tau()) - 1, 1))), rl(ru.size());
     p.base.export_panels(flat.data(), ru.data(), rl.data());
-    std::vector<double> a(size_t(n) * size_t(n), 0.0);
+    std::vector<double> a(static_cast<size_t>(n) * static_cast<size_t>(n), 0.0);
     const ClusterTree& t = p.base.tree->host;
     size_t off = 0;
     for (int l = 1; l <= p.tau(); ++l) {
         const int R = p.base.Rl(l);
         const double* U = flat.data() + off;
-        const double* V = U + size_t(n) * size_t(R);
-        off += 2 * size_t(n) * size_t(R);
+        const double* V = U + static_cast<size_t>(n) * static_cast<size_t>(R);
+        off += 2 * static_cast<size_t>(n) * static_cast<size_t>(R);
         const auto& kids = t.level(l);
         for (size_t j = 0; j < kids.size() / 2; ++j) {
             const Range cl = kids[2 * j], cr = kids[2 * j + 1];
@@ -193,7 +172,7 @@ std::vector<double> prodrep_densify(const DProductRep& p) {
                     for (i64 r = rows.lo; r < rows.hi; ++r) {
                         double s = 0;
                         for (int q = 0; q < R; ++q) s += U[r + q * n] * V[c + q * n];
-                        a[size_t(r + c * n)] = s;
+                        a[static_cast<size_t>(r + c * n)] = s;
                     }
             };
             blk(cl, cr);
@@ -203,20 +182,20 @@ std::vector<double> prodrep_densify(const DProductRep& p) {
     for (const Range& r : t.leaves()) {
         const i64 m = r.size();
         for (i64 c = 0; c < m; ++c)
-            for (i64 q = 0; q < m; ++q) a[size_t(r.lo + q + (r.lo + c) * n)] = flat[off + size_t(q + c * m)];
-        off += size_t(m * m);
+            for (i64 q = 0; q < m; ++q) a[static_cast<size_t>(r.lo + q + (r.lo + c) * n)] = flat[off + static_cast<size_t>(q + c * m)];
+        off += static_cast<size_t>(m * m);
     }
     std::vector<double> cu = p.Cu->download(), cv = p.Cv->download();
     for (int i = 1; i <= p.tau(); ++i) {
-        const int Ci = p.C[size_t(i - 1)];
+        const int Ci = p.C[static_cast<size_t>(i - 1)];
         if (!Ci) continue;
-        const size_t co = size_t(p.coff[size_t(i - 1)]) * size_t(n);
+        const size_t co = static_cast<size_t>(p.coff[static_cast<size_t>(i - 1)]) * static_cast<size_t>(n);
         for (const Range& r : t.level(i - 1))
             for (i64 c = r.lo; c < r.hi; ++c)
                 for (i64 q = r.lo; q < r.hi; ++q) {
                     double s = 0;
-                    for (int k = 0; k < Ci; ++k) s += cu[co + size_t(q + k * n)] * cv[co + size_t(c + k * n)];
-                    a[size_t(q + c * n)] += s;
+                    for (int k = 0; k < Ci; ++k) s += cu[co + static_cast<size_t>(q + k * n)] * cv[co + static_cast<size_t>(c + k * n)];
+                    a[static_cast<size_t>(q + c * n)] += s;
                 }
     }
     return a;

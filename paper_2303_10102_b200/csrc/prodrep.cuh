@@ -20,8 +20,8 @@ struct DProductRep {
     DVecP Cu, Cv;  // n x max(sumC, 1)
     i64 n() const { return base.n(); }
     int tau() const { return base.tau(); }
-    double* Cul(int i) const { return Cu->get() + i64(coff[size_t(i - 1)]) * n(); }
-    double* Cvl(int i) const { return Cv->get() + i64(coff[size_t(i - 1)]) * n(); }
+    double* Cul(int i) const { return Cu->get() + i64(coff[static_cast<size_t>(i - 1)]) * n(); }
+    double* Cvl(int i) const { return Cv->get() + i64(coff[static_cast<size_t>(i - 1)]) * n(); }
 };
 
 /// product_rep.cpp:47-155 (inverse = solve_multiply, else multiply).

@@ -18,14 +18,14 @@ void set_current(Ctx* c) { g_ctx = c; }
 
 // cluster_tree.cpp:10-22
 ClusterTree::ClusterTree(i64 n, int tau) : n_(n), tau_(tau) {
-    levels_.resize(size_t(tau + 1));
+    levels_.resize(static_cast<size_t>(tau + 1));
     levels_[0] = {Range{0, n}};
     for (int d = 1; d <= tau; ++d) {
-        levels_[size_t(d)].reserve(size_t(1) << d);
-        for (const Range& p : levels_[size_t(d - 1)]) {
+        levels_[static_cast<size_t>(d)].reserve(static_cast<size_t>(1) << d);
+        for (const Range& p : levels_[static_cast<size_t>(d - 1)]) {
             i64 left = (p.size() + 1) / 2;
-            levels_[size_t(d)].push_back(Range{p.lo, p.lo + left});
-            levels_[size_t(d)].push_back(Range{p.lo + left, p.hi});
+            levels_[static_cast<size_t>(d)].push_back(Range{p.lo, p.lo + left});
+            levels_[static_cast<size_t>(d)].push_back(Range{p.lo + left, p.hi});
         }
     }
 }
@@ -76,20 +76,20 @@ KdOrdering build_kd_ordering(const double* c, i64 n, int d, i64 leaf_min, i64 le
             });
         }
     out.inv = order;
-    out.perm.resize(size_t(n));
-    for (i64 pos = 0; pos < n; ++pos) out.perm[size_t(order[size_t(pos)])] = pos;
+    out.perm.resize(static_cast<size_t>(n));
+    for (i64 pos = 0; pos < n; ++pos) out.perm[static_cast<size_t>(order[static_cast<size_t>(pos)])] = pos;
     return out;
 }
 
 Partition::Partition(const ClusterTree& t, int d) : depth_(d) {
     const auto& lv = t.level(d);
     nseg_ = int(lv.size());
-    hb_.resize(size_t(nseg_ + 1));
+    hb_.resize(static_cast<size_t>(nseg_ + 1));
     for (int s = 0; s < nseg_; ++s) {
-        hb_[size_t(s)] = int(lv[size_t(s)].lo);
-        max_seg_ = std::max(max_seg_, int(lv[size_t(s)].size()));
+        hb_[static_cast<size_t>(s)] = int(lv[static_cast<size_t>(s)].lo);
+        max_seg_ = std::max(max_seg_, int(lv[static_cast<size_t>(s)].size()));
     }
-    hb_[size_t(nseg_)] = int(t.size());
+    hb_[static_cast<size_t>(nseg_)] = int(t.size());
     db_.upload(hb_);
 }
 
@@ -98,10 +98,10 @@ const TileList& Partition::tiles(int rows) const {
     if (it != cache_.end()) return *it->second;
     auto tl = std::make_unique<TileList>();
     std::vector<WorkItem> items;
-    std::vector<int> first(size_t(nseg_ + 1));
+    std::vector<int> first(static_cast<size_t>(nseg_ + 1));
     for (int s = 0; s < nseg_; ++s) {
-        first[size_t(s)] = int(items.size());
-        int lo = hb_[size_t(s)], hi = hb_[size_t(s + 1)];
+        first[static_cast<size_t>(s)] = int(items.size());
+        int lo = hb_[static_cast<size_t>(s)], hi = hb_[static_cast<size_t>(s + 1)];
         int cnt = 0;
         for (int r = lo; r < hi; r += rows) {
             items.push_back(WorkItem{s, r, std::min(rows, hi - r), 0});
@@ -113,7 +113,7 @@ const TileList& Partition::tiles(int rows) const {
         }
         if (cnt > 1) tl->one_per_seg = false;
     }
-    first[size_t(nseg_)] = int(items.size());
+    first[static_cast<size_t>(nseg_)] = int(items.size());
     tl->count = int(items.size());
     tl->items.upload(items);
     tl->seg_first.upload(first);

@@ -21,9 +21,9 @@ public:
     ClusterTree(i64 n, int tau);
     i64 size() const { return n_; }
     int depth() const { return tau_; }
-    const std::vector<Range>& level(int d) const { return levels_[size_t(d)]; }
-    const std::vector<Range>& leaves() const { return levels_[size_t(tau_)]; }
-    i64 num_leaves() const { return i64(levels_[size_t(tau_)].size()); }
+    const std::vector<Range>& level(int d) const { return levels_[static_cast<size_t>(d)]; }
+    const std::vector<Range>& leaves() const { return levels_[static_cast<size_t>(tau_)]; }
+    i64 num_leaves() const { return i64(levels_[static_cast<size_t>(tau_)].size()); }
     i64 max_leaf_size() const;
     bool same_structure(const ClusterTree& o) const { return n_ == o.n_ && tau_ == o.tau_; }
 
@@ -81,8 +81,8 @@ struct DTree {
     int bmax = 0;                                    // max leaf size
     i64 n() const { return host.size(); }
     int tau() const { return host.depth(); }
-    const Partition& part(int d) const { return *parts[size_t(d)]; }
-    const Partition& leaves() const { return *parts[size_t(tau())]; }
+    const Partition& part(int d) const { return *parts[static_cast<size_t>(d)]; }
+    const Partition& leaves() const { return *parts[static_cast<size_t>(tau())]; }
 };
 using DTreeP = std::shared_ptr<const DTree>;
 

@@ -1,0 +1,177 @@
+"""GPU parity: device forward models, sketch construction and the MLE glue.
+
+The Matérn forward models are checked against the CPU oracle's restatement;
+the construction against the reference's own peeling/derivative tests
+(test_sketch.cpp) and against the oracle's build on identical inputs (same
+host-generated SketchPlan bytes); the MLE glue (mle.cpp:25-54) at config C1.
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2303_10102_b200 import hodlrgp
+
+    return hodlrgp
+
+
+def dev(H, oh):
+    return H.HodlrMatrix.from_panels(oh.export_panels())
+
+
+@pytest.mark.parametrize("nu2", [1, 3, 5])
+@pytest.mark.parametrize("scan", [False, True])
+def test_matern_apply(H, nu2, scan):
+    n = 3000
+    x = np.sort(np.random.default_rng(4).uniform(size=n))
+    v = O.randn(n, 5, 11)
+    for j in (-1, 0, 1):
+        a = O.CovOracle.matern(x, nu2, 1.3, 0.2, 1e-4, scan).apply(v, j)
+        b = H.MaternOracle(x, nu2, 1.3, 0.2, 1e-4, scan).apply(v, j)
+        assert np.linalg.norm(b - a) <= 1e-12 * np.linalg.norm(a)
+
+
+def test_matern_scan_large_chunks(H):
+    n = 1 << 18
+    x = np.sort(np.random.default_rng(5).uniform(size=n))
+    v = O.randn(n, 3, 12)
+    a = O.CovOracle.matern(x, 5, 1.0, 0.05, 1e-6, True).apply(v, 1)
+    b = H.MaternOracle(x, 5, 1.0, 0.05, 1e-6, True).apply(v, 1)
+    assert np.linalg.norm(b - a) <= 1e-11 * np.linalg.norm(a)
+
+
+def test_dense_oracle_and_counters(H):
+    a = O.Hodlr.random_spd(256, 3, 4, 10).densify()
+    o = H.DenseMatrixOracle(a)
+    v = O.randn(256, 3, 1)
+    assert np.linalg.norm(o.apply(v) - a @ v) <= 1e-13 * np.linalg.norm(a @ v)
+    assert o.counters() == (3, 0)
+
+
+def test_peeling_exact_and_budget(H):  # test_sketch.cpp:126-138
+    src = O.Hodlr.random_spd(256, 3, 4, 10)
+    a = src.densify()
+    o = H.DenseMatrixOracle(a)
+    o.reset_counters()
+    h = H.build_hodlr(o, H.ClusterTree(256, 3), 4, 123)
+    assert np.linalg.norm(h.densify() - a) <= 1e-11 * np.linalg.norm(a)
+    assert o.apply_columns() == 2 * 4 * 3 + 32
+
+
+def test_peeling_budget_c2_acceptance(H):  # acceptance.cpp:82-97 (criterion 2)
+    n, k = 1024, 8
+    tau = H.tree_depth(n, 32, 64)
+    a = O.Hodlr.random_spd(n, tau, k, 7).densify()
+    o = H.DenseMatrixOracle(a)
+    o.reset_counters()
+    h = H.build_hodlr(o, H.ClusterTree(n, tau), k, 11)
+    t = H.ClusterTree(n, tau)
+    assert np.linalg.norm(h.densify() - a) / np.linalg.norm(a) <= 1e-10
+    assert o.apply_columns() == 2 * k * tau + t.max_leaf_size()
+
+
+def test_peeling_smooth_kernel(H):  # test_sketch.cpp:140-156
+    n = 128
+    x = np.linspace(0, 1, n)
+    a = np.exp(-((x[:, None] - x[None, :]) ** 2) / (2 * 0.3 * 0.3)) + 1e-6 * np.eye(n)
+    h = H.build_hodlr(H.DenseMatrixOracle(a), H.ClusterTree(n, 2), 16, 5)
+    assert np.linalg.norm(h.densify() - a) <= 1e-9 * np.linalg.norm(a)
+
+
+def _compatible_derivative(kv, seed):
+    from tests.test_oracle_pin import _compatible_derivative as cd
+
+    return cd(kv, seed)
+
+
+def test_derivative_build_exact_and_value_bitwise(H):  # test_sketch.cpp:158-233
+    kv = O.Hodlr.random_spd(256, 3, 4, 30)
+    kd1 = _compatible_derivative(kv, 31)
+    kd2 = _compatible_derivative(kv, 32)
+    kvd = kv.densify()
+    o = H.DenseMatrixOracle(kvd, [kd1, kd2])
+    br = H.build_hodlr_with_derivatives(o, H.ClusterTree(256, 3), 4, 77)
+    plain = H.build_hodlr(o, H.ClusterTree(256, 3), 4, 77)
+    assert np.array_equal(plain.export_panels()["flat"], br.h.export_panels()["flat"])
+    d = br.deriv
+    assert np.linalg.norm(br.h.densify() - kvd) <= 1e-11 * np.linalg.norm(kvd)
+    assert np.linalg.norm(d[0].densify() - kd1) <= 1e-10 * np.linalg.norm(kd1)
+    assert np.linalg.norm(d[1].densify() - kd2) <= 1e-10 * np.linalg.norm(kd2)
+
+
+def c1_points(n=4096):
+    return np.sort(np.random.default_rng(0).uniform(size=n))
+
+
+@pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4),
+                                                    (2048, 128, 40, 5, 0.05, 1e-6)])
+def test_build_parity_vs_oracle(H, n, leaf, k, nu2, ell, nug):
+    x = np.sort(np.random.default_rng(n).uniform(size=n))
+    tau = O.tree_depth(n, leaf, 2 * leaf)
+    oo = O.CovOracle.matern(x, nu2, 1.0, ell, nug, True)
+    ob = O.Build(oo, tau, k, 0, True, p=2)
+    do = H.MaternOracle(x, nu2, 1.0, ell, nug, True)
+    db = H.build_hodlr_with_derivatives(do, H.ClusterTree(n, tau), k, 0)
+    dec_o, dec_d = ob.decisions(), db.decisions()
+    mism = int((dec_o != dec_d).any(axis=1).sum())
+    assert mism <= max(1, len(dec_o) // 100), (mism, len(dec_o))
+    if n <= 4096:
+        a0, a1 = ob.h().densify(), db.h.densify()
+        assert np.linalg.norm(a1 - a0) <= 1e-10 * np.linalg.norm(a0)
+        for j in range(2):
+            d0, d1 = ob.deriv(j).densify(), db.deriv[j].densify()
+            assert np.linalg.norm(d1 - d0) <= 1e-9 * np.linalg.norm(d0)
+
+
+def test_mle_glue_c1(H):
+    """Config C1 (BASELINE.json configs[0]): logdet/loglik, score, Fisher."""
+    n, leaf, k = 4096, 64, 24
+    x = c1_points(n)
+    tau = O.tree_depth(n, leaf, 2 * leaf)
+    oo = O.CovOracle.matern(x, 3, 1.0, 0.2, 1e-4, False)
+    K = oo.apply(np.eye(n))
+    y = np.linalg.cholesky(K) @ O.randn(n, 1, 1)[:, 0]
+    ll0, s0, f0, _ = O.mle_iteration(oo, tau, k, 0, y, 2)
+    do = H.MaternOracle(x, 3, 1.0, 0.2, 1e-4, False)
+    ll1, s1, f1, t = H.mle_iteration(do, tau, k, 0, y)
+    assert ll1 == pytest.approx(ll0, rel=1e-9)
+    assert np.allclose(s1, s0, rtol=1e-7, atol=1e-7 * np.abs(s0).max())
+    assert np.linalg.norm(f1 - f0) <= 1e-9 * np.linalg.norm(f0)
+    # dense cross-check of the HODLR approximation itself (mle.cpp dense_exact)
+    sign, ld = np.linalg.slogdet(K)
+    w = np.linalg.solve(K, y)
+    ll_dense = -0.5 * n * np.log(2 * np.pi) - 0.5 * ld - 0.5 * y @ w
+    assert abs(ll1 - ll_dense) <= 1e-6 * abs(ll_dense)
+
+
+def test_mle_glue_dense_family(H):  # test_mle.cpp:53-84 on the device
+    g = np.random.default_rng(1)
+
+    def rnd(n, shift):
+        m = g.standard_normal((n, n))
+        return m @ m.T / n + shift * np.eye(n)
+
+    n = 96
+    k0, d0, d1 = rnd(n, 4.0), rnd(n, 1.0), rnd(n, 1.0)
+    kk = k0 + 0.7 * d0 + 1.3 * d1
+    h = dev(H, O.Hodlr.from_dense(2, kk))
+    der = [dev(H, O.Hodlr.from_dense(2, d0)), dev(H, O.Hodlr.from_dense(2, d1))]
+    f = H.factorize(h, H.LEFT)
+    y = O.randn(n, 1, 907)[:, 0]
+    w = np.linalg.solve(kk, y)
+    ll = -0.5 * n * np.log(2 * np.pi) - 0.5 * np.linalg.slogdet(kk)[1] - 0.5 * y @ w
+    assert H.log_likelihood(f, y) == pytest.approx(ll, rel=1e-10)
+    kinv = np.linalg.inv(kk)
+    s = H.score(f, der, y)
+    for j, dj in enumerate((d0, d1)):
+        assert s[j] == pytest.approx(-0.5 * np.trace(kinv @ dj) + 0.5 * w @ dj @ w, rel=1e-9)
+    fi = H.fisher_information(f, der)
+    m0, m1 = kinv @ d0, kinv @ d1
+    assert fi[0, 0] == pytest.approx(0.5 * np.trace(m0 @ m0), rel=1e-9)
+    assert fi[0, 1] == pytest.approx(0.5 * np.trace(m0 @ m1), rel=1e-9)
+    assert fi[1, 1] == pytest.approx(0.5 * np.trace(m1 @ m1), rel=1e-9)
