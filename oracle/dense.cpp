@@ -52,11 +52,7 @@ Mat Mat::transpose() const {
     return t;
 }
 
-double Mat::norm() const {
-    double s = 0;
-    for (double v : a) s += v * v;
-    return std::sqrt(s);
-}
+double Mat::norm() const { return std::sqrt(pdot(a.data(), a.data(), Index(a.size()), 1, 1)); }
 
 double Mat::trace() const {
     double t = 0;
@@ -80,10 +76,27 @@ Mat operator*(double s, const Mat& x) {
     return z;
 }
 
-double dot_sum(const Mat& x, const Mat& y) {
-    double s = 0;
-    for (size_t i = 0; i < x.a.size(); ++i) s += x.a[i] * y.a[i];
-    return s;
+double dot_sum(const Mat& x, const Mat& y) { return pdot(x.data(), y.data(), Index(x.a.size()), 1, 1); }
+
+// ------------------------------------------------------------ reductions
+/// Pairwise (blocked) dot product: 4 interleaved accumulators on blocks of
+/// 64, halves combined recursively — the error behaviour of Eigen's
+/// vectorised, cache-blocked reductions rather than a sequential sum.
+double pdot(const double* a, const double* b, Index n, Index sa, Index sb) {
+    if (n <= 64) {
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        Index i = 0;
+        for (; i + 4 <= n; i += 4) {
+            s0 += a[i * sa] * b[i * sb];
+            s1 += a[(i + 1) * sa] * b[(i + 1) * sb];
+            s2 += a[(i + 2) * sa] * b[(i + 2) * sb];
+            s3 += a[(i + 3) * sa] * b[(i + 3) * sb];
+        }
+        for (; i < n; ++i) s0 += a[i * sa] * b[i * sb];
+        return (s0 + s1) + (s2 + s3);
+    }
+    const Index h = n / 2;
+    return pdot(a, b, h, sa, sb) + pdot(a + h * sa, b + h * sb, n - h, sa, sb);
 }
 
 // ------------------------------------------------------------------ GEMM
@@ -155,12 +168,7 @@ void gemm(bool ta, bool tb, Index m, Index n, Index k, double alpha, const doubl
                 bj = B + j * ldb;
             }
             double* cj = C + j * ldc;
-            for (Index i = 0; i < m; ++i) {
-                const double* ai = A + i * lda;
-                double s = 0;
-                for (Index p = 0; p < k; ++p) s += ai[p] * bj[p];
-                cj[i] += alpha * s;
-            }
+            for (Index i = 0; i < m; ++i) cj[i] += alpha * pdot(A + i * lda, bj, k, 1, 1);
         }
     }
 }
@@ -179,11 +187,7 @@ Mat matmul(const Mat& x, const Mat& y) { return matmul_t(x, false, y, false); }
 // ------------------------------------------------------------ Householder
 namespace {
 
-double sq_norm(const double* v, Index n) {
-    double s = 0;
-    for (Index i = 0; i < n; ++i) s += v[i] * v[i];
-    return s;
-}
+double sq_norm(const double* v, Index n) { return pdot(v, v, n, 1, 1); }
 
 /// Eigen MatrixBase::makeHouseholderInPlace on x[0..n): returns tau, beta;
 /// essential part overwrites x[1..n).
@@ -213,8 +217,7 @@ void apply_householder_left(double* blk, Index rows, Index cols, Index ld, const
     if (tau == 0.0) return;
     for (Index j = 0; j < cols; ++j) {
         double* cj = blk + j * ld;
-        double t = 0;
-        for (Index i = 1; i < rows; ++i) t += ess[i - 1] * cj[i];
+        double t = pdot(ess, cj + 1, rows - 1, 1, 1);
         t += cj[0];
         cj[0] -= tau * t;
         for (Index i = 1; i < rows; ++i) cj[i] -= tau * ess[i - 1] * t;

@@ -5,6 +5,7 @@
 // Each function cites the reference lines it follows.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <numeric>
 #include <random>
@@ -374,8 +375,7 @@ double HodlrMatrix::trace_product(const HodlrMatrix& a, const HodlrMatrix& b) {
         const Mat& x = a.leaf(i);
         const Mat& y = b.leaf(i);
         double s = 0;
-        for (Index c = 0; c < x.c; ++c)
-            for (Index r = 0; r < x.r; ++r) s += x(c, r) * y(r, c);
+        for (Index c = 0; c < x.c; ++c) s += pdot(&x.a[static_cast<size_t>(c)], y.col(c), x.r, x.r, 1);
         t += s;
     }
     for (int l = 1; l <= a.depth(); ++l) {
@@ -1047,9 +1047,13 @@ Mat ProductRep::densify() const {
     return a;
 }
 
+bool g_solve_association = false;
+void set_solve_association(bool on) { g_solve_association = on; }
+
 namespace {
 struct LevelFactor {
     std::vector<Mat> p, q;
+    const std::vector<HodlrFactorization::LevelBlock>* blocks = nullptr;
 };
 
 // product_rep.cpp:32-45
@@ -1062,6 +1066,12 @@ void apply_blocks_to_rows(const ClusterTree& tree, const LevelFactor& lf, int df
         if (lf.p[static_cast<size_t>(b)].c == 0) continue;
         auto rng = tree.level(df)[static_cast<size_t>(b)];
         Mat rows = m.middle_rows(rng.lo - row0, rng.size());
+        if (lf.blocks && g_solve_association) {
+            const auto& blk = (*lf.blocks)[static_cast<size_t>(b)];
+            Mat t = blk.cap.solve_transpose(matmul_t(blk.u, true, rows, false));
+            m.add_block(rng.lo - row0, 0, matmul(blk.v, t), -1.0);
+            continue;
+        }
         m.add_block(rng.lo - row0, 0, matmul(lf.p[static_cast<size_t>(b)], matmul_t(lf.q[static_cast<size_t>(b)], true, rows, false)));
     }
 }
@@ -1084,6 +1094,7 @@ ProductRep pipeline(const HodlrFactorization& f, const HodlrMatrix& b, bool inve
         const auto& nodes = tree.level(i - 1);
         const auto& lev = f.level(i);
         LevelFactor lf;
+        if (inverse) lf.blocks = &lev;
         lf.p.resize(nodes.size());
         lf.q.resize(nodes.size());
         for (size_t j = 0; j < nodes.size(); ++j) {

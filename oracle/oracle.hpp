@@ -65,6 +65,8 @@ Mat matmul_t(const Mat& x, bool tx, const Mat& y, bool ty);
 void gemm(bool ta, bool tb, Index m, Index n, Index k, double alpha, const double* A, Index lda,
           const double* B, Index ldb, double beta, double* C, Index ldc);
 double dot_sum(const Mat& x, const Mat& y);  // sum(x .* y)
+/// Pairwise-summed dot product with strides.
+double pdot(const double* a, const double* b, Index n, Index sa, Index sb);
 
 /// Use an external BLAS dgemm (scipy's bundled OpenBLAS) for large GEMMs
 /// when available; only affects the CPU timing baseline, never semantics.
@@ -409,6 +411,12 @@ struct ProductRep {
     Index size() const { return base.size(); }
     Mat densify() const;
 };
+/// Diagnostic switch (default off = the reference's association,
+/// product_rep.cpp:74-78 + :32-45: p = -(cap^{-1} v^T)^T precomputed, then
+/// rows += p (q^T rows)). On: rows -= v cap^{-T} (u^T rows) via the LU solve,
+/// the association the device path uses; identical in exact arithmetic but
+/// it avoids forming p when the capacitance is ill-conditioned.
+void set_solve_association(bool on);
 ProductRep multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 ProductRep solve_multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 double trace_product_rep(const ProductRep& p);

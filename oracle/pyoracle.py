@@ -40,6 +40,7 @@ def lib():
             "or_last_error": (C.c_char_p, []),
             "or_enable_blas": (C.c_int, [C.c_char_p, C.c_int]),
             "or_blas_backend": (C.c_char_p, []),
+            "or_set_solve_association": (None, [C.c_int]),
             "or_tree_depth": (C.c_int, [i64, i64, i64]),
             "or_tree_ranges": (C.c_int, [i64, C.c_int, lp]),
             "or_kd_ordering": (C.c_int, [i64, C.c_int, dp, i64, i64, lp, lp, ip]),
@@ -128,6 +129,11 @@ def _d(a):
 def _f(a):
     """Fortran-ordered float64 copy."""
     return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def set_solve_association(on):
+    """Diagnostic: product association of the device path (see oracle.hpp)."""
+    lib().or_set_solve_association(int(on))
 
 
 def randn(r, c, seed):
