@@ -1,0 +1,342 @@
+#!/usr/bin/env python3
+"""Benchmark: one HODLR maximum-likelihood iteration at n = 2^20 on B200.
+
+Workload = BASELINE.json configs[3] (C4): n = 2^20 sorted U[0,1] points,
+Matérn nu = 5/2 (sigma2 = 1, ell = 0.05, nugget 1e-6), leaf 128 (tau = 13),
+rank 32 + 8 oversampling (k = 40), SketchPlan seed 7. One step = build of H and
+dH/dtheta (sigma2, ell) from sketches + factorization + logdet + log-likelihood
++ solve of 4 seeded right-hand sides + score + 2x2 Fisher via exact traces
+(acceptance.cpp:297-308 plus the RHS solves). Secondary: H-matvec GB/s
+against a 2^20 x 64 N(0,1) block.
+
+Synthetic data: x ~ U[0,1] (numpy seed 0, sorted), y ~ N(0, I) (seed 1; a
+dense N(0,K) draw is infeasible at 2^20), B ~ N(0, I) n x 4 (seed 2). Inputs
+(GBs of factors) exceed L2, so no explicit flush is needed.
+
+--impl reference runs the CPU restatement of the reference (oracle/, the
+reference itself cannot be built here: Eigen is absent) on a bounded sample
+and extrapolates with the reference's O(n log^2 n) cost model.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLE-iteration time (build+logdet+solve+Fisher traces) at n=2^20"
+N_LOG2 = 20
+LEAF, K_RANK, SEED = 128, 40, 7
+NU2, SIGMA2, ELL, NUGGET = 5, 1.0, 0.05, 1e-6
+NRHS = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hodlr", choices=["hodlr", "reference"])
+    ap.add_argument("--log2n", type=int, default=N_LOG2)
+    ap.add_argument("--cpu-sample-log2", type=int, default=13)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(log2n):
+    n = 1 << log2n
+    x = np.sort(np.random.default_rng(0).uniform(size=n))
+    y = np.random.default_rng(1).standard_normal(n)
+    B = np.asfortranarray(np.random.default_rng(2).standard_normal((n, NRHS)))
+    return n, x, y, B
+
+
+def config(log2n, tau):
+    return {
+        "workload": "C4: 1D Matern-5/2 HODLR MLE iteration (BASELINE.json configs[3])",
+        "n": 1 << log2n, "leaf": LEAF, "tau": tau, "rank": K_RANK, "oversampling_included": True,
+        "nu": 2.5, "sigma2": SIGMA2, "ell": ELL, "nugget": NUGGET, "params": ["sigma2", "ell"],
+        "rhs": NRHS, "sketch_seed": SEED, "parallelism": "replicas",
+        "l2_flush": "inputs larger than L2 (factors are GBs)",
+    }
+
+
+def extrapolate(t_sample, n_sample, n):
+    """Reference cost model O(n log^2 n)."""
+    import math
+
+    return t_sample * (n / n_sample) * (math.log2(n) / math.log2(n_sample)) ** 2
+
+
+def cpu_sample(log2s, steps=1):
+    """Oracle (CPU restatement) MLE iteration on a 2^log2s sample, all host threads."""
+    from oracle import pyoracle as O
+
+    threads = os.cpu_count() or 1
+    blas = "/opt/prime-rl/.venv/lib/python3.12/site-packages/scipy.libs"
+    so = [f for f in os.listdir(blas) if f.startswith("libscipy_openblas")] if os.path.isdir(blas) else []
+    used_blas = bool(so) and O.lib().or_enable_blas(os.path.join(blas, so[0]).encode(), threads) == 1
+    n, x, y, _ = workload(log2s)
+    tau = O.tree_depth(n, LEAF, 2 * LEAF)
+    o = O.CovOracle.matern(x, NU2, SIGMA2, ELL, NUGGET, True)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.mle_iteration(o, tau, K_RANK, SEED, y, 2, cache=True)
+        times.append(time.perf_counter() - t0)
+    return times, n, threads, used_blas
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        load = [s for s in sm if s > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W, K = args.warmup, args.steps
+    _, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=max(W, 0))
+    times, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=K)
+    n = 1 << args.log2n
+    t = extrapolate(statistics.mean(times), n_s, n)
+    tau = int(np.floor(np.log2(n / LEAF)))
+    sample = (f"oracle/ CPU restatement of the reference, one MLE iteration at n=2^{args.cpu_sample_log2} "
+              f"(same C4 settings), mean {statistics.mean(times):.2f}s, extrapolated to n=2^{args.log2n} "
+              f"by n log^2 n; OpenMP at the reference's sites{', OpenBLAS dgemm' if used_blas else ''}")
+    line = {"impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": args.gpus, "steps": K,
+            "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config(args.log2n, tau),
+            "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def measure_fp64_peak(torch):
+    """cuBLAS DGEMM (DMMA) 8192^3 best of 5: the FP64 roofline denominator
+    (MEASURED_PEAKS.json has none)."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    return best
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2303_10102_b200 import hodlrgp as H
+
+    stream = torch.cuda.current_stream()
+    ctx = H.Context(local, stream.cuda_stream)
+    n, x, y, B = workload(args.log2n)
+    tau = H.tree_depth(n, LEAF, 2 * LEAF)
+    orc = H.MaternOracle(x, NU2, SIGMA2, ELL, NUGGET, True, ctx=ctx)
+    yd = torch.from_numpy(y).cuda()
+    Bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda().T  # column-major n x 4
+    Xd = torch.empty((NRHS, n), dtype=torch.float64, device="cuda").T
+    L = H.lib()
+    out_ll = H.C.c_double()
+    out_s = np.zeros(2)
+    out_f = np.zeros((2, 2), order="F")
+    out_t = np.zeros(5)
+
+    def step(ptr_y, ptr_B, ptr_X, loc):
+        H._check(L.hg_mle_evaluate(ctx.ptr, orc.ptr, tau, K_RANK, SEED, ptr_y, ptr_B, NRHS, ptr_X, loc,
+                                   H.C.byref(out_ll), H._d(out_s), H._d(out_f), H._d(out_t)))
+
+    dev_args = (yd.data_ptr(), Bd.data_ptr(), Xd.data_ptr(), H.DEVICE)
+    for _ in range(max(args.warmup, 0)):
+        step(*dev_args)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs
+    clocks = Clocks(local)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(*dev_args)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launches - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = dict(zip(["build_deriv_seconds", "factorize_seconds", "loglik_solve_seconds", "score_seconds",
+                       "fisher_seconds"], [float(v) for v in out_t]))
+    results = {"loglik": out_ll.value, "score": out_s.tolist(), "fisher": out_f.ravel().tolist()}
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- e2e through the public C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.from_numpy(y).pin_memory()
+        Bh = torch.from_numpy(np.asfortranarray(B).T.copy()).pin_memory()  # row-major (4, n) == col-major n x 4
+        Xh = torch.empty((NRHS, n), dtype=torch.float64).pin_memory()
+        host_args = (yh.data_ptr(), Bh.data_ptr(), Xh.data_ptr(), H.HOST)
+        step(*host_args)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        f0.record(stream)
+        for _ in range(args.steps):
+            step(*host_args)
+        f1.record(stream)
+        barrier()
+        wall = (time.perf_counter() - w0) / args.steps
+        ems = f0.elapsed_time(f1) / args.steps
+        if dist is not None:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": ems * 1e-3, "unit": "s", "h2d_bytes_per_step": 8 * n * (1 + NRHS),
+               "d2h_bytes_per_step": 8 * n * NRHS + 8 * 7, "wall_s_per_step": wall,
+               "path": "hg_mle_evaluate(loc=HG_HOST), pinned host y/B/X"}
+
+    # ---- kernel ledger of one profiled step (roofline of the dominant class)
+    H.prof_enable(True)
+    H.prof_read(reset=True)
+    step(*dev_args)
+    prof = H.prof_read(reset=True)
+    H.prof_enable(False)
+    fp64_peak = measure_fp64_peak(torch)
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    d = prof[dom]
+    achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    roofline = {"bound": "tensor", "kernel": f"k_{dom}", "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+                "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                "launches": d["launches"], "share_of_step": d["ms"] / sum(v["ms"] for v in prof.values())}
+    ledger = {c: {"ms": round(v["ms"], 3), "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3),
+                  "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1), "launches": v["launches"]}
+              for c, v in prof.items() if v["launches"]}
+
+    # ---- H-matvec GB/s (value HODLR of this workload)
+    hb = H.C.c_void_p()
+    H._check(L.hg_build(ctx.ptr, orc.ptr, tau, K_RANK, SEED, 0, H.C.byref(hb)))
+    hh = H.C.c_void_p()
+    H._check(L.hg_build_h(hb, H.C.byref(hh)))
+    L.hg_build_free(hb)
+    matvec = {}
+    for s in (64, 1):
+        X = torch.randn((s, n), dtype=torch.float64, device="cuda").T
+        Y = torch.empty((s, n), dtype=torch.float64, device="cuda").T
+        for _ in range(3):
+            H._check(L.hg_hodlr_matvec(ctx.ptr, hh, X.data_ptr(), n, s, Y.data_ptr(), n, H.DEVICE))
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        m0.record(stream)
+        for _ in range(reps):
+            H._check(L.hg_hodlr_matvec(ctx.ptr, hh, X.data_ptr(), n, s, Y.data_ptr(), n, H.DEVICE))
+        m1.record(stream)
+        torch.cuda.synchronize()
+        mms = m0.elapsed_time(m1) / reps
+        nbytes = 8 * n * (LEAF + K_RANK * tau) + 16 * n * s
+        flops = 2 * n * s * (LEAF + 2 * K_RANK * tau)
+        matvec[f"s{s}"] = {"ms": mms, "GB/s": nbytes / (mms * 1e-3) / 1e9, "TFLOP/s": flops / (mms * 1e-3) / 1e12,
+                           "algorithmic_bytes": nbytes}
+    L.hg_hodlr_free(hh)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    for v in matvec.values():
+        v["hbm_frac"] = v["GB/s"] / hbm
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=1)
+        t_ext = extrapolate(times[0], n_s, n)
+        cpu = {"value": t_ext, "unit": "s", "cores": threads, "kind": "port",
+               "sample": (f"oracle/ restatement, one MLE iteration at n=2^{args.cpu_sample_log2} in {times[0]:.2f}s, "
+                          f"extrapolated to n=2^{args.log2n} by n log^2 n"
+                          f"{' (OpenBLAS dgemm)' if used_blas else ''}")}
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (x~U[0,1] sorted, y~N(0,I), B~N(0,I))",
+                "config": config(args.log2n, tau), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk, "gpu_launches": launches, "stages": stages, "h_matvec": matvec,
+                "kernel_ledger": ledger, "results": results}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -170,6 +170,21 @@ hg_status hg_fisher_information(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* d
  * factorize, loglik, score, fisher seconds (device events). */
 hg_status hg_mle_iteration(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
                            double* loglik, double* score, double* fisher, double* times);
+/* The same iteration plus the solve of nrhs right-hand sides B (n x nrhs) into
+ * X, with y/B/X at `loc` (HG_HOST: copied in/out inside the call; HG_DEVICE:
+ * device pointers). times[5] = build_deriv, factorize, loglik+solves, score,
+ * fisher seconds (device events). */
+hg_status hg_mle_evaluate(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
+                          const double* B, int64_t nrhs, double* X, int loc, double* loglik, double* score,
+                          double* fisher, double* times);
+
+/* ---------------------------------------------------- kernel-level ledger */
+/* Per kernel class (seg_tn, seg_nn, leaf_mm, leaf_solve, leaf_factor, cap_lu,
+ * cap_solve, qr, form_q, oracle, reduce, other): device ms from CUDA events
+ * around each launch, algorithmic flops and bytes, launch count. Off by
+ * default; returns the number of classes written (<= 12). */
+void hg_prof_enable(int on);
+int hg_prof_read(int reset, double* ms, double* flops, double* bytes, int64_t* launches);
 
 #ifdef __cplusplus
 }

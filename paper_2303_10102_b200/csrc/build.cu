@@ -392,6 +392,11 @@ DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
     HG_LAUNCH();
     count_launch();
     cache[key] = plan;
+    // The plan is fixed for a whole fit (mle.cpp:195): keep the most recent
+    // ones alive so repeated evaluations reuse the uploaded samplers.
+    static std::vector<DSketchPlanP> recent;
+    recent.push_back(plan);
+    if (recent.size() > 2) recent.erase(recent.begin());
     return plan;
 }
 

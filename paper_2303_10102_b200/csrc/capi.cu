@@ -130,6 +130,10 @@ double scalar_result(const std::function<void(double*)>& f) {
 
 }  // namespace
 
+namespace hg {
+hg_status capi_guard(hg_ctx_t ctx, const std::function<void()>& f) { return guard(ctx, f); }
+}  // namespace hg
+
 extern "C" {
 
 const char* hg_last_error(void) { return g_err.c_str(); }

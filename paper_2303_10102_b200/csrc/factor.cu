@@ -4,6 +4,7 @@
 #include <cmath>
 
 #include "factor.cuh"
+#include "prof.cuh"
 
 namespace hg {
 
@@ -450,6 +451,7 @@ void cap_solve(const DFactor& f, int i, const double* Q, bool top_odd, bool tran
     while (thr > 8 && static_cast<size_t>(m) * thr * sizeof(double) > SMEM_CAP) thr >>= 1;
     const size_t smem = static_cast<size_t>(m) * thr * sizeof(double);
     if (smem > SMEM_CAP) throw std::length_error("cap_solve: capacitance too large for shared memory");
+    ProfScope prof(PROF_CAP_SOLVE, 2.0 * nodes * double(m) * m * w, 8.0 * nodes * (double(m) * m + 2.0 * m * w));
     set_smem(reinterpret_cast<const void*>(k_cap_solve), smem);
     CapSolveArgs g{R, w, f.cap[static_cast<size_t>(i - 1)]->get(), f.cap_piv[static_cast<size_t>(i - 1)]->get(), Q, top_odd ? 1 : 0,
                    trans ? 1 : 0, T};
@@ -466,6 +468,8 @@ void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) {
     const Partition& lv = f.tree->leaves();
     const int m = lv.max_seg();
     const size_t smem = (static_cast<size_t>(m) * (SOLVE_COLS + 1) + 16 * static_cast<size_t>(m + 1)) * sizeof(double);
+    const double rows = double(f.n());
+    ProfScope prof(PROF_LEAF_SOLVE, 2.0 * rows * m * w, 8.0 * (rows * m + 2.0 * rows * w));
     set_smem(reinterpret_cast<const void*>(k_leaf_solve), smem);
     LeafSolveArgs g{lv.dbounds(), f.bmax(), f.leaf_fac->get(), f.leaf_kind->get(), f.leaf_piv->get(), Y, ldy, w};
     dim3 grid(unsigned(lv.nseg()), unsigned(cdiv(w, SOLVE_COLS)));

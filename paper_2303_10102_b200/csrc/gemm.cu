@@ -6,6 +6,7 @@
 // with a one-step register prefetch. Split-K partials are reduced in a fixed
 // order so every result is bitwise reproducible run to run.
 #include "kernels.cuh"
+#include "prof.cuh"
 #include "tile.cuh"
 
 namespace hg {
@@ -363,6 +364,8 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
             i64 tstride, int ldt, double alpha, double beta) {
     if (ca <= 0 || cb <= 0) return;
     auto& c = current();
+    const double rows = double(p.hbounds().back() - p.hbounds().front());
+    ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
     const TileList& tl = p.tiles(SEG_CHUNK);
     const int tiles_m = cdiv(ca, TM), tiles_n = cdiv(cb, TN);
     SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
@@ -396,6 +399,8 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
         if (beta != 1.0) panel_axpby(p.hbounds().back(), w, 0.0, nullptr, 0, beta, Y, ldy);
         return;
     }
+    const double rows = double(p.hbounds().back() - p.hbounds().front());
+    ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
     const TileList& tl = p.tiles(TM);
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
     dim3 grid(unsigned(tl.count), unsigned(cdiv(w, TN)));
@@ -409,6 +414,8 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     if (w <= 0) return;
     auto& c = current();
     const int rt = cdiv(leaves.max_seg(), TM);
+    const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
+    ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + rows * w * (beta != 0.0 ? 3.0 : 2.0)));
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
     dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, TN)));
     if (trans)

@@ -3,6 +3,7 @@
 #include <cmath>
 
 #include "oracle.cuh"
+#include "prof.cuh"
 #include "tile.cuh"
 
 namespace hg {
@@ -257,6 +258,8 @@ protected:
         if (j >= 2) throw std::invalid_argument("apply_derivative: parameter index");
         const Poly P = matern_poly(nu2_, j, sigma2_, ell_);
         auto& c = current();
+        ProfScope prof(PROF_ORACLE, scan_ ? 4.0 * double(n_) * s * P.nt * P.nt : 2.0 * double(n_) * n_ * s,
+                       16.0 * double(n_) * s);
         if (!scan_) {
             dim3 grid(unsigned(cdiv(n_, TM)), unsigned(cdiv(s, TN)));
             k_matern_dense<<<grid, NT, 0, c.stream>>>(x_.get(), int(n_), P, V, ldv, s, Y, ldy);

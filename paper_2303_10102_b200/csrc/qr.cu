@@ -1,6 +1,7 @@
 // Batched (column-pivoted) Householder QR and Q formation — see qr.cuh.
 #include <cfloat>
 
+#include "prof.cuh"
 #include "qr.cuh"
 
 namespace hg {
@@ -233,6 +234,9 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     DBuf<QrDesc> dd;
     dd.upload(blocks);
     auto& c = current();
+    double rows = 0;
+    for (const auto& b : blocks) rows += b.rows;
+    ProfScope prof(PROF_QR, 2.0 * rows * w * w, 16.0 * rows * w);
     if (pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<true>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -256,6 +260,9 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     DBuf<QfDesc> dd;
     dd.upload(blocks);
     auto& c = current();
+    double rows = 0;
+    for (const auto& b : blocks) rows += b.rows;
+    ProfScope prof(PROF_FORM_Q, 4.0 * rows * w * qcols, 8.0 * rows * (w + 2.0 * qcols));
     HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     k_form_q<<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);

@@ -77,7 +77,47 @@ _SIGS = {
     "hg_score": (C.c_int, [vp, vp, C.POINTER(vp), C.c_int, dp, dp, dp]),
     "hg_fisher_information": (C.c_int, [vp, vp, C.POINTER(vp), C.c_int, dp]),
     "hg_mle_iteration": (C.c_int, [vp, vp, C.c_int, i64, u64, dp, dp, dp, dp, dp]),
+    "hg_mle_evaluate": (C.c_int, [vp, vp, C.c_int, i64, u64, vp, vp, i64, vp, C.c_int, dp, dp, dp, dp]),
+    "hg_prof_enable": (None, [C.c_int]),
+    "hg_prof_read": (C.c_int, [C.c_int, dp, dp, dp, lp]),
 }
+
+PROF_CATEGORIES = ["seg_tn", "seg_nn", "leaf_mm", "leaf_solve", "leaf_factor", "cap_lu", "cap_solve", "qr",
+                   "form_q", "oracle", "reduce", "other"]
+
+
+def prof_enable(on=True):
+    """Per-kernel-class device timing + algorithmic flop/byte ledger."""
+    lib().hg_prof_enable(int(on))
+
+
+def prof_read(reset=True):
+    k = len(PROF_CATEGORIES)
+    ms, fl, by = np.zeros(k), np.zeros(k), np.zeros(k)
+    ln = np.zeros(k, dtype=np.int64)
+    lib().hg_prof_read(int(reset), _d(ms), _d(fl), _d(by), ln.ctypes.data_as(lp))
+    return {c: dict(ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]), launches=int(ln[i]))
+            for i, c in enumerate(PROF_CATEGORIES)}
+
+
+def mle_evaluate(oracle, tau, k, seed, y, B, X, loc=HOST):
+    """One MLE iteration + the solve of B into X (hg_mle_evaluate).
+
+    y, B, X: numpy arrays (loc=HOST, pinned or pageable) or raw device pointers
+    (loc=DEVICE). Returns (loglik, score, fisher, times[5])."""
+    p = oracle.p
+    ll = C.c_double()
+    s = np.zeros(p)
+    fi = np.zeros((p, p), order="F")
+    t = np.zeros(5)
+
+    def ptr(a):
+        return a if isinstance(a, int) else a.ctypes.data
+
+    nrhs = B.shape[1] if hasattr(B, "shape") else (0 if B is None else None)
+    _check(lib().hg_mle_evaluate(oracle.ctx.ptr, oracle.ptr, tau, k, seed, ptr(y), ptr(B) if B is not None else None,
+                                 nrhs, ptr(X) if X is not None else None, loc, C.byref(ll), _d(s), _d(fi), _d(t)))
+    return ll.value, s, fi, t
 
 _lib = None
 _ctx = None
