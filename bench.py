@@ -83,7 +83,7 @@ def cpu_sample(log2s, steps=1):
     threads = os.cpu_count() or 1
     blas = "/opt/prime-rl/.venv/lib/python3.12/site-packages/scipy.libs"
     so = [f for f in os.listdir(blas) if f.startswith("libscipy_openblas")] if os.path.isdir(blas) else []
-    used_blas = bool(so) and O.lib().or_enable_blas(os.path.join(blas, so[0]).encode(), threads) == 1
+    used_blas = bool(so) and O.lib().or_enable_blas(os.path.join(blas, so[0]).encode(), 1) == 1
     n, x, y, _ = workload(log2s)
     tau = O.tree_depth(n, LEAF, 2 * LEAF)
     o = O.CovOracle.matern(x, NU2, SIGMA2, ELL, NUGGET, True)

@@ -1,9 +1,8 @@
 // Segmented FP64 GEMM engine and deterministic reductions (see kernels.cuh).
 //
-// Tile engine: 64x64 output tile per 256-thread CTA, 4x4 register micro-tile
-// per thread (rows tm+16i, cols tn+16j so that shared-memory reads are
-// contiguous/broadcast), K staged 16 at a time through padded shared memory
-// with a one-step register prefetch. Split-K partials are reduced in a fixed
+// Tile engine (tile.cuh): 64x64 output tile per 256-thread CTA on the FP64
+// tensor cores (DMMA m8n8k4), K staged 16 at a time through shared memory
+// with a one-step register prefetch of the next global tile. Split-K partials are reduced in a fixed
 // order so every result is bitwise reproducible run to run.
 #include "kernels.cuh"
 #include "prof.cuh"
@@ -13,11 +12,12 @@ namespace hg {
 
 namespace {
 
+using tile::Acc;
 using tile::KS;
+using tile::LDS;
 using tile::NT;
 using tile::TM;
 using tile::TN;
-using tile::mma16;
 constexpr int SEG_CHUNK = 512;  // rows per split-K work item
 constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
 
@@ -39,16 +39,13 @@ struct SegTnArgs {
 };
 
 __global__ void __launch_bounds__(NT) k_seg_tn(SegTnArgs g) {
-    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
     const WorkItem it = g.items[blockIdx.x];
     const int m0 = (blockIdx.y % g.tiles_m) * TM, n0 = (blockIdx.y / g.tiles_m) * TN;
-    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    const int tid = threadIdx.x;
     const int lk = tid & 15, lc = tid >> 4;
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    Acc acc;
+    acc.zero();
     double ra[4], rb[4];
     auto load = [&](int kb) {
         const int r = kb + lk;
@@ -71,25 +68,19 @@ __global__ void __launch_bounds__(NT) k_seg_tn(SegTnArgs g) {
         }
         __syncthreads();
         if (kb + KS < it.rows) load(kb + KS);
-        mma16(As, Bs, acc, tm, tn);
+        tile::mma_tile(As, Bs, acc);
         __syncthreads();
     }
     double* o = g.out + (g.direct ? i64(it.seg) : i64(blockIdx.x)) * g.ostride;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int n = n0 + tn + 16 * j;
-        if (n >= g.cb) continue;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int m = m0 + tm + 16 * i;
-            if (m >= g.ca) continue;
-            double* p = o + m + i64(n) * g.ldo;
-            if (g.direct)
-                *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
-            else
-                *p = acc[i][j];
-        }
-    }
+    tile::for_each(acc, [&](int mi, int ni, double v) {
+        const int m = m0 + mi, n = n0 + ni;
+        if (m >= g.ca || n >= g.cb) return;
+        double* p = o + m + i64(n) * g.ldo;
+        if (g.direct)
+            *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        else
+            *p = v;
+    });
 }
 
 __global__ void k_seg_reduce(const double* ws, i64 wstride, int ca, int cb, const int* seg_first, double* T,
@@ -121,17 +112,14 @@ struct SegNnArgs {
 };
 
 __global__ void __launch_bounds__(NT) k_seg_nn(SegNnArgs g) {
-    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
     const WorkItem it = g.items[blockIdx.x];
     const int n0 = blockIdx.y * TN;
-    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
+    const int tid = threadIdx.x;
     const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.tstride +
                        ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    Acc acc;
+    acc.zero();
     const int am = tid & 63, akq = tid >> 6;  // A loads: 64 rows x 4 k-phases
     const int bk = tid & 15, bn = tid >> 4;   // B loads: 16 k x 16 cols
     double ra[4], rb[4];
@@ -153,21 +141,15 @@ __global__ void __launch_bounds__(NT) k_seg_nn(SegNnArgs g) {
         }
         __syncthreads();
         if (kb + KS < g.k) load(kb + KS);
-        mma16(As, Bs, acc, tm, tn);
+        tile::mma_tile(As, Bs, acc);
         __syncthreads();
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int n = n0 + tn + 16 * j;
-        if (n >= g.w) continue;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int m = tm + 16 * i;
-            if (m >= it.rows) continue;
-            double* p = g.Y + i64(it.row0 + m) + i64(n) * g.ldy;
-            *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
-        }
-    }
+    tile::for_each(acc, [&](int m, int ni, double v) {
+        const int n = n0 + ni;
+        if (n >= g.w || m >= it.rows) return;
+        double* p = g.Y + i64(it.row0 + m) + i64(n) * g.ldy;
+        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+    });
 }
 
 // ----------------------------------------------------------------- leaf_mm
@@ -187,18 +169,15 @@ struct LeafMmArgs {
 
 template <bool TRANS>
 __global__ void __launch_bounds__(NT) k_leaf_mm(LeafMmArgs g) {
-    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
     const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
     const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * TM;
     if (r0 >= m) return;
     const int n0 = blockIdx.y * TN;
     const double* Lb = g.L + i64(b) * g.lstride;
-    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int tid = threadIdx.x;
+    Acc acc;
+    acc.zero();
     const int bk = tid & 15, bn = tid >> 4;
     double ra[4], rb[4];
     auto load = [&](int kb) {
@@ -227,21 +206,15 @@ __global__ void __launch_bounds__(NT) k_leaf_mm(LeafMmArgs g) {
         }
         __syncthreads();
         if (kb + KS < m) load(kb + KS);
-        mma16(As, Bs, acc, tm, tn);
+        tile::mma_tile(As, Bs, acc);
         __syncthreads();
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int n = n0 + tn + 16 * j;
-        if (n >= g.w) continue;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int mi = r0 + tm + 16 * i;
-            if (mi >= m) continue;
-            double* p = g.Y + i64(lo + mi) + i64(n) * g.ldy;
-            *p = g.alpha * acc[i][j] + (g.beta != 0.0 ? g.beta * *p : 0.0);
-        }
-    }
+    tile::for_each(acc, [&](int mi0, int ni, double v) {
+        const int mi = r0 + mi0, n = n0 + ni;
+        if (n >= g.w || mi >= m) return;
+        double* p = g.Y + i64(lo + mi) + i64(n) * g.ldy;
+        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+    });
 }
 
 // ------------------------------------------------------------ elementwise

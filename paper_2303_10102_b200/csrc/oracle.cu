@@ -88,10 +88,11 @@ using tile::TN;
 /// Y = K V with K(i,j) = k(|x_i - x_j|) formed tile by tile in shared memory.
 __global__ void __launch_bounds__(NT) k_matern_dense(const double* x, int n, Poly P, const double* V, i64 ldv,
                                                        int s, double* Y, i64 ldy) {
-    __shared__ double As[KS][TM + 1], Bs[KS][TN + 1];
+    __shared__ __align__(16) double As[KS][tile::LDS], Bs[KS][tile::LDS];
     const int r0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
-    const int tid = threadIdx.x, tm = tid & 15, tn = tid >> 4;
-    double acc[4][4] = {};
+    const int tid = threadIdx.x;
+    tile::Acc acc;
+    acc.zero();
     const int am = tid & 63, akq = tid >> 6, bk = tid & 15, bn = tid >> 4;
     const double xr = r0 + am < n ? x[r0 + am] : 0.0;
     for (int kb = 0; kb < n; kb += KS) {
@@ -103,17 +104,13 @@ __global__ void __launch_bounds__(NT) k_matern_dense(const double* x, int n, Pol
             Bs[bk][bn + 16 * q] = (kb + bk < n && c < s) ? V[i64(kb + bk) + i64(c) * ldv] : 0.0;
         }
         __syncthreads();
-        tile::mma16(As, Bs, acc, tm, tn);
+        tile::mma_tile(As, Bs, acc);
         __syncthreads();
     }
-    for (int j = 0; j < 4; ++j) {
-        const int c = n0 + tn + 16 * j;
-        if (c >= s) continue;
-        for (int i = 0; i < 4; ++i) {
-            const int r = r0 + tm + 16 * i;
-            if (r < n) Y[i64(r) + i64(c) * ldy] = acc[i][j];
-        }
-    }
+    tile::for_each(acc, [&](int mi, int ni, double v) {
+        const int r = r0 + mi, c = n0 + ni;
+        if (r < n && c < s) Y[i64(r) + i64(c) * ldy] = v;
+    });
 }
 
 __device__ __forceinline__ void propagate(double* st, int nt, double d, double rho) {
@@ -176,29 +173,51 @@ __global__ void k_scan_local(ScanArgs g) {
 /// locB[c] the full backward state at its first point (sequential per column;
 /// the chunk-to-chunk transfer exp(-lambda dx) is recomputed from x).
 __global__ void k_scan_carry(ScanArgs g, double lambda) {
-    const int col = blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= g.s) return;
-    double* F = g.locF + i64(col) * g.nch * 4;
-    double* B = g.locB + i64(col) * g.nch * 4;
-    double st[4];
-    for (int m = 0; m < 4; ++m) st[m] = F[m];
-    for (int c = 1; c < g.nch; ++c) {
-        const int e_prev = c * g.ch - 1, e_cur = min(g.n, (c + 1) * g.ch) - 1;
-        const double d = g.x[e_cur] - g.x[e_prev];
-        propagate(st, g.nt, d, exp(-lambda * d));
-        for (int m = 0; m < 4; ++m) {
-            st[m] += F[c * 4 + m];
-            F[c * 4 + m] = st[m];
+    // One CTA per column: chunk summaries staged in shared memory, the
+    // forward carry run by warp 0's lane 0 and the backward one by warp 1's.
+    extern __shared__ double sh[];
+    const int col = blockIdx.x, nch = g.nch;
+    double* F = g.locF + i64(col) * nch * 4;
+    double* B = g.locB + i64(col) * nch * 4;
+    double* sF = sh;
+    double* sB = sh + 4 * nch;
+    double* xe = sh + 8 * nch;  // x at each chunk's last point
+    double* xs = sh + 9 * nch;  // x at each chunk's first point
+    for (int e = threadIdx.x; e < 4 * nch; e += blockDim.x) {
+        sF[e] = F[e];
+        sB[e] = B[e];
+    }
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        xe[c] = g.x[min(g.n, (c + 1) * g.ch) - 1];
+        xs[c] = g.x[c * g.ch];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double st[4] = {sF[0], sF[1], sF[2], sF[3]};
+        for (int c = 1; c < nch; ++c) {
+            const double d = xe[c] - xe[c - 1];
+            propagate(st, g.nt, d, exp(-lambda * d));
+            for (int m = 0; m < 4; ++m) {
+                st[m] += sF[c * 4 + m];
+                sF[c * 4 + m] = st[m];
+            }
+        }
+    } else if (threadIdx.x == 32) {
+        double st[4];
+        for (int m = 0; m < 4; ++m) st[m] = sB[(nch - 1) * 4 + m];
+        for (int c = nch - 2; c >= 0; --c) {
+            const double d = xs[c + 1] - xs[c];
+            propagate(st, g.nt, d, exp(-lambda * d));
+            for (int m = 0; m < 4; ++m) {
+                st[m] += sB[c * 4 + m];
+                sB[c * 4 + m] = st[m];
+            }
         }
     }
-    for (int m = 0; m < 4; ++m) st[m] = B[(g.nch - 1) * 4 + m];
-    for (int c = g.nch - 2; c >= 0; --c) {
-        const double d = g.x[(c + 1) * g.ch] - g.x[c * g.ch];
-        propagate(st, g.nt, d, exp(-lambda * d));
-        for (int m = 0; m < 4; ++m) {
-            st[m] += B[c * 4 + m];
-            B[c * 4 + m] = st[m];
-        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4 * nch; e += blockDim.x) {
+        F[e] = sF[e];
+        B[e] = sB[e];
     }
 }
 
@@ -274,7 +293,7 @@ protected:
             ++c.launches;
             cached_lambda_ = P.lambda;
         }
-        const int ch = int(std::max<i64>(64, (n_ + 4095) / 4096));
+        const int ch = int(std::max<i64>(64, (n_ + 1023) / 1024));
         const int nch = cdiv(n_, ch);
         DVec locF(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4), locB(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4);
         ScanArgs g{dx_.get(), rho_.get(), x_.get(), int(n_), ch, nch, s, P.nt, V, ldv, Y, ldy, locF.get(),
@@ -282,7 +301,11 @@ protected:
         const int threads = nch * s;
         k_scan_local<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
         HG_LAUNCH();
-        k_scan_carry<<<cdiv(s, 32), 32, 0, c.stream>>>(g, P.lambda);
+        const size_t csm = static_cast<size_t>(nch) * 10 * sizeof(double);
+        if (csm > 48 * 1024)
+            HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_scan_carry),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+        k_scan_carry<<<s, 256, csm, c.stream>>>(g, P.lambda);
         HG_LAUNCH();
         k_scan_final<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
         HG_LAUNCH();
