@@ -115,13 +115,17 @@ __global__ void __launch_bounds__(NT) k_matern_dense(const double* x, int n, Pol
 
 __device__ __forceinline__ void propagate(double* st, int nt, double d, double rho) {
     // st_m <- rho * sum_{q<=m} C(m,q) d^{m-q} st_q
-    double ns[4];
+    // All four moments are carried (branch-free); coefficients past the
+    // kernel's degree are zero, so the extra moments never reach the output.
+    (void)nt;
     const double d2 = d * d;
-    ns[0] = st[0];
-    if (nt > 1) ns[1] = st[1] + d * st[0];
-    if (nt > 2) ns[2] = st[2] + 2.0 * d * st[1] + d2 * st[0];
-    if (nt > 3) ns[3] = st[3] + 3.0 * d * st[2] + 3.0 * d2 * st[1] + d2 * d * st[0];
-    for (int m = 0; m < nt; ++m) st[m] = rho * ns[m];
+    const double n3 = st[3] + 3.0 * d * st[2] + 3.0 * d2 * st[1] + d2 * d * st[0];
+    const double n2 = st[2] + 2.0 * d * st[1] + d2 * st[0];
+    const double n1 = st[1] + d * st[0];
+    st[0] *= rho;
+    st[1] = rho * n1;
+    st[2] = rho * n2;
+    st[3] = rho * n3;
 }
 
 __global__ void k_steps(const double* x, int n, double lambda, double* dx, double* rho) {
@@ -145,28 +149,92 @@ struct ScanArgs {
     double* locB;
     double c[4];
     double diag;  // added to the diagonal: nugget (value) - c0 (double-counted self term)
+    double lambda;
 };
 
-__global__ void k_scan_local(ScanArgs g) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.nch * g.s) return;
-    const int chunk = t % g.nch, col = t / g.nch;
-    const int lo = chunk * g.ch, hi = min(g.n, lo + g.ch);
-    const double* v = g.V + i64(col) * g.ldv;
+// Block-cooperative scan: a CTA owns one chunk of SC_CH rows x 32 columns,
+// staged in shared memory (coalesced); warp w scans rows [32w, 32w+32) of
+// every column (lane = column), sub-chunk summaries are combined by one warp.
+constexpr int SC_SUB = 32, SC_WARPS = 16, SC_CH = SC_SUB * SC_WARPS, SC_LD = 33;
+
+struct ScanSmem {
+    double* Vs;   // SC_CH x SC_LD
+    double* dxs;  // SC_CH + 1
+    double* rhs;  // SC_CH + 1
+    double* sub;  // 2 x SC_WARPS x 32 x 4 (forward / backward summaries)
+    double* cin;  // 2 x SC_WARPS x 32 x 4 (carry-ins)
+};
+
+__device__ ScanSmem scan_smem(double* sm) {
+    ScanSmem s;
+    s.Vs = sm;
+    s.dxs = s.Vs + SC_CH * SC_LD;
+    s.rhs = s.dxs + SC_CH + 1;
+    s.sub = s.rhs + SC_CH + 1;
+    s.cin = s.sub + 2 * SC_WARPS * 32 * 4;
+    return s;
+}
+
+/// Stage V[lo:hi, c0:c0+32] and the step tables; local sub-chunk scans.
+__device__ void scan_stage(const ScanArgs& g, const ScanSmem& S, int lo, int rows, int c0) {
+    for (int e = threadIdx.x; e < rows * 32; e += blockDim.x) {
+        const int r = e % rows, cc = e / rows, col = c0 + cc;
+        S.Vs[r * SC_LD + cc] = col < g.s ? g.V[i64(lo + r) + i64(col) * g.ldv] : 0.0;
+    }
+    for (int r = threadIdx.x; r <= rows; r += blockDim.x) {
+        const bool in = lo + r < g.n;
+        S.dxs[r] = in ? g.dx[lo + r] : 0.0;
+        S.rhs[r] = in ? g.rho[lo + r] : 1.0;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = w * SC_SUB, r1 = min(rows, r0 + SC_SUB);
     double st[4] = {0, 0, 0, 0};
-    for (int i = lo; i < hi; ++i) {
-        if (i > lo) propagate(st, g.nt, g.dx[i], g.rho[i]);
-        st[0] += v[i];
+    for (int r = r0; r < r1; ++r) {
+        if (r > r0) propagate(st, g.nt, S.dxs[r], S.rhs[r]);
+        st[0] += S.Vs[r * SC_LD + lane];
     }
-    double* o = g.locF + (i64(col) * g.nch + chunk) * 4;
-    for (int m = 0; m < 4; ++m) o[m] = st[m];
+    double* f = S.sub + ((0 * SC_WARPS + w) * 32 + lane) * 4;
+    for (int m = 0; m < 4; ++m) f[m] = st[m];
     for (int m = 0; m < 4; ++m) st[m] = 0.0;
-    for (int i = hi - 1; i >= lo; --i) {
-        if (i < hi - 1) propagate(st, g.nt, g.dx[i + 1], g.rho[i + 1]);
-        st[0] += v[i];
+    for (int r = r1 - 1; r >= r0; --r) {
+        if (r < r1 - 1) propagate(st, g.nt, S.dxs[r + 1], S.rhs[r + 1]);
+        st[0] += S.Vs[r * SC_LD + lane];
     }
-    o = g.locB + (i64(col) * g.nch + chunk) * 4;
-    for (int m = 0; m < 4; ++m) o[m] = st[m];
+    double* b = S.sub + ((1 * SC_WARPS + w) * 32 + lane) * 4;
+    for (int m = 0; m < 4; ++m) b[m] = st[m];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SC_CH) k_scan_local(ScanArgs g) {
+    extern __shared__ double sm[];
+    const ScanSmem S = scan_smem(sm);
+    const int chunk = blockIdx.x, c0 = blockIdx.y * 32;
+    const int lo = chunk * g.ch, rows = min(g.n, lo + g.ch) - lo;
+    scan_stage(g, S, lo, rows, c0);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, col = c0 + lane;
+    const int nsub = (rows + SC_SUB - 1) / SC_SUB;
+    if (w == 0 && col < g.s) {  // chunk forward summary at its last point
+        double st[4];
+        for (int m = 0; m < 4; ++m) st[m] = S.sub[(0 * 32 + lane) * 4 + m];
+        for (int v = 1; v < nsub; ++v) {
+            const double d = g.x[lo + min(rows, (v + 1) * SC_SUB) - 1] - g.x[lo + v * SC_SUB - 1];
+            propagate(st, g.nt, d, exp(-g.lambda * d));
+            for (int m = 0; m < 4; ++m) st[m] += S.sub[((0 * SC_WARPS + v) * 32 + lane) * 4 + m];
+        }
+        double* o = g.locF + (i64(col) * g.nch + chunk) * 4;
+        for (int m = 0; m < 4; ++m) o[m] = st[m];
+    } else if (w == 1 && col < g.s) {  // chunk backward summary at its first point
+        double st[4];
+        for (int m = 0; m < 4; ++m) st[m] = S.sub[((1 * SC_WARPS + nsub - 1) * 32 + lane) * 4 + m];
+        for (int v = nsub - 2; v >= 0; --v) {
+            const double d = g.x[lo + (v + 1) * SC_SUB] - g.x[lo + v * SC_SUB];
+            propagate(st, g.nt, d, exp(-g.lambda * d));
+            for (int m = 0; m < 4; ++m) st[m] += S.sub[((1 * SC_WARPS + v) * 32 + lane) * 4 + m];
+        }
+        double* o = g.locB + (i64(col) * g.nch + chunk) * 4;
+        for (int m = 0; m < 4; ++m) o[m] = st[m];
+    }
 }
 
 /// Carries: locF[c] becomes the full forward state at the chunk's last point,
@@ -221,36 +289,76 @@ __global__ void k_scan_carry(ScanArgs g, double lambda) {
     }
 }
 
-__global__ void k_scan_final(ScanArgs g) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.nch * g.s) return;
-    const int chunk = t % g.nch, col = t / g.nch;
-    const int lo = chunk * g.ch, hi = min(g.n, lo + g.ch);
-    const double* v = g.V + i64(col) * g.ldv;
-    double* y = g.Y + i64(col) * g.ldy;
-    double st[4] = {0, 0, 0, 0};
-    if (chunk > 0) {
-        const double* c = g.locF + (i64(col) * g.nch + chunk - 1) * 4;
-        for (int m = 0; m < 4; ++m) st[m] = c[m];
+__global__ void __launch_bounds__(SC_CH) k_scan_final(ScanArgs g) {
+    extern __shared__ double sm[];
+    const ScanSmem S = scan_smem(sm);
+    const int chunk = blockIdx.x, c0 = blockIdx.y * 32;
+    const int lo = chunk * g.ch, rows = min(g.n, lo + g.ch) - lo;
+    scan_stage(g, S, lo, rows, c0);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, col = c0 + lane;
+    const int nsub = (rows + SC_SUB - 1) / SC_SUB;
+    // Carry-ins of every sub-chunk: forward state at the row before it,
+    // backward state at the row after it (chunk carries from k_scan_carry).
+    if (w == 0) {
+        double st[4] = {0, 0, 0, 0};
+        if (chunk > 0 && col < g.s)
+            for (int m = 0; m < 4; ++m) st[m] = g.locF[(i64(col) * g.nch + chunk - 1) * 4 + m];
+        double xprev = lo > 0 ? g.x[lo - 1] : g.x[0];
+        for (int v = 0; v < nsub; ++v) {
+            for (int m = 0; m < 4; ++m) S.cin[((0 * SC_WARPS + v) * 32 + lane) * 4 + m] = st[m];
+            const double xend = g.x[lo + min(rows, (v + 1) * SC_SUB) - 1];
+            const double d = xend - xprev;
+            propagate(st, g.nt, d, exp(-g.lambda * d));
+            for (int m = 0; m < 4; ++m) st[m] += S.sub[((0 * SC_WARPS + v) * 32 + lane) * 4 + m];
+            xprev = xend;
+        }
+    } else if (w == 1) {
+        double st[4] = {0, 0, 0, 0};
+        if (chunk < g.nch - 1 && col < g.s)
+            for (int m = 0; m < 4; ++m) st[m] = g.locB[(i64(col) * g.nch + chunk + 1) * 4 + m];
+        double xnext = lo + rows < g.n ? g.x[lo + rows] : g.x[g.n - 1];
+        for (int v = nsub - 1; v >= 0; --v) {
+            for (int m = 0; m < 4; ++m) S.cin[((1 * SC_WARPS + v) * 32 + lane) * 4 + m] = st[m];
+            const double xs = g.x[lo + v * SC_SUB];
+            const double d = xnext - xs;
+            propagate(st, g.nt, d, exp(-g.lambda * d));
+            for (int m = 0; m < 4; ++m) st[m] += S.sub[((1 * SC_WARPS + v) * 32 + lane) * 4 + m];
+            xnext = xs;
+        }
     }
-    for (int i = lo; i < hi; ++i) {
-        if (i > 0) propagate(st, g.nt, g.dx[i], g.rho[i]);
-        st[0] += v[i];
-        double a = 0.0;
-        for (int m = 0; m < g.nt; ++m) a += g.c[m] * st[m];
-        y[i] = a;
+    __syncthreads();
+    const int r0 = w * SC_SUB, r1 = min(rows, r0 + SC_SUB);
+    double aF[SC_SUB];
+    double st[4];
+    for (int m = 0; m < 4; ++m) st[m] = S.cin[((0 * SC_WARPS + w) * 32 + lane) * 4 + m];
+#pragma unroll
+    for (int q = 0; q < SC_SUB; ++q) {
+        const int r = r0 + q;
+        if (r < r1) {
+            if (lo + r > 0) propagate(st, g.nt, S.dxs[r], S.rhs[r]);
+            st[0] += S.Vs[r * SC_LD + lane];
+            double a = 0.0;
+            a = g.c[0] * st[0] + g.c[1] * st[1] + g.c[2] * st[2] + g.c[3] * st[3];
+            aF[q] = a;
+        }
     }
-    for (int m = 0; m < 4; ++m) st[m] = 0.0;
-    if (chunk < g.nch - 1) {
-        const double* c = g.locB + (i64(col) * g.nch + chunk + 1) * 4;
-        for (int m = 0; m < 4; ++m) st[m] = c[m];
+    for (int m = 0; m < 4; ++m) st[m] = S.cin[((1 * SC_WARPS + w) * 32 + lane) * 4 + m];
+#pragma unroll
+    for (int q = SC_SUB - 1; q >= 0; --q) {
+        const int r = r0 + q;
+        if (r < r1) {
+            if (lo + r < g.n - 1) propagate(st, g.nt, S.dxs[r + 1], S.rhs[r + 1]);
+            const double v = S.Vs[r * SC_LD + lane];
+            st[0] += v;
+            double a = 0.0;
+            a = g.c[0] * st[0] + g.c[1] * st[1] + g.c[2] * st[2] + g.c[3] * st[3];
+            S.Vs[r * SC_LD + lane] = aF[q] + a + g.diag * v;
+        }
     }
-    for (int i = hi - 1; i >= lo; --i) {
-        if (i < g.n - 1) propagate(st, g.nt, g.dx[i + 1], g.rho[i + 1]);
-        st[0] += v[i];
-        double a = 0.0;
-        for (int m = 0; m < g.nt; ++m) a += g.c[m] * st[m];
-        y[i] += a + g.diag * v[i];
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * 32; e += blockDim.x) {
+        const int r = e % rows, cc = e / rows, cl = c0 + cc;
+        if (cl < g.s) g.Y[i64(lo + r) + i64(cl) * g.ldy] = S.Vs[r * SC_LD + cc];
     }
 }
 
@@ -293,21 +401,32 @@ protected:
             ++c.launches;
             cached_lambda_ = P.lambda;
         }
-        const int ch = int(std::max<i64>(64, (n_ + 1023) / 1024));
+        const int ch = SC_CH;
         const int nch = cdiv(n_, ch);
-        DVec locF(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4), locB(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4);
-        ScanArgs g{dx_.get(), rho_.get(), x_.get(), int(n_), ch, nch, s, P.nt, V, ldv, Y, ldy, locF.get(),
-                   locB.get(), {P.c[0], P.c[1], P.c[2], P.c[3]}, (j < 0 ? nugget_ : 0.0) - P.c[0]};
-        const int threads = nch * s;
-        k_scan_local<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
-        HG_LAUNCH();
         const size_t csm = static_cast<size_t>(nch) * 10 * sizeof(double);
-        if (csm > 48 * 1024)
+        if (csm > 220 * 1024) throw std::length_error("Matern scan: n above 2^21 not supported");
+        DVec locF(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4),
+            locB(static_cast<size_t>(nch) * static_cast<size_t>(s) * 4);
+        ScanArgs g{dx_.get(), rho_.get(), x_.get(), int(n_), ch, nch, s, P.nt, V, ldv, Y, ldy, locF.get(),
+                   locB.get(), {P.c[0], P.c[1], P.c[2], P.c[3]}, (j < 0 ? nugget_ : 0.0) - P.c[0], P.lambda};
+        const size_t ssm = (static_cast<size_t>(SC_CH) * SC_LD + 2 * (SC_CH + 1) + 4 * SC_WARPS * 32 * 4) *
+                           sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_scan_local),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm)));
+            HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_scan_final),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm)));
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_scan_carry),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            attr = true;
+        }
+        dim3 grid(unsigned(nch), unsigned(cdiv(s, 32)));
+        k_scan_local<<<grid, SC_CH, ssm, c.stream>>>(g);
+        HG_LAUNCH();
         k_scan_carry<<<s, 256, csm, c.stream>>>(g, P.lambda);
         HG_LAUNCH();
-        k_scan_final<<<cdiv(threads, 128), 128, 0, c.stream>>>(g);
+        k_scan_final<<<grid, SC_CH, ssm, c.stream>>>(g);
         HG_LAUNCH();
         c.launches += 3;
     }
