@@ -92,11 +92,13 @@ __device__ double cta_sum(double v) {
 
 /// sketch.cpp:60-74: complete deficient columns with canonical basis vectors
 /// orthogonalised twice against the kept ones (skipping norms below 0.5).
-__global__ void k_complete(const int* bounds, int k, const int* nr, double* S, i64 lds, double* scratch) {
+__global__ void k_complete(const int* bounds, int k, const int* nr, double* S, i64 lds, double* scratch,
+                           int max_rows) {
     const int j = blockIdx.x;
     int filled = nr[j];
     if (filled >= k) return;
     const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
+    if (m > max_rows) return;  // long blocks take the batched path (complete_batched)
     double* Q = S + lo;
     double* v = scratch + lo;
     __shared__ double g[512];
@@ -134,6 +136,89 @@ __global__ void k_complete(const int* bounds, int k, const int* nr, double* S, i
         for (int i = tid; i < m; i += blockDim.x) Q[i + i64(filled) * lds] = v[i] / nv;
         ++filled;
         __syncthreads();
+    }
+}
+
+/// Row-parallel S[cl] = Q diag(sign) (identity for full-width nodes).
+__global__ void k_q_sign_rows(const WorkItem* items, const int* bounds, int k, const int* qmap, const double* sign,
+                              double* S, i64 lds) {
+    const WorkItem it = items[blockIdx.x];
+    if (it.seg & 1) return;  // right children hold no basis
+    const int j = it.seg >> 1;
+    const bool full = qmap[j] < 0;
+    const int clo = bounds[2 * j];
+    for (int e = threadIdx.x; e < it.rows * k; e += blockDim.x) {
+        const int r = e % it.rows, c = e / it.rows;
+        double* p = S + i64(it.row0 + r) + i64(c) * lds;
+        if (full)
+            *p = (it.row0 + r - clo) == c ? 1.0 : 0.0;
+        else
+            *p *= sign[j * k + c];
+    }
+}
+
+/// presc partial sums: per work item and param, sum of squares of dY rows.
+__global__ void k_presc_part(const WorkItem* items, int k, int p, const double* dY, i64 ld, double* part) {
+    const WorkItem it = items[blockIdx.x];
+    for (int q = 0; q < p; ++q) {
+        double s = 0.0;
+        if (!(it.seg & 1))
+            for (int e = threadIdx.x; e < it.rows * k; e += blockDim.x) {
+                const int r = e % it.rows, c = e / it.rows;
+                const double v = dY[i64(it.row0 + r) + i64(q * k + c) * ld];
+                s += v * v;
+            }
+        s = cta_sum(s);
+        if (threadIdx.x == 0) part[i64(blockIdx.x) * p + q] = s;
+        __syncthreads();
+    }
+}
+
+__global__ void k_presc_final(int nodes, const int* seg_first, int p, const double* part, double* presc) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nodes) return;
+    double best = 0.0;
+    for (int q = 0; q < p; ++q) {
+        double s = 0.0;
+        for (int it = seg_first[2 * j]; it < seg_first[2 * j + 1]; ++it) s += part[i64(it) * p + q];
+        best = fmax(best, sqrt(s));
+    }
+    presc[j] = best;
+}
+
+/// Completion of long deficient blocks, batched (equivalent to the
+/// sequential loop of sketch.cpp:60-74 when every candidate is accepted):
+/// G_j = S[cl.lo + t, :]^T for t < c_j (the rows of the canonical candidates).
+__global__ void k_cand_rows(const int* bounds, int k, int cmax, const int* cj, const double* S, i64 lds, double* G) {
+    const int j = blockIdx.x;
+    const int lo = bounds[2 * j];
+    double* Gj = G + i64(j) * k * cmax;
+    for (int e = threadIdx.x; e < k * cmax; e += blockDim.x) {
+        const int a = e % k, t = e / k;
+        Gj[e] = t < cj[j] ? S[i64(lo + t) + i64(a) * lds] : 0.0;
+    }
+}
+
+/// W[cl.lo + t, t] += 1 (t < c_j): W = E - S G.
+__global__ void k_add_canonical(const int* bounds, const int* cj, double* W, i64 ldw) {
+    const int j = blockIdx.x;
+    const int lo = bounds[2 * j];
+    for (int t = threadIdx.x; t < cj[j]; t += blockDim.x) W[i64(lo + t) + i64(t) * ldw] += 1.0;
+}
+
+/// S[cl, nr_j + t] = sign(R_tt) Qw[cl, t] for t < c_j.
+__global__ void k_place_completion(const WorkItem* items, const int* cj, const int* nr, const double* Rw, int cmax,
+                                   const int* rmap, const double* Qw, i64 ldq, double* S, i64 lds) {
+    const WorkItem it = items[blockIdx.x];
+    if (it.seg & 1) return;
+    const int j = it.seg >> 1;
+    const int c = cj[j];
+    if (c <= 0 || rmap[j] < 0) return;
+    const double* R = Rw + i64(rmap[j]) * cmax * cmax;
+    for (int e = threadIdx.x; e < it.rows * c; e += blockDim.x) {
+        const int r = e % it.rows, t = e / it.rows;
+        const double sg = R[t + t * cmax] < 0 ? -1.0 : 1.0;
+        S[i64(it.row0 + r) + i64(nr[j] + t) * lds] = sg * Qw[i64(it.row0 + r) + i64(t) * ldq];
     }
 }
 
@@ -347,6 +432,109 @@ void compress_level(DHodlr& D, int l, double rtol) {
     }
 }
 
+constexpr int COMPLETE_BATCH_ROWS = 8192;
+
+/// sketch.cpp:60-74 for every node of a level whose numeric rank is below k.
+/// Short blocks run the sequential loop one CTA per node (k_complete). Long
+/// blocks project the canonical candidates e_0..e_{c-1} twice against the
+/// kept columns and orthonormalise them with a (TSQR) Householder QR: the
+/// sequential loop computes exactly this Q when every candidate passes the
+/// 0.5 norm test, and R_tt is that norm, so a failing test sends the node
+/// back to the sequential loop.
+void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double* S, i64 n) {
+    auto& ctx = current();
+    const int nodes = pc.nseg() / 2;
+    const auto& hb = pc.hbounds();
+    const std::vector<int> nrh = nr.download();
+    bool any_small = false;
+    std::vector<int> big, cj(static_cast<size_t>(nodes), 0), wkeep(static_cast<size_t>(nodes), k);
+    int cmax = 0;
+    for (int j = 0; j < nodes; ++j) {
+        const int m = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
+        if (nrh[static_cast<size_t>(j)] >= k) continue;
+        if (m <= COMPLETE_BATCH_ROWS) {
+            any_small = true;
+        } else {
+            big.push_back(j);
+            cj[static_cast<size_t>(j)] = k - nrh[static_cast<size_t>(j)];
+            wkeep[static_cast<size_t>(j)] = nrh[static_cast<size_t>(j)];
+            cmax = std::max(cmax, cj[static_cast<size_t>(j)]);
+        }
+    }
+    DVec scratch;
+    if (any_small) {
+        scratch.alloc(static_cast<size_t>(n));
+        k_complete<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, nr.get(), S, n, scratch.get(),
+                                                  COMPLETE_BATCH_ROWS);
+        HG_LAUNCH();
+        count_launch();
+    }
+    if (big.empty()) return;
+    DBuf<int> dcj, dkeep;
+    dcj.upload(cj);
+    dkeep.upload(wkeep);
+    k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dkeep.get(), k, S, n);
+    HG_LAUNCH();
+    DVec G(static_cast<size_t>(nodes) * k * cmax), H(static_cast<size_t>(2 * nodes) * k * cmax),
+        W(static_cast<size_t>(n) * cmax);
+    k_cand_rows<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, cmax, dcj.get(), S, n, G.get());
+    HG_LAUNCH();
+    seg_nn(pc, S, n, k, G.get(), i64(k) * cmax, k, TMap::parent(0, 0), W.get(), n, cmax, -1.0, 0.0);
+    k_add_canonical<<<nodes, 64, 0, ctx.stream>>>(pc.dbounds(), dcj.get(), W.get(), n);
+    HG_LAUNCH();
+    seg_tn(pc, S, n, k, W.get(), n, cmax, H.get(), i64(k) * cmax, k);
+    seg_nn(pc, S, n, k, H.get(), i64(k) * cmax, k, TMap::same(), W.get(), n, cmax, -1.0, 1.0);
+    k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dcj.get(), cmax, W.get(), n);
+    HG_LAUNCH();
+    ctx.launches += 4;
+    std::vector<BatchedQR::Block> blocks;
+    std::vector<int> rmap(static_cast<size_t>(nodes), -1);
+    for (int j : big) {
+        rmap[static_cast<size_t>(j)] = int(blocks.size());
+        blocks.push_back({W.get() + hb[static_cast<size_t>(2 * j)], n,
+                          hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)]});
+    }
+    BatchedQR qr(blocks, cmax, false);
+    std::vector<double> Rh(blocks.size() * static_cast<size_t>(cmax) * cmax);
+    HG_CUDA(cudaMemcpyAsync(Rh.data(), qr.R(), Rh.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    sync();
+    std::vector<int> fallback_nr(static_cast<size_t>(nodes), k);
+    bool any_fallback = false;
+    for (int j : big) {
+        const double* R = Rh.data() + static_cast<size_t>(rmap[static_cast<size_t>(j)]) * cmax * cmax;
+        for (int t = 0; t < cj[static_cast<size_t>(j)]; ++t)
+            if (std::abs(R[t + t * cmax]) < 0.5) {
+                rmap[static_cast<size_t>(j)] = -1;
+                fallback_nr[static_cast<size_t>(j)] = nrh[static_cast<size_t>(j)];
+                any_fallback = true;
+                break;
+            }
+    }
+    DVec Qw(static_cast<size_t>(n) * cmax);
+    std::vector<double*> qo;
+    std::vector<i64> ql;
+    for (int j : big) {
+        qo.push_back(Qw.get() + hb[static_cast<size_t>(2 * j)]);
+        ql.push_back(n);
+    }
+    qr.form_q(cmax, nullptr, 0, 0, qo, ql);
+    DBuf<int> drmap;
+    drmap.upload(rmap);
+    const TileList& tl = pc.tiles(256);
+    k_place_completion<<<tl.count, 256, 0, ctx.stream>>>(tl.items.get(), dcj.get(), nr.get(), qr.R(), cmax,
+                                                         drmap.get(), Qw.get(), n, S, n);
+    HG_LAUNCH();
+    count_launch();
+    if (any_fallback) {
+        DBuf<int> dfb;
+        dfb.upload(fallback_nr);
+        if (scratch.empty()) scratch.alloc(static_cast<size_t>(n));
+        k_complete<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, dfb.get(), S, n, scratch.get(), 1 << 30);
+        HG_LAUNCH();
+        count_launch();
+    }
+}
+
 /// Y = K X - H X with H restricted to levels < l (peeling), full n x s panels.
 void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y) {
     const i64 n = H.n();
@@ -467,12 +655,12 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                                                         qr ? qr->perm() : dummyP.get(), Rn.get(), perm.get(),
                                                         sign.get(), nr.get());
             HG_LAUNCH();
-            k_q_sign<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, dqmap.get(), sign.get(), S.get(), n);
+            const TileList& tl256 = pc.tiles(256);
+            k_q_sign_rows<<<tl256.count, 256, 0, ctx.stream>>>(tl256.items.get(), pc.dbounds(), k, dqmap.get(),
+                                                               sign.get(), S.get(), n);
             HG_LAUNCH();
-            DVec scratch(static_cast<size_t>(n));
-            k_complete<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, nr.get(), S.get(), n, scratch.get());
-            HG_LAUNCH();
-            ctx.launches += 3;
+            ctx.launches += 2;
+            complete_deficient(pc, k, nr, S.get(), n);
         }
         // Pass 2: Z = K S - H S (sketch.cpp:177-183).
         DVec Z(static_cast<size_t>(n) * k);
@@ -487,9 +675,16 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         if (p > 0) {
             DVec resid(static_cast<size_t>(n) * kp), presc(static_cast<size_t>(nodes)), G(static_cast<size_t>(2 * nodes) * k * kp);
             panel_axpby(n, kp, 1.0, dY.get(), n, 0.0, resid.get(), n);
-            k_presc<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), k, p, dY.get(), n, presc.get());
-            HG_LAUNCH();
-            ++ctx.launches;
+            {
+                const TileList& tl = pc.tiles(2048);
+                DVec part(static_cast<size_t>(tl.count) * p);
+                k_presc_part<<<tl.count, 256, 0, ctx.stream>>>(tl.items.get(), k, p, dY.get(), n, part.get());
+                HG_LAUNCH();
+                k_presc_final<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, tl.seg_first.get(), p, part.get(),
+                                                                      presc.get());
+                HG_LAUNCH();
+                ctx.launches += 2;
+            }
             for (int pass = 0; pass < 2; ++pass) {
                 seg_tn(pc, S.get(), n, k, resid.get(), n, kp, G.get(), i64(k) * kp, k);
                 seg_nn(pc, S.get(), n, k, G.get(), i64(k) * kp, k, TMap::same(), resid.get(), n, kp, -1.0, 1.0);
