@@ -157,6 +157,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def reduce_max(value, dist, device="cuda"):
+    """Max over ranks (replicas time their own GPU; the job is as slow as the slowest)."""
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measure_fp64_peak(torch):
     """cuBLAS DGEMM (DMMA) 8192^3 best of 5: the FP64 roofline denominator
     (MEASURED_PEAKS.json has none)."""
@@ -236,10 +247,7 @@ def main():
     stages = dict(zip(["build_deriv_seconds", "factorize_seconds", "loglik_solve_seconds", "score_seconds",
                        "fisher_seconds"], [float(v) for v in out_t]))
     results = {"loglik": out_ll.value, "score": out_s.tolist(), "fisher": out_f.ravel().tolist()}
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max(ms, dist)
 
     # ---- e2e through the public C ABI with pinned host buffers
     e2e = None
@@ -259,10 +267,7 @@ def main():
         barrier()
         wall = (time.perf_counter() - w0) / args.steps
         ems = f0.elapsed_time(f1) / args.steps
-        if dist is not None:
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = reduce_max(ems, dist)
         e2e = {"value": ems * 1e-3, "unit": "s", "h2d_bytes_per_step": 8 * n * (1 + NRHS),
                "d2h_bytes_per_step": 8 * n * NRHS + 8 * 7, "wall_s_per_step": wall,
                "path": "hg_mle_evaluate(loc=HG_HOST), pinned host y/B/X"}
