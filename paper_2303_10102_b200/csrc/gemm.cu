@@ -13,11 +13,11 @@ namespace hg {
 namespace {
 
 using tile::Acc;
-using tile::KS;
-using tile::LDS;
-using tile::NT;
-using tile::TM;
-using tile::TN;
+using tile::BK;
+using tile::BM;
+using tile::BN;
+using tile::THREADS;
+__device__ __forceinline__ int cdiv_d(int a, int b) { return (a + b - 1) / b; }
 constexpr int SEG_CHUNK = 512;  // rows per split-K work item
 constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
 
@@ -38,39 +38,16 @@ struct SegTnArgs {
     double alpha, beta;
 };
 
-__global__ void __launch_bounds__(NT) k_seg_tn(SegTnArgs g) {
-    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
+/// T_s tile = A[rows]^T B[rows]: both operands k-contiguous (rows = k).
+__global__ void __launch_bounds__(THREADS) k_seg_tn(SegTnArgs g) {
+    extern __shared__ double smem[];
     const WorkItem it = g.items[blockIdx.x];
-    const int m0 = (blockIdx.y % g.tiles_m) * TM, n0 = (blockIdx.y / g.tiles_m) * TN;
-    const int tid = threadIdx.x;
-    const int lk = tid & 15, lc = tid >> 4;
+    const int m0 = (blockIdx.y % g.tiles_m) * BM, n0 = (blockIdx.y / g.tiles_m) * BN;
+    tile::LoadKC la{g.A + it.row0 + i64(m0) * g.lda, g.lda, it.rows, g.ca - m0};
+    tile::LoadKC lb{g.B + it.row0 + i64(n0) * g.ldb, g.ldb, it.rows, g.cb - n0};
     Acc acc;
     acc.zero();
-    double ra[4], rb[4];
-    auto load = [&](int kb) {
-        const int r = kb + lk;
-        const bool rv = r < it.rows;
-        const i64 row = i64(it.row0) + r;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int m = m0 + lc + 16 * q;
-            ra[q] = (rv && m < g.ca) ? g.A[row + i64(m) * g.lda] : 0.0;
-            const int n = n0 + lc + 16 * q;
-            rb[q] = (rv && n < g.cb) ? g.B[row + i64(n) * g.ldb] : 0.0;
-        }
-    };
-    load(0);
-    for (int kb = 0; kb < it.rows; kb += KS) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            As[lk][lc + 16 * q] = ra[q];
-            Bs[lk][lc + 16 * q] = rb[q];
-        }
-        __syncthreads();
-        if (kb + KS < it.rows) load(kb + KS);
-        tile::mma_tile(As, Bs, acc);
-        __syncthreads();
-    }
+    tile::run(la, lb, cdiv_d(it.rows, BK), smem, acc);
     double* o = g.out + (g.direct ? i64(it.seg) : i64(blockIdx.x)) * g.ostride;
     tile::for_each(acc, [&](int mi, int ni, double v) {
         const int m = m0 + mi, n = n0 + ni;
@@ -111,39 +88,18 @@ struct SegNnArgs {
     double alpha, beta;
 };
 
-__global__ void __launch_bounds__(NT) k_seg_nn(SegNnArgs g) {
-    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
+/// Y[rows] = X[rows] T_sel: X m-contiguous (rows = m), T k-contiguous.
+__global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
+    extern __shared__ double smem[];
     const WorkItem it = g.items[blockIdx.x];
-    const int n0 = blockIdx.y * TN;
-    const int tid = threadIdx.x;
-    const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.tstride +
-                       ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
+    const int n0 = blockIdx.y * BN;
+    const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.map.mult * g.tstride +
+                       i64(g.map.add) * g.tstride + ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
+    tile::LoadMC la{g.X + it.row0, g.ldx, it.rows, g.k};
+    tile::LoadKC lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
     Acc acc;
     acc.zero();
-    const int am = tid & 63, akq = tid >> 6;  // A loads: 64 rows x 4 k-phases
-    const int bk = tid & 15, bn = tid >> 4;   // B loads: 16 k x 16 cols
-    double ra[4], rb[4];
-    auto load = [&](int kb) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int kk = akq + 4 * q;
-            ra[q] = (am < it.rows && kb + kk < g.k) ? g.X[i64(it.row0 + am) + i64(kb + kk) * g.ldx] : 0.0;
-            const int n = n0 + bn + 16 * q;
-            rb[q] = (kb + bk < g.k && n < g.w) ? Tb[(kb + bk) + i64(n) * g.ldt] : 0.0;
-        }
-    };
-    load(0);
-    for (int kb = 0; kb < g.k; kb += KS) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            As[akq + 4 * q][am] = ra[q];
-            Bs[bk][bn + 16 * q] = rb[q];
-        }
-        __syncthreads();
-        if (kb + KS < g.k) load(kb + KS);
-        tile::mma_tile(As, Bs, acc);
-        __syncthreads();
-    }
+    tile::run(la, lb, cdiv_d(g.k, BK), smem, acc);
     tile::for_each(acc, [&](int m, int ni, double v) {
         const int n = n0 + ni;
         if (n >= g.w || m >= it.rows) return;
@@ -167,47 +123,25 @@ struct LeafMmArgs {
     double alpha, beta;
 };
 
+/// Y[leaf rows] = op(L_b) X[leaf rows]; op(L) is m-contiguous (no transpose)
+/// or k-contiguous (transpose), X is k-contiguous.
 template <bool TRANS>
-__global__ void __launch_bounds__(NT) k_leaf_mm(LeafMmArgs g) {
-    __shared__ __align__(16) double As[KS][LDS], Bs[KS][LDS];
+__global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
+    extern __shared__ double smem[];
     const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
-    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * TM;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * BM;
     if (r0 >= m) return;
-    const int n0 = blockIdx.y * TN;
+    const int n0 = blockIdx.y * BN;
     const double* Lb = g.L + i64(b) * g.lstride;
-    const int tid = threadIdx.x;
+    tile::LoadKC lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
     Acc acc;
     acc.zero();
-    const int bk = tid & 15, bn = tid >> 4;
-    double ra[4], rb[4];
-    auto load = [&](int kb) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!TRANS) {
-                const int i = tid & 63, kk = (tid >> 6) + 4 * q;
-                ra[q] = (r0 + i < m && kb + kk < m) ? Lb[(r0 + i) + i64(kb + kk) * g.ldl] : 0.0;
-            } else {
-                const int kk = tid & 15, i = (tid >> 4) + 16 * q;
-                ra[q] = (r0 + i < m && kb + kk < m) ? Lb[(kb + kk) + i64(r0 + i) * g.ldl] : 0.0;
-            }
-            const int n = n0 + bn + 16 * q;
-            rb[q] = (kb + bk < m && n < g.w) ? g.X[i64(lo + kb + bk) + i64(n) * g.ldx] : 0.0;
-        }
-    };
-    load(0);
-    for (int kb = 0; kb < m; kb += KS) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!TRANS)
-                As[(tid >> 6) + 4 * q][tid & 63] = ra[q];
-            else
-                As[tid & 15][(tid >> 4) + 16 * q] = ra[q];
-            Bs[bk][bn + 16 * q] = rb[q];
-        }
-        __syncthreads();
-        if (kb + KS < m) load(kb + KS);
-        tile::mma_tile(As, Bs, acc);
-        __syncthreads();
+    if (!TRANS) {
+        tile::LoadMC la{Lb + r0, g.ldl, m - r0, m};
+        tile::run(la, lb, cdiv_d(m, BK), smem, acc);
+    } else {
+        tile::LoadKC la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
+        tile::run(la, lb, cdiv_d(m, BK), smem, acc);
     }
     tile::for_each(acc, [&](int mi0, int ni, double v) {
         const int mi = r0 + mi0, n = n0 + ni;
@@ -331,6 +265,17 @@ void reduce(F f, i64 total, double* out, bool accumulate) {
     c.launches += 2;
 }
 
+void smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    const void* fns[] = {reinterpret_cast<const void*>(k_seg_tn), reinterpret_cast<const void*>(k_seg_nn),
+                         reinterpret_cast<const void*>(k_leaf_mm<true>),
+                         reinterpret_cast<const void*>(k_leaf_mm<false>)};
+    for (const void* f : fns)
+        HG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tile::SMEM_BYTES));
+    done = true;
+}
+
 }  // namespace
 
 void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* B, i64 ldb, int cb, double* T,
@@ -340,11 +285,12 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
     const TileList& tl = p.tiles(SEG_CHUNK);
-    const int tiles_m = cdiv(ca, TM), tiles_n = cdiv(cb, TN);
+    const int tiles_m = cdiv(ca, BM), tiles_n = cdiv(cb, BN);
+    smem_attrs();
     SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
     dim3 grid(unsigned(tl.count), unsigned(tiles_m * tiles_n));
     if (tl.one_per_seg) {
-        k_seg_tn<<<grid, NT, 0, c.stream>>>(g);
+        k_seg_tn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
         HG_LAUNCH();
         ++c.launches;
         return;
@@ -355,7 +301,7 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     g.ostride = wstride;
     g.ldo = ca;
     g.direct = 0;
-    k_seg_tn<<<grid, NT, 0, c.stream>>>(g);
+    k_seg_tn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
     HG_LAUNCH();
     dim3 rgrid(unsigned(cdiv(wstride, 256)), unsigned(p.nseg()));
     k_seg_reduce<<<rgrid, 256, 0, c.stream>>>(ws.get(), wstride, ca, cb, tl.seg_first.get(), T, tstride, ldt, alpha,
@@ -374,10 +320,11 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     }
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
-    const TileList& tl = p.tiles(TM);
+    const TileList& tl = p.tiles(BM);
+    smem_attrs();
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
-    dim3 grid(unsigned(tl.count), unsigned(cdiv(w, TN)));
-    k_seg_nn<<<grid, NT, 0, c.stream>>>(g);
+    dim3 grid(unsigned(tl.count), unsigned(cdiv(w, BN)));
+    k_seg_nn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
     HG_LAUNCH();
     ++c.launches;
 }
@@ -386,15 +333,16 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
              double* Y, i64 ldy, int w, double alpha, double beta) {
     if (w <= 0) return;
     auto& c = current();
-    const int rt = cdiv(leaves.max_seg(), TM);
+    const int rt = cdiv(leaves.max_seg(), BM);
+    smem_attrs();
     const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
     ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + rows * w * (beta != 0.0 ? 3.0 : 2.0)));
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
-    dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, TN)));
+    dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, BN)));
     if (trans)
-        k_leaf_mm<true><<<grid, NT, 0, c.stream>>>(g);
+        k_leaf_mm<true><<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
     else
-        k_leaf_mm<false><<<grid, NT, 0, c.stream>>>(g);
+        k_leaf_mm<false><<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
     HG_LAUNCH();
     ++c.launches;
 }

@@ -15,12 +15,14 @@
 namespace hg {
 
 /// Selects the small right factor of segment s in seg_nn:
-/// index = (s >> shift) ^ xr; first row = (s & 1) ? row_odd : row_even.
+/// index = ((s >> shift) ^ xr) * mult + add; first row = (s & 1) ? row_odd : row_even.
 struct TMap {
-    int shift = 0, xr = 0, row_even = 0, row_odd = 0;
+    int shift = 0, xr = 0, row_even = 0, row_odd = 0, mult = 1, add = 0;
     static TMap same() { return TMap{}; }
-    static TMap sibling() { return TMap{0, 1, 0, 0}; }
-    static TMap parent(int re, int ro) { return TMap{1, 0, re, ro}; }
+    static TMap sibling() { return TMap{0, 1, 0, 0, 1, 0}; }
+    static TMap parent(int re, int ro) { return TMap{1, 0, re, ro, 1, 0}; }
+    /// child (2s + c) of segment s of a coarser partition
+    static TMap child(int c) { return TMap{0, 0, 0, 0, 2, c}; }
 };
 
 /// T_s (ca x cb, col-major, ld ldt, stride tstride per segment) =

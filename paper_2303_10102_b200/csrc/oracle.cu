@@ -80,33 +80,38 @@ __device__ __forceinline__ double poly_eval(const Poly& P, double d) {
     return p * exp(-P.lambda * d);
 }
 
-using tile::KS;
-using tile::NT;
-using tile::TM;
-using tile::TN;
+using tile::BK;
+using tile::BM;
+using tile::BN;
+
+/// Kernel tile K(r0 + m, kt*BK + k) computed straight into the m-contiguous
+/// shared layout (a computing loader for tile::run).
+struct LoadMatern {
+    static constexpr bool KC = false;
+    const double* x;
+    int r0, n;
+    Poly P;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        const int m = threadIdx.x & 63;
+        const double xr = r0 + m < n ? x[r0 + m] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = (threadIdx.x >> 6) + 2 * q, kk = kt * BK + k;
+            S[k * tile::LD_MC + m] = (r0 + m < n && kk < n) ? poly_eval(P, fabs(xr - x[kk])) : 0.0;
+        }
+    }
+};
 
 /// Y = K V with K(i,j) = k(|x_i - x_j|) formed tile by tile in shared memory.
-__global__ void __launch_bounds__(NT) k_matern_dense(const double* x, int n, Poly P, const double* V, i64 ldv,
-                                                       int s, double* Y, i64 ldy) {
-    __shared__ __align__(16) double As[KS][tile::LDS], Bs[KS][tile::LDS];
-    const int r0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
-    const int tid = threadIdx.x;
+__global__ void __launch_bounds__(tile::THREADS) k_matern_dense(const double* x, int n, Poly P, const double* V,
+                                                                i64 ldv, int s, double* Y, i64 ldy) {
+    extern __shared__ double smem[];
+    const int r0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    LoadMatern la{x, r0, n, P};
+    tile::LoadKC lb{V + i64(n0) * ldv, ldv, n, s - n0};
     tile::Acc acc;
     acc.zero();
-    const int am = tid & 63, akq = tid >> 6, bk = tid & 15, bn = tid >> 4;
-    const double xr = r0 + am < n ? x[r0 + am] : 0.0;
-    for (int kb = 0; kb < n; kb += KS) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int kk = akq + 4 * q;
-            As[kk][am] = (r0 + am < n && kb + kk < n) ? poly_eval(P, fabs(xr - x[kb + kk])) : 0.0;
-            const int c = n0 + bn + 16 * q;
-            Bs[bk][bn + 16 * q] = (kb + bk < n && c < s) ? V[i64(kb + bk) + i64(c) * ldv] : 0.0;
-        }
-        __syncthreads();
-        tile::mma_tile(As, Bs, acc);
-        __syncthreads();
-    }
+    tile::run(la, lb, (n + BK - 1) / BK, smem, acc);
     tile::for_each(acc, [&](int mi, int ni, double v) {
         const int r = r0 + mi, c = n0 + ni;
         if (r < n && c < s) Y[i64(r) + i64(c) * ldy] = v;
@@ -388,8 +393,15 @@ protected:
         ProfScope prof(PROF_ORACLE, scan_ ? 4.0 * double(n_) * s * P.nt * P.nt : 2.0 * double(n_) * n_ * s,
                        16.0 * double(n_) * s);
         if (!scan_) {
-            dim3 grid(unsigned(cdiv(n_, TM)), unsigned(cdiv(s, TN)));
-            k_matern_dense<<<grid, NT, 0, c.stream>>>(x_.get(), int(n_), P, V, ldv, s, Y, ldy);
+            static bool attr = false;
+            if (!attr) {
+                HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_matern_dense),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tile::SMEM_BYTES));
+                attr = true;
+            }
+            dim3 grid(unsigned(cdiv(n_, BM)), unsigned(cdiv(s, BN)));
+            k_matern_dense<<<grid, tile::THREADS, tile::SMEM_BYTES, c.stream>>>(x_.get(), int(n_), P, V, ldv, s, Y,
+                                                                                ldy);
             HG_LAUNCH();
             ++c.launches;
             if (j < 0 && nugget_ != 0.0) panel_axpby(n_, s, nugget_, V, ldv, 1.0, Y, ldy);
