@@ -18,6 +18,10 @@ using tile::BM;
 using tile::BN;
 using tile::THREADS;
 __device__ __forceinline__ int cdiv_d(int a, int b) { return (a + b - 1) / b; }
+// Short-K GEMMs (seg_nn: k = rank; leaf_mm: k = leaf size) are latency-bound:
+// two stages (40 KB) keep five CTAs resident per SM instead of three.
+constexpr int NS_SHORT = 2;
+constexpr int SMEM_SHORT = tile::smem_bytes(NS_SHORT);
 constexpr int SEG_CHUNK = 512;  // rows per split-K work item
 constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
 
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
     tile::LoadKC lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
     Acc acc;
     acc.zero();
-    tile::run(la, lb, cdiv_d(g.k, BK), smem, acc);
+    tile::run<NS_SHORT>(la, lb, cdiv_d(g.k, BK), smem, acc);
     tile::for_each(acc, [&](int m, int ni, double v) {
         const int n = n0 + ni;
         if (n >= g.w || m >= it.rows) return;
@@ -138,10 +142,10 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     acc.zero();
     if (!TRANS) {
         tile::LoadMC la{Lb + r0, g.ldl, m - r0, m};
-        tile::run(la, lb, cdiv_d(m, BK), smem, acc);
+        tile::run<NS_SHORT>(la, lb, cdiv_d(m, BK), smem, acc);
     } else {
         tile::LoadKC la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
-        tile::run(la, lb, cdiv_d(m, BK), smem, acc);
+        tile::run<NS_SHORT>(la, lb, cdiv_d(m, BK), smem, acc);
     }
     tile::for_each(acc, [&](int mi0, int ni, double v) {
         const int mi = r0 + mi0, n = n0 + ni;
@@ -324,7 +328,7 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     smem_attrs();
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
     dim3 grid(unsigned(tl.count), unsigned(cdiv(w, BN)));
-    k_seg_nn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
+    k_seg_nn<<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
     HG_LAUNCH();
     ++c.launches;
 }
@@ -340,9 +344,9 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
     dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, BN)));
     if (trans)
-        k_leaf_mm<true><<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
+        k_leaf_mm<true><<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
     else
-        k_leaf_mm<false><<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
+        k_leaf_mm<false><<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
     HG_LAUNCH();
     ++c.launches;
 }

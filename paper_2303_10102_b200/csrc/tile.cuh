@@ -80,12 +80,12 @@ __device__ __forceinline__ void mma_stage(const double* As, const double* Bs, Ac
 /// Pipelined main loop. Loader objects provide
 ///   static constexpr bool KC;
 ///   __device__ void issue(double* stage, int kt);   // cp.async one BK slice
-template <class LA, class LB>
+template <int NS = STAGES, class LA, class LB>
 __device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Acc& acc) {
     double* As = smem;
-    double* Bs = smem + STAGES * TILE_ELEMS;
+    double* Bs = smem + NS * TILE_ELEMS;
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
+    for (int s = 0; s < NS - 1; ++s) {
         if (s < ktiles) {
             la.issue(As + s * TILE_ELEMS, s);
             lb.issue(Bs + s * TILE_ELEMS, s);
@@ -93,21 +93,22 @@ __device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Ac
         cp_commit();
     }
     for (int kt = 0; kt < ktiles; ++kt) {
-        cp_wait<STAGES - 2>();
-        __syncthreads();
-        const int st = kt % STAGES;
-        mma_stage<LA::KC, LB::KC>(As + st * TILE_ELEMS, Bs + st * TILE_ELEMS, acc);
-        const int nk = kt + STAGES - 1;
+        cp_wait<NS - 2>();
+        __syncthreads();  // tile kt landed; every warp is done with tile kt-1's buffer
+        const int nk = kt + NS - 1;
         if (nk < ktiles) {
-            la.issue(As + (nk % STAGES) * TILE_ELEMS, nk);
-            lb.issue(Bs + (nk % STAGES) * TILE_ELEMS, nk);
+            la.issue(As + (nk % NS) * TILE_ELEMS, nk);
+            lb.issue(Bs + (nk % NS) * TILE_ELEMS, nk);
         }
         cp_commit();
+        const int st = kt % NS;
+        mma_stage<LA::KC, LB::KC>(As + st * TILE_ELEMS, Bs + st * TILE_ELEMS, acc);
     }
     cp_wait<0>();
 }
 
-constexpr int SMEM_BYTES = 2 * STAGES * TILE_ELEMS * int(sizeof(double));
+constexpr int smem_bytes(int ns) { return 2 * ns * TILE_ELEMS * int(sizeof(double)); }
+constexpr int SMEM_BYTES = smem_bytes(STAGES);
 
 /// Column-major operand whose rows are the reduction index k (k-contiguous):
 /// element (k, m) at base[k + m * ld], valid for k < kmax, m < mmax.
