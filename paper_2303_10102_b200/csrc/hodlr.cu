@@ -221,8 +221,10 @@ void DHodlr::make_asymmetric() {
     }
 }
 
-void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
-                 bool with_leaves, bool transpose, double beta, double alpha) {
+/// Reference implementation of hodlr_apply, one segmented GEMM pair per level
+/// (kept for testing the level-fused kernels in mlapply.cu).
+void hodlr_apply_levelwise(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin,
+                           int lmax, bool with_leaves, bool transpose, double beta, double alpha) {
     if (s <= 0) return;
     const i64 n = h.n();
     if (with_leaves && !h.leaves_zero) {

@@ -1,0 +1,331 @@
+// Level-fused HODLR apply: Y = beta Y + alpha H_sel X with H_sel the levels
+// [lmin, lmax] (+ leaves), in three launches whatever the number of levels:
+//   1. k_ml_proj   T_l[s] = V_l[s]^T X[s] for every level at once (work items
+//                  ordered chunk-major so X stays L2-resident across levels);
+//   2. k_ml_reduce deterministic sum of the split-K partials (coarse levels);
+//   3. k_ml_update Y[tile] (+)= sum_l U_l[tile] T_l[sib(s_l)] — one GEMM whose
+//                  K runs over the concatenated level ranks, so Y is read and
+//                  written once.
+// Reference: HodlrMatrix::matvec / sub_matvec (hodlr_matrix.cpp:198-265).
+#include <algorithm>
+#include <mutex>
+
+#include "hodlr.cuh"
+#include "prof.cuh"
+#include "tile.cuh"
+
+namespace hg {
+
+namespace {
+
+using tile::Acc;
+using tile::BK;
+using tile::BM;
+using tile::BN;
+using tile::THREADS;
+
+constexpr int MAXL = 24;
+constexpr int ML_CHUNK = 512;
+
+struct MlLevels {
+    int nl;
+    int depth[MAXL];        // partition depth of level l (= l)
+    int R[MAXL];            // rank capacity
+    int ktoff[MAXL + 1];    // prefix of ceil(R/BK) (update kernel K tiles)
+    const double* P[MAXL];  // projection operand (V_l, or U_l when transposed)
+    const double* Q[MAXL];  // update operand (U_l, or V_l when transposed)
+    double* T[MAXL];        // per-level projections: nseg_l x R_l x s (ld R_l)
+    double* ws[MAXL];       // split-K partial workspace (null when one chunk per segment)
+    int item_off[MAXL + 1]; // first projection work item of each level
+};
+
+struct MlItem {  // projection work item
+    int level, seg, row0, rows, chunk;  // chunk = index within the level's partial workspace
+};
+
+struct ProjArgs {
+    MlLevels L;
+    const MlItem* items;
+    const double* X;
+    i64 ldx, n;
+    int s, tiles_n;
+};
+
+__device__ __forceinline__ int cdiv_i(int a, int b) { return (a + b - 1) / b; }
+
+__global__ void __launch_bounds__(THREADS) k_ml_proj(ProjArgs g) {
+    extern __shared__ double smem[];
+    const MlItem it = g.items[blockIdx.x];
+    const int l = it.level, R = g.L.R[l];
+    const int m0 = (blockIdx.y / g.tiles_n) * BM, n0 = (blockIdx.y % g.tiles_n) * BN;
+    if (m0 >= R) return;
+    tile::LoadKC la{g.L.P[l] + it.row0 + i64(m0) * g.n, g.n, it.rows, R - m0};
+    tile::LoadKC lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
+    Acc acc;
+    acc.zero();
+    tile::run(la, lb, cdiv_i(it.rows, BK), smem, acc);
+    const i64 blk = i64(R) * g.s;
+    double* o = g.L.ws[l] ? g.L.ws[l] + i64(it.chunk) * blk : g.L.T[l] + i64(it.seg) * blk;
+    tile::for_each(acc, [&](int mi, int ni, double v) {
+        const int m = m0 + mi, c = n0 + ni;
+        if (m < R && c < g.s) o[m + i64(c) * R] = v;
+    });
+}
+
+struct ReduceArgs {
+    MlLevels L;
+    const int* seg_level;  // per reduce segment: level
+    const int* seg_index;  // segment index within the level
+    const int* first;      // partial range [first, first+count) in that level's ws
+    const int* count;
+    int s;
+};
+
+__global__ void k_ml_reduce(ReduceArgs g) {
+    const int r = blockIdx.y;
+    const int l = g.seg_level[r], R = g.L.R[l];
+    const i64 blk = i64(R) * g.s;
+    const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= blk) return;
+    const double* w = g.L.ws[l];
+    double sum = 0.0;
+    for (int c = g.first[r]; c < g.first[r] + g.count[r]; ++c) sum += w[i64(c) * blk + e];
+    g.L.T[l][i64(g.seg_index[r]) * blk + e] = sum;
+}
+
+struct UpdArgs {
+    MlLevels L;
+    const WorkItem* items;  // row tiles of the finest partition (depth tau)
+    int tau;
+    i64 n;
+    double* Y;
+    i64 ldy;
+    int s;
+    double alpha, beta;
+};
+
+/// A operand: rows of the update panels, K = concatenated level columns.
+struct LoadUpdA {
+    static constexpr bool KC = false;
+    const MlLevels* L;
+    int row0, rows;
+    i64 n;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        int l = 0;
+        while (kt >= L->ktoff[l + 1]) ++l;
+        const int kb = (kt - L->ktoff[l]) * BK, R = L->R[l];
+        const double* base = L->Q[l] + row0;
+        const int m = threadIdx.x & 63;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = (threadIdx.x >> 6) + 2 * q, kk = kb + k;
+            const bool v = m < rows && kk < R;
+            tile::cp_async8(S + k * tile::LD_MC + m, v ? base + m + kk * n : base, v);
+        }
+    }
+};
+
+/// B operand: T_l of the sibling segment at each level (k-contiguous, ld R_l).
+struct LoadUpdB {
+    static constexpr bool KC = true;
+    const MlLevels* L;
+    int leaf, tau, s, n0;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        int l = 0;
+        while (kt >= L->ktoff[l + 1]) ++l;
+        const int kb = (kt - L->ktoff[l]) * BK, R = L->R[l];
+        const int seg = (leaf >> (tau - L->depth[l])) ^ 1;
+        const double* base = L->T[l] + i64(seg) * R * s + i64(n0) * R;
+        const int k = threadIdx.x & 15, kk = kb + k;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int c = (threadIdx.x >> 4) + 8 * q;
+            const bool v = kk < R && n0 + c < s;
+            tile::cp_async8(S + c * tile::LD_KC + k, v ? base + kk + i64(c) * R : base, v);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
+    extern __shared__ double smem[];
+    __shared__ MlLevels L;
+    for (int i = threadIdx.x; i < int(sizeof(MlLevels) / sizeof(int)); i += blockDim.x)
+        reinterpret_cast<int*>(&L)[i] = reinterpret_cast<const int*>(&g.L)[i];
+    __syncthreads();
+    const WorkItem it = g.items[blockIdx.x];
+    const int n0 = blockIdx.y * BN;
+    LoadUpdA la{&L, it.row0, it.rows, g.n};
+    LoadUpdB lb{&L, it.seg, g.tau, g.s, n0};
+    Acc acc;
+    acc.zero();
+    tile::run<2>(la, lb, L.ktoff[L.nl], smem, acc);
+    tile::for_each(acc, [&](int m, int ni, double v) {
+        const int c = n0 + ni;
+        if (c >= g.s || m >= it.rows) return;
+        double* p = g.Y + i64(it.row0 + m) + i64(c) * g.ldy;
+        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+    });
+}
+
+/// Projection work items of levels [lmin, lmax] (chunk-major), cached per tree.
+struct ItemPlan {
+    DBuf<MlItem> items;
+    int count = 0;
+    std::vector<int> item_off;           // per level (relative to lmin)
+    std::vector<int> nchunks;            // per level: partial count (0 => direct)
+    DBuf<int> rl, ri, rf, rc;            // reduce segments
+    int nred = 0;
+};
+
+const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
+    static std::mutex mu;
+    static std::map<std::tuple<const DTree*, int, int>, std::unique_ptr<ItemPlan>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(&t, lmin, lmax);
+    auto itc = cache.find(key);
+    if (itc != cache.end()) return *itc->second;
+    auto p = std::make_unique<ItemPlan>();
+    const int nl = lmax - lmin + 1;
+    // Per level: chunks of at most ML_CHUNK rows that never cross a segment.
+    std::vector<std::vector<MlItem>> per(static_cast<size_t>(nl));
+    std::vector<int> rl, ri, rf, rc;
+    p->nchunks.assign(static_cast<size_t>(nl), 0);
+    for (int i = 0; i < nl; ++i) {
+        const Partition& pt = t.part(lmin + i);
+        const auto& hb = pt.hbounds();
+        bool multi = false;
+        for (int sgi = 0; sgi < pt.nseg(); ++sgi)
+            if (hb[static_cast<size_t>(sgi + 1)] - hb[static_cast<size_t>(sgi)] > ML_CHUNK) multi = true;
+        int chunk = 0;
+        for (int sgi = 0; sgi < pt.nseg(); ++sgi) {
+            const int lo = hb[static_cast<size_t>(sgi)], hi = hb[static_cast<size_t>(sgi + 1)];
+            const int first = chunk;
+            for (int r = lo; r < hi || r == lo; r += ML_CHUNK) {
+                per[static_cast<size_t>(i)].push_back(MlItem{i, sgi, r, std::min(ML_CHUNK, hi - r), chunk++});
+                if (hi == lo) break;
+            }
+            if (multi) {
+                rl.push_back(i);
+                ri.push_back(sgi);
+                rf.push_back(first);
+                rc.push_back(chunk - first);
+            }
+        }
+        p->nchunks[static_cast<size_t>(i)] = multi ? chunk : 0;
+    }
+    // Chunk-major interleave: items touching the same rows run back to back.
+    std::vector<MlItem> all;
+    std::vector<size_t> pos(static_cast<size_t>(nl), 0);
+    p->item_off.assign(static_cast<size_t>(nl + 1), 0);
+    bool left = true;
+    while (left) {
+        left = false;
+        // advance every level up to the same row position
+        int row = 1 << 30;
+        for (int i = 0; i < nl; ++i)
+            if (pos[static_cast<size_t>(i)] < per[static_cast<size_t>(i)].size())
+                row = std::min(row, per[static_cast<size_t>(i)][pos[static_cast<size_t>(i)]].row0);
+        for (int i = 0; i < nl; ++i) {
+            auto& v = per[static_cast<size_t>(i)];
+            while (pos[static_cast<size_t>(i)] < v.size() && v[pos[static_cast<size_t>(i)]].row0 <= row) {
+                all.push_back(v[pos[static_cast<size_t>(i)]++]);
+            }
+            if (pos[static_cast<size_t>(i)] < v.size()) left = true;
+        }
+    }
+    p->count = int(all.size());
+    p->items.upload(all);
+    p->nred = int(rl.size());
+    if (p->nred) {
+        p->rl.upload(rl);
+        p->ri.upload(ri);
+        p->rf.upload(rf);
+        p->rc.upload(rc);
+    }
+    auto& ref = *p;
+    cache[key] = std::move(p);
+    return ref;
+}
+
+void ml_attrs() {
+    static bool done = false;
+    if (done) return;
+    HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_ml_proj), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tile::SMEM_BYTES));
+    HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_ml_update),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tile::smem_bytes(2)));
+    done = true;
+}
+
+}  // namespace
+
+void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
+                 bool with_leaves, bool transpose, double beta, double alpha) {
+    if (s <= 0) return;
+    const i64 n = h.n();
+    const DTree& t = *h.tree;
+    if (with_leaves && !h.leaves_zero) {
+        leaf_mm(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), transpose, X, ldx, Y, ldy, s, alpha, beta);
+        beta = 1.0;
+    }
+    lmin = std::max(lmin, 1);
+    lmax = std::min(lmax, h.tau());
+    // levels with nonzero rank
+    std::vector<int> lv;
+    for (int l = lmin; l <= lmax; ++l)
+        if (h.Rl(l) > 0) lv.push_back(l);
+    if (lv.empty()) {
+        if (beta != 1.0) panel_axpby(n, s, 0.0, nullptr, 0, beta, Y, ldy);
+        return;
+    }
+    if (int(lv.size()) > MAXL) throw std::length_error("hodlr_apply: too many levels");
+    ml_attrs();
+    auto& c = current();
+    const ItemPlan& ip = item_plan(t, lmin, lmax);
+    MlLevels L{};
+    L.nl = lmax - lmin + 1;
+    std::vector<DVec> Tbuf(static_cast<size_t>(L.nl)), Wbuf(static_cast<size_t>(L.nl));
+    double flops = 0, bytes = 8.0 * double(n) * (s + 2.0 * s);
+    L.ktoff[0] = 0;
+    for (int i = 0; i < L.nl; ++i) {
+        const int l = lmin + i, R = h.Rl(l);
+        const Partition& pt = t.part(l);
+        L.depth[i] = l;
+        L.R[i] = R;
+        L.ktoff[i + 1] = L.ktoff[i] + (R + BK - 1) / BK;
+        L.P[i] = transpose ? h.Ul(l) : h.Vl(l);
+        L.Q[i] = transpose ? h.Vl(l) : h.Ul(l);
+        if (R > 0) {
+            Tbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(pt.nseg()) * R * s);
+            if (ip.nchunks[static_cast<size_t>(i)])
+                Wbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(ip.nchunks[static_cast<size_t>(i)]) * R * s);
+        }
+        L.T[i] = Tbuf[static_cast<size_t>(i)].get();
+        L.ws[i] = Wbuf[static_cast<size_t>(i)].get();
+        flops += 4.0 * double(n) * R * s;
+        bytes += 16.0 * double(n) * R;
+    }
+    ProfScope prof(PROF_SEG_TN, flops, bytes);
+    int max_tiles_m = 1;
+    for (int i = 0; i < L.nl; ++i) max_tiles_m = std::max(max_tiles_m, (L.R[i] + BM - 1) / BM);
+    const int tiles_n = (s + BN - 1) / BN;
+    ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n};
+    k_ml_proj<<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, tile::SMEM_BYTES, c.stream>>>(pa);
+    HG_LAUNCH();
+    ++c.launches;
+    if (ip.nred) {
+        int maxblk = 0;
+        for (int i = 0; i < L.nl; ++i) maxblk = std::max(maxblk, L.R[i] * s);
+        ReduceArgs ra{L, ip.rl.get(), ip.ri.get(), ip.rf.get(), ip.rc.get(), s};
+        k_ml_reduce<<<dim3(unsigned(cdiv(maxblk, 256)), unsigned(ip.nred)), 256, 0, c.stream>>>(ra);
+        HG_LAUNCH();
+        ++c.launches;
+    }
+    const TileList& tl = t.leaves().tiles(BM);
+    UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta};
+    k_ml_update<<<dim3(unsigned(tl.count), unsigned(tiles_n)), THREADS, tile::smem_bytes(2), c.stream>>>(ua);
+    HG_LAUNCH();
+    ++c.launches;
+}
+
+}  // namespace hg
