@@ -432,6 +432,100 @@ void compress_level(DHodlr& D, int l, double rtol) {
     }
 }
 
+__global__ void k_transpose_blocks(int w, const double* A, double* B) {
+    const int j = blockIdx.x;
+    const double* a = A + i64(j) * w * w;
+    double* b = B + i64(j) * w * w;
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+        const int r = e % w, c = e / w;
+        b[c + r * w] = a[e];
+    }
+}
+
+/// Structured recompression of a derivative level built by the sketch
+/// (sketch.cpp:297-311 then :331-341). Its left factor is
+/// [dqc | Q | q2] = [Q | q2] [[Omega, I, 0], [0, 0, I]] with [Q | q2]
+/// orthonormal (dqc = Q Omega, q2 projected off Q twice), so the block is
+/// [Q | q2] Z^T with Z = [t Omega^T + dt | dt2] = [dt - t Omega | dt2]
+/// (Omega skew). Only Z needs a QR (c' x (k + w2) instead of two c x
+/// (2k + w2) QRs); the core R_Z^T is truncated by a rank-revealing pivoted QR
+/// at rtol (SVD truncation in hodlr_matrix.cpp:56-60).
+void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double rtol) {
+    const int W = D.Rl(l);
+    if (W == 0) return;
+    const int w = W - k;
+    const DTree& t = *D.tree;
+    const i64 n = t.n();
+    const Partition& pc = t.part(l);
+    const int nodes = 1 << (l - 1);
+    const auto& hb = pc.hbounds();
+    auto& ctx = current();
+    double* P = D.Ul(l);
+    DVec Z(static_cast<size_t>(n) * w);
+    panel_axpby(n, k, 1.0, P + i64(k) * n, n, 0.0, Z.get(), n);
+    seg_nn(pc, P, n, k, Om, i64(k) * k, k, TMap::parent(0, 0), Z.get(), n, k, -1.0, 1.0);
+    if (w > k) panel_axpby(n, w - k, 1.0, P + i64(2 * k) * n, n, 0.0, Z.get() + i64(k) * n, n);
+    std::vector<BatchedQR::Block> blocks;
+    for (int j = 0; j < nodes; ++j)
+        blocks.push_back({Z.get() + hb[static_cast<size_t>(2 * j + 1)], n,
+                          hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)]});
+    BatchedQR qz(blocks, w, false);
+    DVec M(static_cast<size_t>(nodes) * w * w);
+    k_transpose_blocks<<<nodes, 256, 0, ctx.stream>>>(w, qz.R(), M.get());
+    HG_LAUNCH();
+    count_launch();
+    std::vector<BatchedQR::Block> mb;
+    for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * w * w, w, w});
+    BatchedQR mq(mb, w, true);
+    std::vector<int> wmin(static_cast<size_t>(nodes));
+    for (int j = 0; j < nodes; ++j) {
+        const int cl = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
+        const int cr = hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)];
+        wmin[static_cast<size_t>(j)] = std::min({cl, cr, w});
+    }
+    DBuf<int> dwmin, dr(static_cast<size_t>(nodes));
+    dwmin.upload(wmin);
+    k_trunc_rank<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, w, mq.R(), dwmin.get(), rtol, dr.get());
+    HG_LAUNCH();
+    count_launch();
+    std::vector<int> r = dl_int(dr);
+    int rmax = 0;
+    for (int x : r) rmax = std::max(rmax, x);
+    auto Pn = rmax ? make_dvec(static_cast<size_t>(n) * static_cast<size_t>(rmax), true) : nullptr;
+    if (rmax) {
+        // Tin[2j] = Q_M[:, :r_j]; Tin[2j+1] = P_M R_M[:r_j, :]^T (w x rmax each)
+        DVec Tin(static_cast<size_t>(2 * nodes) * w * rmax);
+        std::vector<double*> qo;
+        std::vector<i64> ql;
+        for (int j = 0; j < nodes; ++j) {
+            qo.push_back(Tin.get() + i64(2 * j) * w * rmax);
+            ql.push_back(w);
+        }
+        mq.form_q(rmax, nullptr, 0, 0, qo, ql);
+        k_tins<<<nodes, 256, 0, ctx.stream>>>(w, rmax, dr.get(), mq.R(), mq.perm(), Tin.get());
+        HG_LAUNCH();
+        count_launch();
+        // left' = [Q | q2] Q_M[:, :r] on left-child rows (odd rows are overwritten next)
+        seg_nn(pc, P + i64(k) * n, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n, rmax,
+               1.0, 0.0);
+        // right' = Q_Z P_M R_M[:r, :]^T on right-child rows
+        std::vector<double*> out;
+        std::vector<i64> ld;
+        for (int j = 0; j < nodes; ++j) {
+            out.push_back(Pn->get() + hb[static_cast<size_t>(2 * j + 1)]);
+            ld.push_back(n);
+        }
+        qz.form_q(rmax, Tin.get() + i64(w) * rmax, i64(2) * w * rmax, w, out, ld);
+    }
+    D.R[static_cast<size_t>(l - 1)] = rmax;
+    D.U[static_cast<size_t>(l - 1)] = Pn;
+    D.V[static_cast<size_t>(l - 1)] = Pn;
+    for (int j = 0; j < nodes; ++j) {
+        D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+        D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+    }
+}
+
 constexpr int COMPLETE_BATCH_ROWS = 8192;
 
 /// sketch.cpp:60-74 for every node of a level whose numeric rank is below k.
@@ -610,6 +704,8 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
     out.p = p;
     out.h = DHodlr::zero(tree);
     for (int q = 0; q < p; ++q) out.deriv.push_back(DHodlr::zero(tree));
+    // Omega (in-span rotation of diff_qr) per param and level, for the recompression.
+    std::vector<std::vector<DVecP>> omegas(static_cast<size_t>(p), std::vector<DVecP>(static_cast<size_t>(tau)));
     auto& ctx = current();
 
     for (int l = 1; l <= tau; ++l) {
@@ -723,7 +819,10 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         // Differentiated passes (sketch.cpp:236-295) and the commit (:297-311).
         std::vector<std::vector<int>> rws(static_cast<size_t>(p));
         for (int q = 0; q < p; ++q) {
-            DVec G(static_cast<size_t>(2 * nodes) * k * k), Om(static_cast<size_t>(nodes) * k * k), ds(static_cast<size_t>(n) * k);
+            DVec G(static_cast<size_t>(2 * nodes) * k * k), ds(static_cast<size_t>(n) * k);
+            DVecP OmP = make_dvec(static_cast<size_t>(nodes) * k * k, false);
+            omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)] = OmP;
+            DVec& Om = *OmP;
             DBuf<int> rw(static_cast<size_t>(nodes)), ill(static_cast<size_t>(nodes));
             const double* dYq = dY.get() + i64(q) * k * n;
             seg_tn(pc, S.get(), n, k, dYq, n, k, G.get(), i64(k) * k, k);
@@ -799,7 +898,9 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
     }
     // Recompress every derivative off-diagonal block (sketch.cpp:331-341).
     for (int q = 0; q < p; ++q)
-        for (int l = 1; l <= tau; ++l) compress_level(out.deriv[static_cast<size_t>(q)], l, 1e-13);
+        for (int l = 1; l <= tau; ++l)
+            compress_level_structured(out.deriv[static_cast<size_t>(q)], l, k,
+                                      omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(), 1e-13);
     return out;
 }
 
