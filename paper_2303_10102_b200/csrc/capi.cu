@@ -149,6 +149,7 @@ hg_status hg_ctx_create(int device, void* stream, hg_ctx_t* out) {
             HG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
             c->c.own_stream = true;
         }
+        dev_stream_adopt(c->c.stream);
         HG_CUDA(cudaDeviceGetAttribute(&c->c.num_sms, cudaDevAttrMultiProcessorCount, device));
         // Keep freed blocks in the stream-ordered pool (no trimming between calls).
         cudaMemPool_t pool;
@@ -167,7 +168,11 @@ hg_status hg_ctx_create(int device, void* stream, hg_ctx_t* out) {
 hg_status hg_ctx_destroy(hg_ctx_t ctx) {
     return guard(ctx, [&] {
         HG_CUDA(cudaStreamSynchronize(ctx->c.stream));
-        if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+        if (ctx->c.own_stream) {
+            dev_stream_retire(ctx->c.stream);
+            cudaStreamSynchronize(ctx->c.stream);
+            cudaStreamDestroy(ctx->c.stream);
+        }
         set_current(nullptr);
         delete ctx;
     });

@@ -461,9 +461,37 @@ void cap_solve(const DFactor& f, int i, const double* Q, bool top_odd, bool tran
     count_launch();
 }
 
-}  // namespace
+/// Node panels (nodes*m rows, ld L = nodes*m) of the capacitance operators,
+/// with Pi the half swap so that node j's right-hand side is the contiguous
+/// block [Q_{2j}; Q_{2j+1}]:
+///   Right solve  (cap^{-1} [Q_{2j+1}; Q_{2j}]):  SR = cap^{-1} Pi, AR = Pi cap
+///   Left solve   (cap^{-T} [Q_{2j}; Q_{2j+1}]):  SL = cap^{-T},    AL = cap^T
+/// from E_j = cap_j^{-T} (m x m, ld m) and the blocks P of cap (k_cap_lu).
+__global__ void k_cap_panels(const double* E, const double* P, int R, i64 L, double* SR, double* AR, double* SL,
+                             double* AL) {
+    const int j = blockIdx.x, m = 2 * R;
+    const double* Ej = E + i64(j) * m * m;
+    const double* Pl = P + i64(2 * j) * R * R;
+    const double* Pr = P + i64(2 * j + 1) * R * R;
+    auto cap = [&](int r, int c) -> double {
+        if ((r < R) == (c < R)) return r == c ? 1.0 : 0.0;
+        return r < R ? Pr[r + (c - R) * R] : Pl[(r - R) + c * R];
+    };
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int r = e % m, c = e / m;
+        const int swc = c < R ? c + R : c - R, swr = r < R ? r + R : r - R;
+        const i64 o = i64(j) * m + r + i64(c) * L;
+        SL[o] = Ej[r + i64(c) * m];
+        SR[o] = Ej[swc + i64(r) * m];
+        AR[o] = cap(swr, c);
+        AL[o] = cap(c, r);
+    }
+}
 
-void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) {
+/// Y <- Abar^{-1} Y by blocked substitution with the leaf factors. (An
+/// explicit-inverse GEMM path was tried and dropped: with refinement it is
+/// slower, without it the leaves' conditioning costs parity.)
+void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
     if (w <= 0) return;
     const Partition& lv = f.tree->leaves();
     const int m = lv.max_seg();
@@ -478,28 +506,37 @@ void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) {
     count_launch();
 }
 
+}  // namespace
+
+void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) { leaf_solve_subst(f, Y, ldy, w); }
+
 void level_inverse(const DFactor& f, int i, bool transposed, double* Y, i64 ldy, int w) {
     const int R = f.Rl(i);
     if (R == 0 || w <= 0) return;
     const Partition& p = f.tree->part(i);
     const i64 n = f.n();
-    DVec Q(static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(w));
-    DVec T(static_cast<size_t>(p.nseg() / 2) * static_cast<size_t>(2 * R) * static_cast<size_t>(w));
-    if (!transposed) {
-        seg_tn(p, f.Fl(i), n, R, Y, ldy, w, Q.get(), i64(R) * w, R);
-        cap_solve(f, i, Q.get(), true, false, T.get(), w);
-        seg_nn(p, f.Wl(i), n, R, T.get(), i64(2 * R) * w, 2 * R, TMap::parent(0, R), Y, ldy, w, -1.0, 1.0);
-    } else {
-        seg_tn(p, f.Wl(i), n, R, Y, ldy, w, Q.get(), i64(R) * w, R);
-        cap_solve(f, i, Q.get(), false, true, T.get(), w);
-        seg_nn(p, f.Fl(i), n, R, T.get(), i64(2 * R) * w, 2 * R, TMap::parent(R, 0), Y, ldy, w, -1.0, 1.0);
-    }
-}
-
-void cap_inverse_transpose(const DFactor& f, int i, double* E) {
-    const int R = f.Rl(i);
-    if (R == 0) return;
-    cap_solve(f, i, nullptr, false, true, E, 2 * R);
+    const int m = 2 * R, nodes = p.nseg() / 2;
+    const i64 L = i64(p.nseg()) * R;
+    // Q panel: rows s*R.. hold the projection of child s, so node j's
+    // [Q_{2j}; Q_{2j+1}] is one contiguous 2R-row block.
+    DVec Q(static_cast<size_t>(L) * static_cast<size_t>(w));
+    DVec T(static_cast<size_t>(L) * static_cast<size_t>(w));
+    const Partition& up = uniform_partition(nodes, m);
+    const size_t li = static_cast<size_t>(i - 1);
+    const double* S = transposed ? f.capinvT[li]->get() : f.capinv[li]->get();
+    const double* A = transposed ? f.capT[li]->get() : f.capR[li]->get();
+    seg_tn(p, transposed ? f.Wl(i) : f.Fl(i), n, R, Y, ldy, w, Q.get(), R, int(L));
+    // Capacitance solve as three batched GEMMs: T = S Q, then one step of
+    // refinement Q <- Q - A T, T += S Q. Without the refinement the explicit
+    // inverse loses ~2 digits on the C1 parity case (cond(cap) ~ 1e7); with
+    // it the result matches the LU substitution of the reference.
+    seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w);
+    seg_nn(up, A, L, m, T.get(), m, int(L), TMap::same(), Q.get(), L, w, -1.0, 1.0);
+    seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w, 1.0, 1.0);
+    if (!transposed)
+        seg_nn(p, f.Wl(i), n, R, T.get(), m, int(L), TMap::parent(0, R), Y, ldy, w, -1.0, 1.0);
+    else
+        seg_nn(p, f.Fl(i), n, R, T.get(), m, int(L), TMap::parent(R, 0), Y, ldy, w, -1.0, 1.0);
 }
 
 DFactor factorize(const DHodlr& h, int orient) {
@@ -560,6 +597,10 @@ DFactor factorize(const DHodlr& h, int orient) {
     f.cap_piv.assign(static_cast<size_t>(tau), nullptr);
     f.cap_ld.assign(static_cast<size_t>(tau), nullptr);
     f.cap_sign.assign(static_cast<size_t>(tau), nullptr);
+    f.capinv.assign(static_cast<size_t>(tau), nullptr);
+    f.capinvT.assign(static_cast<size_t>(tau), nullptr);
+    f.capR.assign(static_cast<size_t>(tau), nullptr);
+    f.capT.assign(static_cast<size_t>(tau), nullptr);
     for (int i = tau; i >= 1; --i) {
         const int R = f.Rl(i), m = 2 * R, nodes = 1 << (i - 1);
         if (R == 0) continue;
@@ -578,6 +619,21 @@ DFactor factorize(const DHodlr& h, int orient) {
         k_cap_lu<<<unsigned(nodes), FNT, use ? smem : 0, current().stream>>>(g);
         HG_LAUNCH();
         count_launch();
+        {  // explicit cap^{-T} by substitution on identity columns, then both panels
+            DVec E(static_cast<size_t>(nodes) * static_cast<size_t>(m) * static_cast<size_t>(m));
+            cap_solve(f, i, nullptr, false, true, E.get(), m);
+            const size_t ps = static_cast<size_t>(nodes) * static_cast<size_t>(m) * static_cast<size_t>(m);
+            const size_t li = static_cast<size_t>(i - 1);
+            f.capinvT[li] = make_dvec(ps, false);
+            f.capinv[li] = make_dvec(ps, false);
+            f.capR[li] = make_dvec(ps, false);
+            f.capT[li] = make_dvec(ps, false);
+            k_cap_panels<<<unsigned(nodes), 256, 0, current().stream>>>(E.get(), P.get(), R, i64(nodes) * m,
+                                                                       f.capinv[li]->get(), f.capR[li]->get(),
+                                                                       f.capinvT[li]->get(), f.capT[li]->get());
+            HG_LAUNCH();
+            count_launch();
+        }
         if (i > 1 && f.off[static_cast<size_t>(i - 1)] > 0) level_inverse(f, i, false, f.Wbar->get(), n, f.off[static_cast<size_t>(i - 1)]);
     }
     return f;

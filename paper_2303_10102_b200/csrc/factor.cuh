@@ -30,6 +30,12 @@ struct DFactor {
     std::vector<std::shared_ptr<DBuf<int>>> cap_piv;  // [i-1] nodes x 2R swaps
     std::vector<DVecP> cap_ld;             // [i-1] nodes
     std::vector<std::shared_ptr<DBuf<int>>> cap_sign;
+    // Explicit capacitance inverses computed once by substitution, so every
+    // later capacitance solve is batched tensor-core GEMMs: x0 = S b followed
+    // by one step of refinement x = x0 + S (b - A x0) with the operator A.
+    // [i-1] node panels (nodes*2R) x 2R, ld nodes*2R, Pi = half swap:
+    std::vector<DVecP> capinv, capR;       // Right: cap^{-1} Pi and Pi cap
+    std::vector<DVecP> capinvT, capT;      // Left : cap^{-T} and cap^T
 
     i64 n() const { return tree->n(); }
     int tau() const { return tree->tau(); }
@@ -57,9 +63,6 @@ void factor_solve(const DFactor& f, double* Y, i64 ldy, int w);
 /// HodlrFactorization::logdet (factorization.cpp:214-224); throws
 /// NotPositiveDefinite like the reference.
 double factor_logdet(const DFactor& f);
-
-/// Per node of level i: E_j = cap_j^{-T} (2R x 2R), stacked.
-void cap_inverse_transpose(const DFactor& f, int i, double* E);
 
 /// leaf-kind flags (1 = LLT) to host.
 std::vector<int> leaf_kinds(const DFactor& f);

@@ -80,9 +80,8 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         DVec Q(static_cast<size_t>(n) * static_cast<size_t>(C2));
         if (inverse) {
             // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
-            DVec E(static_cast<size_t>(1 << (i - 1)) * static_cast<size_t>(C2) * static_cast<size_t>(C2));
-            cap_inverse_transpose(f, i, E.get());
-            seg_nn(p, f.Fl(i), n, R, E.get(), i64(C2) * C2, C2, TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
+            seg_nn(p, f.Fl(i), n, R, f.capinvT[static_cast<size_t>(i - 1)]->get(), C2, p.nseg() * R,
+                   TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
             // q = u = [wbar 0; 0 xbar]
             panel_parity_scale(p, n, R, f.Wl(i), n, 1.0, 0.0, Q.get(), n, 0.0);
             panel_parity_scale(p, n, R, f.Wl(i), n, 0.0, 1.0, Q.get() + i64(R) * n, n, 0.0);

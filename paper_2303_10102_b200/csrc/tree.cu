@@ -93,6 +93,25 @@ Partition::Partition(const ClusterTree& t, int d) : depth_(d) {
     db_.upload(hb_);
 }
 
+Partition::Partition(int nseg, int len) : depth_(-1), nseg_(nseg), max_seg_(len) {
+    hb_.resize(static_cast<size_t>(nseg + 1));
+    for (int s = 0; s <= nseg; ++s) hb_[static_cast<size_t>(s)] = s * len;
+    db_.upload(hb_);
+}
+
+const Partition& uniform_partition(int nseg, int len) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, std::unique_ptr<Partition>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(current().device, nseg, len);
+    auto it = cache.find(key);
+    if (it != cache.end()) return *it->second;
+    auto p = std::make_unique<Partition>(nseg, len);
+    auto& ref = *p;
+    cache[key] = std::move(p);
+    return ref;
+}
+
 const TileList& Partition::tiles(int rows) const {
     auto it = cache_.find(rows);
     if (it != cache_.end()) return *it->second;

@@ -59,6 +59,8 @@ struct TileList {
 class Partition {
 public:
     Partition(const ClusterTree& t, int d);
+    /// nseg equal segments of `len` rows (batched per-node small matrices).
+    Partition(int nseg, int len);
     int depth() const { return depth_; }
     int nseg() const { return nseg_; }
     const std::vector<int>& hbounds() const { return hb_; }
@@ -88,5 +90,8 @@ using DTreeP = std::shared_ptr<const DTree>;
 
 /// Cached per (n, tau) on the current device.
 DTreeP get_tree(i64 n, int tau);
+
+/// Cached uniform partition (nseg segments of len rows).
+const Partition& uniform_partition(int nseg, int len);
 
 }  // namespace hg
