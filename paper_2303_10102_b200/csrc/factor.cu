@@ -498,6 +498,7 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
     const size_t smem = (static_cast<size_t>(m) * (SOLVE_COLS + 1) + 16 * static_cast<size_t>(m + 1)) * sizeof(double);
     const double rows = double(f.n());
     ProfScope prof(PROF_LEAF_SOLVE, 2.0 * rows * m * w, 8.0 * (rows * m + 2.0 * rows * w));
+    if (prof_enabled()) prof.key(prof_tag("leafsolve w=%d", w));
     set_smem(reinterpret_cast<const void*>(k_leaf_solve), smem);
     LeafSolveArgs g{lv.dbounds(), f.bmax(), f.leaf_fac->get(), f.leaf_kind->get(), f.leaf_piv->get(), Y, ldy, w};
     dim3 grid(unsigned(lv.nseg()), unsigned(cdiv(w, SOLVE_COLS)));

@@ -215,6 +215,19 @@ struct PairDot {
     }
 };
 
+struct XorDot {
+    int ra, rc, xr, ld;
+    i64 gs;
+    const double *G, *H;
+    __device__ double operator()(i64 e) const {
+        const i64 per = i64(ra) * rc;
+        const int s = int(e / per);
+        const int rem = int(e % per), a = rem % ra, c = rem / ra;
+        const i64 o = a + i64(c) * ld;
+        return G[i64(s) * gs + o] * H[i64(s ^ xr) * gs + o];
+    }
+};
+
 struct LeafTrace {
     const int* bounds;
     int bmax, ldl;
@@ -288,6 +301,7 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     auto& c = current();
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
+    if (prof_enabled()) prof.key(prof_tag("tn nseg=%d ca=%d cb=%d", p.nseg(), ca, cb));
     const TileList& tl = p.tiles(SEG_CHUNK);
     const int tiles_m = cdiv(ca, BM), tiles_n = cdiv(cb, BN);
     smem_attrs();
@@ -324,6 +338,7 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     }
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
+    if (prof_enabled()) prof.key(prof_tag("nn nseg=%d k=%d w=%d", p.nseg(), k, w));
     const TileList& tl = p.tiles(BM);
     smem_attrs();
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
@@ -341,6 +356,7 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     smem_attrs();
     const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
     ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + rows * w * (beta != 0.0 ? 3.0 : 2.0)));
+    if (prof_enabled()) prof.key(prof_tag("leafmm w=%d tr=%d", w, int(trans)));
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
     dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, BN)));
     if (trans)
@@ -379,6 +395,11 @@ void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb
 void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,
                   int ldh, double* out, bool accumulate) {
     reduce(PairDot{ra, rb, xr, ldg, ldh, gs, hs, G, H}, i64(nseg) * ra * rb, out, accumulate);
+}
+
+void seg_xor_dot(int nseg, int xr, const double* G, const double* H, i64 gs, int ld, int ra, int rc, double* out,
+                 bool accumulate) {
+    reduce(XorDot{ra, rc, xr, ld, gs, G, H}, i64(nseg) * ra * rc, out, accumulate);
 }
 
 void leaf_trace(const Partition& leaves, const double* L, i64 lstride, int ldl, double* out, bool accumulate) {

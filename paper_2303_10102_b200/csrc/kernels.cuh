@@ -55,6 +55,11 @@ void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb
 void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,
                   int ldh, double* out, bool accumulate);
 
+/// out[0] (+)= sum_s sum_{a<ra,c<rc} G_s(a,c) H_{s^xr}(a,c), both ra x rc
+/// (ld ld, stride gs).
+void seg_xor_dot(int nseg, int xr, const double* G, const double* H, i64 gs, int ld, int ra, int rc, double* out,
+                 bool accumulate);
+
 /// out[0] (+)= sum_b trace(L_b) (leaves, ld ldl, stride lstride).
 void leaf_trace(const Partition& leaves, const double* L, i64 lstride, int ldl, double* out, bool accumulate);
 /// out[0] (+)= sum_b sum(A_b^T .* B_b).

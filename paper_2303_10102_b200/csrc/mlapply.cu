@@ -306,6 +306,11 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         bytes += 16.0 * double(n) * R;
     }
     ProfScope prof(PROF_SEG_TN, flops, bytes);
+    if (prof_enabled()) {
+        int rmax = 0;
+        for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
+        prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
+    }
     int max_tiles_m = 1;
     for (int i = 0; i < L.nl; ++i) max_tiles_m = std::max(max_tiles_m, (L.R[i] + BM - 1) / BM);
     const int tiles_n = (s + BN - 1) / BN;

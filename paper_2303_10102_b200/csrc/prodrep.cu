@@ -119,33 +119,64 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
     const int tau = pb.tau();
     const i64 n = pb.n();
     const DTree& t = *pb.base.tree;
+    const bool same = &pb == &pd;  // tr((A^-1 dA)^2): mirrored terms computed once
     hodlr_trace_product(pb.base, pd.base, out, accumulate);
-    // Cross terms sum(v .* (base_sub u)) (product_rep.cpp:212-224).
-    auto cross = [&](const DHodlr& h, const DProductRep& corr) {
-        for (int i = 1; i <= tau; ++i) {
-            const int Ci = corr.C[static_cast<size_t>(i - 1)];
-            if (!Ci) continue;
-            DVec Y(static_cast<size_t>(n) * static_cast<size_t>(Ci));
-            hodlr_apply(h, corr.Cul(i), n, Ci, Y.get(), n, i, tau, true, false, 0.0);
-            dot_panels(n, Ci, corr.Cvl(i), n, Y.get(), n, out, true);
+    // Cross terms sum_i tr(Cv_i^T h_{>=i} Cu_i) (product_rep.cpp:212-224),
+    // regrouped by the level of h: the leaves act on every correction, level
+    // l on corrections i <= l, i.e. on the column prefix W_l of Cu / Cv, so
+    //   sum = tr(Cv^T Leaves Cu) + sum_l sum_s <U_l[s]^T Cv_{<=l}[s], V_l[s^1]^T Cu_{<=l}[s^1]>
+    // (two projections per level and a sibling dot; no n x C products).
+    auto cross = [&](const DHodlr& h, const DProductRep& corr, double alpha) {
+        if (!corr.sumC) return;
+        if (!h.leaves_zero) {
+            constexpr int CH = 256;
+            DVec Y(static_cast<size_t>(n) * static_cast<size_t>(std::min(corr.sumC, CH)));
+            for (int c0 = 0; c0 < corr.sumC; c0 += CH) {
+                const int cw = std::min(CH, corr.sumC - c0);
+                leaf_mm(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), false, corr.Cu->get() + i64(c0) * n, n,
+                        Y.get(), n, cw, alpha, 0.0);
+                dot_panels(n, cw, corr.Cv->get() + i64(c0) * n, n, Y.get(), n, out, true);
+            }
+        }
+        for (int l = 1; l <= tau; ++l) {
+            const int R = h.Rl(l);
+            const int W = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
+            if (!R || !W) continue;
+            const Partition& p = t.part(l);
+            const size_t sz = static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(W);
+            DVec P(sz), Q(sz);
+            seg_tn(p, h.Ul(l), n, R, corr.Cv->get(), n, W, P.get(), i64(R) * W, R, alpha);
+            seg_tn(p, h.Vl(l), n, R, corr.Cu->get(), n, W, Q.get(), i64(R) * W, R);
+            seg_xor_dot(p.nseg(), 1, P.get(), Q.get(), i64(R) * W, R, R, W, out, true);
         }
     };
-    cross(pb.base, pd);
-    cross(pd.base, pb);
+    if (same) {
+        cross(pb.base, pb, 2.0);
+    } else {
+        cross(pb.base, pd, 1.0);
+        cross(pd.base, pb, 1.0);
+    }
     // Correction pairs aligned by the finer level (product_rep.cpp:159-176,227-233):
-    // all coarse levels of one operand against fine level f of the other at once.
-    auto pairs = [&](const DProductRep& coarse, int W, const DProductRep& fine, int f) {
+    // coarse levels [c0, c0+W) columns of one operand against fine level f of the other.
+    auto pairs = [&](const DProductRep& coarse, int c0, int W, const DProductRep& fine, int f, double alpha) {
         const int Cf = fine.C[static_cast<size_t>(f - 1)];
         if (!W || !Cf) return;
         const Partition& p = t.part(f - 1);
-        DVec G1(static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf)), G2(static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf));
-        seg_tn(p, coarse.Cv->get(), n, W, fine.Cul(f), n, Cf, G1.get(), i64(W) * Cf, W);
-        seg_tn(p, fine.Cvl(f), n, Cf, coarse.Cu->get(), n, W, G2.get(), i64(W) * Cf, Cf);
+        const size_t sz = static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf);
+        DVec G1(sz), G2(sz);
+        seg_tn(p, coarse.Cv->get() + i64(c0) * n, n, W, fine.Cul(f), n, Cf, G1.get(), i64(W) * Cf, W, alpha);
+        seg_tn(p, fine.Cvl(f), n, Cf, coarse.Cu->get() + i64(c0) * n, n, W, G2.get(), i64(W) * Cf, Cf);
         seg_pair_dot(p.nseg(), 0, G1.get(), i64(W) * Cf, W, W, Cf, G2.get(), i64(W) * Cf, Cf, out, true);
     };
     for (int f = 1; f <= tau; ++f) {
-        pairs(pb, pb.coff[static_cast<size_t>(f - 1)] + pb.C[static_cast<size_t>(f - 1)], pd, f);  // i <= j: coarse from pb
-        pairs(pd, pd.coff[static_cast<size_t>(f - 1)], pb, f);                         // i > j: coarse from pd
+        const int cf = pb.coff[static_cast<size_t>(f - 1)];
+        if (same) {  // sum_{i<=f} + sum_{i<f} = 2 sum_{i<f} + (i = f)
+            pairs(pb, 0, cf, pb, f, 2.0);
+            pairs(pb, cf, pb.C[static_cast<size_t>(f - 1)], pb, f, 1.0);
+        } else {
+            pairs(pb, 0, cf + pb.C[static_cast<size_t>(f - 1)], pd, f, 1.0);  // i <= j: coarse from pb
+            pairs(pd, 0, pd.coff[static_cast<size_t>(f - 1)], pb, f, 1.0);    // i > j: coarse from pd
+        }
     }
 }
 

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
 #include <vector>
 
 namespace hg {
@@ -35,14 +36,22 @@ void prof_enable(bool on);
 /// Synchronizes, folds pending event pairs into totals, returns them.
 std::vector<ProfTotals> prof_read(bool reset);
 
+/// printf-style shape tag.
+std::string prof_tag(const char* fmt, ...);
+
 /// Records an event pair around the kernel(s) launched in its scope.
 class ProfScope {
 public:
     ProfScope(int cat, double flops, double bytes);
     ~ProfScope();
+    /// Shape tag for HG_PROF_DETAIL=1 (per-shape breakdown printed by prof_read).
+    void key(const std::string& k) {
+        if (a_) key_ = k;
+    }
 
 private:
     int cat_;
+    std::string key_;
     double flops_, bytes_;
     cudaEvent_t a_ = nullptr;
 };

@@ -237,6 +237,7 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     double rows = 0;
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_QR, 2.0 * rows * w * w, 16.0 * rows * w);
+    if (prof_enabled()) prof.key(prof_tag("qr%d w=%d blocks=%d rows=%d", int(pivot), w, int(blocks.size()), max_rows));
     if (pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<true>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -263,6 +264,7 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     double rows = 0;
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_FORM_Q, 4.0 * rows * w * qcols, 8.0 * rows * (w + 2.0 * qcols));
+    if (prof_enabled()) prof.key(prof_tag("formq w=%d q=%d blocks=%d rows=%d", w, qcols, int(blocks.size()), max_rows));
     HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     k_form_q<<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);
