@@ -92,7 +92,7 @@ public:
         }
         return *this;
     }
-    DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_), own_(o.own_) {
         o.p_ = nullptr;
         o.n_ = 0;
     }
@@ -101,14 +101,24 @@ public:
             release();
             p_ = o.p_;
             n_ = o.n_;
+            own_ = o.own_;
             o.p_ = nullptr;
             o.n_ = 0;
         }
         return *this;
     }
+    /// Non-owning view of n elements at p (see make_view).
+    static DBuf view(T* p, size_t n) {
+        DBuf b;
+        b.p_ = p;
+        b.n_ = n;
+        b.own_ = false;
+        return b;
+    }
     void alloc(size_t n) {
         release();
         n_ = n;
+        own_ = true;
         if (n) p_ = static_cast<T*>(dev_alloc(n * sizeof(T)));
     }
     void zero() {
@@ -131,15 +141,17 @@ public:
     size_t size() const { return n_; }
     bool empty() const { return n_ == 0; }
     void release() {
-        if (p_) dev_free(p_);
+        if (p_ && own_) dev_free(p_);
         p_ = nullptr;
         n_ = 0;
+        own_ = true;
     }
 
 private:
     void copy_from(const DBuf& o) {
         p_ = nullptr;
         n_ = 0;
+        own_ = true;
         if (o.n_) {
             alloc(o.n_);
             HG_CUDA(cudaMemcpyAsync(p_, o.p_, n_ * sizeof(T), cudaMemcpyDeviceToDevice, current().stream));
@@ -147,10 +159,16 @@ private:
     }
     T* p_ = nullptr;
     size_t n_ = 0;
+    bool own_ = true;
 };
 
 using DVec = DBuf<double>;
 using DVecP = std::shared_ptr<DVec>;
+
+/// Shared non-owning view of n doubles at p inside `owner` (kept alive by the view).
+inline DVecP make_view(const DVecP& owner, double* p, size_t n) {
+    return DVecP(new DVec(DVec::view(p, n)), [owner](DVec* d) { delete d; });
+}
 
 inline DVecP make_dvec(size_t n, bool zero = true) {
     auto p = std::make_shared<DVec>(n);

@@ -51,10 +51,6 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
     DProductRep rep;
     rep.base = b;
     rep.base.make_asymmetric();
-    // Left factors are rewritten: give the base its own copies (right factors stay aliased).
-    for (int l = 1; l <= tau; ++l)
-        if (rep.base.Rl(l)) rep.base.U[static_cast<size_t>(l - 1)] = std::make_shared<DVec>(*b.U[static_cast<size_t>(l - 1)]);
-    rep.base.leaves = std::make_shared<DVec>(*b.leaves);
     rep.C.assign(static_cast<size_t>(tau), 0);
     rep.coff.assign(static_cast<size_t>(tau), 0);
     for (int i = 1; i <= tau; ++i) {
@@ -62,17 +58,37 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         rep.C[static_cast<size_t>(i - 1)] = 2 * f.Rl(i);
         rep.sumC += rep.C[static_cast<size_t>(i - 1)];
     }
-    rep.Cu = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(rep.sumC, 1)), true);
-    rep.Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(rep.sumC, 1)), true);
+    // Every column the pipeline rewrites lives in ONE n-row panel, ordered
+    //   [U_tau | ... | U_2 | U_1 | Cu_1 | ... | Cu_tau | leaves]
+    // so the columns factor level i acts on (the base's coarser left factors
+    // U_{m<i} and the older corrections Cu_{<i}) are one contiguous block, and
+    // the final leaf step is a single call over the whole panel.
+    std::vector<int> ucum(static_cast<size_t>(tau + 1), 0);  // ucum[m] = sum_{m' <= m} R_m'
+    for (int m = 1; m <= tau; ++m) ucum[static_cast<size_t>(m)] = ucum[static_cast<size_t>(m - 1)] + rep.base.Rl(m);
+    const int sumR = ucum[static_cast<size_t>(tau)], cw = std::max(rep.sumC, 1), bm = f.bmax();
+    const int cuo = sumR, lo = sumR + cw, total = lo + bm;
+    DVecP store = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(total), false);
+    double* S = store->get();
+    panel_axpby(n, cw, 0.0, nullptr, 0, 0.0, S + i64(cuo) * n, n);
+    // Left factors are rewritten: the base gets its own copies (right factors stay aliased).
+    for (int m = 1; m <= tau; ++m) {
+        const int R = rep.base.Rl(m);
+        if (!R) continue;
+        double* dst = S + i64(sumR - ucum[static_cast<size_t>(m)]) * n;
+        panel_axpby(n, R, 1.0, b.Ul(m), n, 0.0, dst, n);
+        rep.base.U[static_cast<size_t>(m - 1)] = make_view(store, dst, static_cast<size_t>(n) * static_cast<size_t>(R));
+    }
+    rep.base.leaves = std::make_shared<DVec>(*b.leaves);
+    rep.Cu = make_view(store, S + i64(cuo) * n, static_cast<size_t>(n) * static_cast<size_t>(cw));
+    rep.Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(cw), true);
 
     for (int i = 1; i <= tau; ++i) {
         const int R = f.Rl(i);
         if (R == 0) continue;
-        // product_rep.cpp:84-90: older corrections' left factors.
-        level_op(f, i, inverse, rep.Cu->get(), rep.coff[static_cast<size_t>(i - 1)]);
-        // product_rep.cpp:92-104: the running base's coarser left factors.
-        for (int m = 1; m < i; ++m)
-            if (rep.base.Rl(m)) level_op(f, i, inverse, rep.base.Ul(m), rep.base.Rl(m));
+        // product_rep.cpp:84-104: older corrections' left factors and the
+        // running base's coarser left factors, in one call.
+        const int us = ucum[static_cast<size_t>(i - 1)];
+        level_op(f, i, inverse, S + i64(cuo - us) * n, us + rep.coff[static_cast<size_t>(i - 1)]);
         // product_rep.cpp:106-119: spawn c.u = p, c.v = B_sub^T q.
         const Partition& p = f.tree->part(i);
         const int C2 = 2 * R;
@@ -96,17 +112,10 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         hodlr_apply(rep.base, Q.get(), n, C2, rep.Cvl(i), n, i, tau, true, true, 0.0);
     }
     // product_rep.cpp:124-152: leaf factor on every stored left factor and the leaves.
-    leaf_step(f, inverse, rep.Cu->get(), rep.sumC);
-    for (int m = 1; m <= tau; ++m)
-        if (rep.base.Rl(m)) leaf_step(f, inverse, rep.base.Ul(m), rep.base.Rl(m));
-    {
-        const int bm = f.bmax();
-        DVec P(static_cast<size_t>(n) * static_cast<size_t>(bm));
-        leaves_panel(*f.tree, rep.base.leaves->get(), P.get(), true);
-        leaf_step(f, inverse, P.get(), bm);
-        leaves_panel(*f.tree, rep.base.leaves->get(), P.get(), false);
-        rep.base.leaves_zero = false;
-    }
+    leaves_panel(*f.tree, rep.base.leaves->get(), S + i64(lo) * n, true);
+    leaf_step(f, inverse, S, total);
+    leaves_panel(*f.tree, rep.base.leaves->get(), S + i64(lo) * n, false);
+    rep.base.leaves_zero = false;
     return rep;
 }
 
