@@ -5,6 +5,7 @@
 
 #include "factor.cuh"
 #include "prof.cuh"
+#include "tile.cuh"
 
 namespace hg {
 
@@ -313,6 +314,8 @@ __global__ void __launch_bounds__(FNT) k_leaf_solve(LeafSolveArgs g) {
     }
 }
 
+#include "leafsolve_tc.cuh"
+
 // --------------------------------------------------------------- capacitance
 struct CapLuArgs {
     int R;
@@ -499,6 +502,22 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
     const double rows = double(f.n());
     ProfScope prof(PROF_LEAF_SOLVE, 2.0 * rows * m * w, 8.0 * (rows * m + 2.0 * rows * w));
     if (prof_enabled()) prof.key(prof_tag("leafsolve w=%d", w));
+    if (f.all_llt && f.bmax() <= TS_MAX) {
+        static bool attr = false;
+        if (!attr) {
+            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc), TS_SMEM);
+            attr = true;
+        }
+        // Column tiles per CTA: enough CTAs for ~4 waves, the factor loaded once per CTA.
+        const int ct = cdiv(w, TS_NC);
+        const int groups = std::max(1, std::min(ct, cdiv(4 * 2 * current().num_sms, lv.nseg())));
+        const int cpt = cdiv(ct, groups);
+        LeafSolveTcArgs a{lv.dbounds(), f.bmax(), f.leaf_fac->get(), Y, ldy, w, ct, cpt};
+        k_leaf_solve_tc<<<unsigned(lv.nseg()) * unsigned(cdiv(ct, cpt)), TS_THREADS, TS_SMEM, current().stream>>>(a);
+        HG_LAUNCH();
+        count_launch();
+        return;
+    }
     set_smem(reinterpret_cast<const void*>(k_leaf_solve), smem);
     LeafSolveArgs g{lv.dbounds(), f.bmax(), f.leaf_fac->get(), f.leaf_kind->get(), f.leaf_piv->get(), Y, ldy, w};
     dim3 grid(unsigned(lv.nseg()), unsigned(cdiv(w, SOLVE_COLS)));
@@ -587,6 +606,13 @@ DFactor factorize(const DHodlr& h, int orient) {
         k_leaf_factor<<<unsigned(nl), FNT, use ? smem : 0, current().stream>>>(g);
         HG_LAUNCH();
         count_launch();
+        const std::vector<int> kinds = f.leaf_kind->download();
+        f.all_llt = std::all_of(kinds.begin(), kinds.end(), [](int k) { return k == 1; });
+        if (f.all_llt && bm <= TS_MAX) {  // tensor-core solve path: invert diagonal blocks once
+            k_leaf_diag_inv<<<unsigned(nl), 128, 0, current().stream>>>(lv.dbounds(), bm, f.leaf_fac->get());
+            HG_LAUNCH();
+            count_launch();
+        }
     }
     // Working left factors (factorization.cpp:75-119): Wbar = Abar^{-1} F.
     f.Wbar = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(std::max(f.sumR, 1)), false);

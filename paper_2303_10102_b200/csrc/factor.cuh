@@ -26,6 +26,7 @@ struct DFactor {
     std::shared_ptr<DBuf<int>> leaf_piv;   // LU row swaps per leaf (bmax each)
     DVecP leaf_ld;                         // log|det| per leaf
     std::shared_ptr<DBuf<int>> leaf_sign;  // +1 / -1 (sign of det)
+    bool all_llt = false;                  // every leaf Cholesky-factored
     std::vector<DVecP> cap;                // [i-1] nodes x (2R)^2 LU
     std::vector<std::shared_ptr<DBuf<int>>> cap_piv;  // [i-1] nodes x 2R swaps
     std::vector<DVecP> cap_ld;             // [i-1] nodes
