@@ -1,9 +1,10 @@
 // Segmented FP64 GEMM engine and deterministic reductions (see kernels.cuh).
 //
-// Tile engine (tile.cuh): 64x64 output tile per 256-thread CTA on the FP64
-// tensor cores (DMMA m8n8k4), K staged 16 at a time through shared memory
-// with a one-step register prefetch of the next global tile. Split-K partials are reduced in a fixed
-// order so every result is bitwise reproducible run to run.
+// Tile engine (tile.cuh): a TBM x TBN output tile per 128-thread CTA on the
+// FP64 tensor cores (DMMA m8n8k4), the tile shape picked per call from the
+// problem's M and N, K staged 16 at a time through a cp.async pipeline.
+// Split-K partials are reduced in a fixed order so every result is bitwise
+// reproducible run to run.
 #include "kernels.cuh"
 #include "prof.cuh"
 #include "tile.cuh"
@@ -21,7 +22,6 @@ __device__ __forceinline__ int cdiv_d(int a, int b) { return (a + b - 1) / b; }
 // Short-K GEMMs (seg_nn: k = rank; leaf_mm: k = leaf size) are latency-bound:
 // two stages (40 KB) keep five CTAs resident per SM instead of three.
 constexpr int NS_SHORT = 2;
-constexpr int SMEM_SHORT = tile::smem_bytes(NS_SHORT);
 constexpr int SEG_CHUNK = 512;  // rows per split-K work item
 constexpr int RED_BLOCKS = 296; // 2 x 148 SMs; fixed => deterministic reductions
 
@@ -43,17 +43,18 @@ struct SegTnArgs {
 };
 
 /// T_s tile = A[rows]^T B[rows]: both operands k-contiguous (rows = k).
+template <int TBM, int TBN>
 __global__ void __launch_bounds__(THREADS) k_seg_tn(SegTnArgs g) {
     extern __shared__ double smem[];
     const WorkItem it = g.items[blockIdx.x];
-    const int m0 = (blockIdx.y % g.tiles_m) * BM, n0 = (blockIdx.y / g.tiles_m) * BN;
-    tile::LoadKC la{g.A + it.row0 + i64(m0) * g.lda, g.lda, it.rows, g.ca - m0};
-    tile::LoadKC lb{g.B + it.row0 + i64(n0) * g.ldb, g.ldb, it.rows, g.cb - n0};
-    Acc acc;
+    const int m0 = (blockIdx.y % g.tiles_m) * TBM, n0 = (blockIdx.y / g.tiles_m) * TBN;
+    tile::LoadKCT<TBM> la{g.A + it.row0 + i64(m0) * g.lda, g.lda, it.rows, g.ca - m0};
+    tile::LoadKCT<TBN> lb{g.B + it.row0 + i64(n0) * g.ldb, g.ldb, it.rows, g.cb - n0};
+    tile::AccT<TBM / 16, TBN / 16> acc;
     acc.zero();
-    tile::run(la, lb, cdiv_d(it.rows, BK), smem, acc);
+    tile::run_t<tile::STAGES, TBM, TBN>(la, lb, cdiv_d(it.rows, BK), smem, acc);
     double* o = g.out + (g.direct ? i64(it.seg) : i64(blockIdx.x)) * g.ostride;
-    tile::for_each(acc, [&](int mi, int ni, double v) {
+    tile::for_each_t<TBM, TBN>(acc, [&](int mi, int ni, double v) {
         const int m = m0 + mi, n = n0 + ni;
         if (m >= g.ca || n >= g.cb) return;
         double* p = o + m + i64(n) * g.ldo;
@@ -93,18 +94,19 @@ struct SegNnArgs {
 };
 
 /// Y[rows] = X[rows] T_sel: X m-contiguous (rows = m), T k-contiguous.
+template <int TBN>
 __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
     extern __shared__ double smem[];
     const WorkItem it = g.items[blockIdx.x];
-    const int n0 = blockIdx.y * BN;
+    const int n0 = blockIdx.y * TBN;
     const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.map.mult * g.tstride +
                        i64(g.map.add) * g.tstride + ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
-    tile::LoadMC la{g.X + it.row0, g.ldx, it.rows, g.k};
-    tile::LoadKC lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
-    Acc acc;
+    tile::LoadMCT<BM> la{g.X + it.row0, g.ldx, it.rows, g.k};
+    tile::LoadKCT<TBN> lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
+    tile::AccT<BM / 16, TBN / 16> acc;
     acc.zero();
-    tile::run<NS_SHORT>(la, lb, cdiv_d(g.k, BK), smem, acc);
-    tile::for_each(acc, [&](int m, int ni, double v) {
+    tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(g.k, BK), smem, acc);
+    tile::for_each_t<BM, TBN>(acc, [&](int m, int ni, double v) {
         const int n = n0 + ni;
         if (n >= g.w || m >= it.rows) return;
         double* p = g.Y + i64(it.row0 + m) + i64(n) * g.ldy;
@@ -129,25 +131,25 @@ struct LeafMmArgs {
 
 /// Y[leaf rows] = op(L_b) X[leaf rows]; op(L) is m-contiguous (no transpose)
 /// or k-contiguous (transpose), X is k-contiguous.
-template <bool TRANS>
+template <bool TRANS, int TBN>
 __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     extern __shared__ double smem[];
     const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
     const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * BM;
     if (r0 >= m) return;
-    const int n0 = blockIdx.y * BN;
+    const int n0 = blockIdx.y * TBN;
     const double* Lb = g.L + i64(b) * g.lstride;
-    tile::LoadKC lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
-    Acc acc;
+    tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
+    tile::AccT<BM / 16, TBN / 16> acc;
     acc.zero();
     if (!TRANS) {
-        tile::LoadMC la{Lb + r0, g.ldl, m - r0, m};
-        tile::run<NS_SHORT>(la, lb, cdiv_d(m, BK), smem, acc);
+        tile::LoadMCT<BM> la{Lb + r0, g.ldl, m - r0, m};
+        tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
     } else {
-        tile::LoadKC la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
-        tile::run<NS_SHORT>(la, lb, cdiv_d(m, BK), smem, acc);
+        tile::LoadKCT<BM> la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
+        tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
     }
-    tile::for_each(acc, [&](int mi0, int ni, double v) {
+    tile::for_each_t<BM, TBN>(acc, [&](int mi0, int ni, double v) {
         const int mi = r0 + mi0, n = n0 + ni;
         if (n >= g.w || mi >= m) return;
         double* p = g.Y + i64(lo + mi) + i64(n) * g.ldy;
@@ -282,17 +284,6 @@ void reduce(F f, i64 total, double* out, bool accumulate) {
     c.launches += 2;
 }
 
-void smem_attrs() {
-    static bool done = false;
-    if (done) return;
-    const void* fns[] = {reinterpret_cast<const void*>(k_seg_tn), reinterpret_cast<const void*>(k_seg_nn),
-                         reinterpret_cast<const void*>(k_leaf_mm<true>),
-                         reinterpret_cast<const void*>(k_leaf_mm<false>)};
-    for (const void* f : fns)
-        HG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tile::SMEM_BYTES));
-    done = true;
-}
-
 }  // namespace
 
 void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* B, i64 ldb, int cb, double* T,
@@ -303,29 +294,36 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
     if (prof_enabled()) prof.key(prof_tag("tn nseg=%d ca=%d cb=%d", p.nseg(), ca, cb));
     const TileList& tl = p.tiles(SEG_CHUNK);
-    const int tiles_m = cdiv(ca, BM), tiles_n = cdiv(cb, BN);
-    smem_attrs();
+    const int tbm = tile::tile_for(ca), tbn = tile::tile_for(cb);
+    const int tiles_m = cdiv(ca, tbm), tiles_n = cdiv(cb, tbn);
     SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
-    dim3 grid(unsigned(tl.count), unsigned(tiles_m * tiles_n));
-    if (tl.one_per_seg) {
-        k_seg_tn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
-        HG_LAUNCH();
-        ++c.launches;
-        return;
+    DVec ws;
+    if (!tl.one_per_seg) {
+        const i64 wstride = i64(ca) * cb;
+        ws.alloc(static_cast<size_t>(wstride) * static_cast<size_t>(tl.count));
+        g.out = ws.get();
+        g.ostride = wstride;
+        g.ldo = ca;
+        g.direct = 0;
     }
-    const i64 wstride = i64(ca) * cb;
-    DVec ws(static_cast<size_t>(wstride) * static_cast<size_t>(tl.count));
-    g.out = ws.get();
-    g.ostride = wstride;
-    g.ldo = ca;
-    g.direct = 0;
-    k_seg_tn<<<grid, THREADS, tile::SMEM_BYTES, c.stream>>>(g);
+    const dim3 grid(unsigned(tl.count), unsigned(tiles_m * tiles_n));
+    with_tile(tbm, [&](auto TM) {
+        with_tile(tbn, [&](auto TN) {
+            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+            attr_once<k_seg_tn<M, N>>(bytes);
+            k_seg_tn<M, N><<<grid, THREADS, bytes, c.stream>>>(g);
+        });
+    });
     HG_LAUNCH();
+    ++c.launches;
+    if (tl.one_per_seg) return;
+    const i64 wstride = i64(ca) * cb;
     dim3 rgrid(unsigned(cdiv(wstride, 256)), unsigned(p.nseg()));
     k_seg_reduce<<<rgrid, 256, 0, c.stream>>>(ws.get(), wstride, ca, cb, tl.seg_first.get(), T, tstride, ldt, alpha,
                                               beta);
     HG_LAUNCH();
-    c.launches += 2;
+    ++c.launches;
 }
 
 void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T, i64 tstride, int ldt, TMap map,
@@ -340,10 +338,14 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
     if (prof_enabled()) prof.key(prof_tag("nn nseg=%d k=%d w=%d", p.nseg(), k, w));
     const TileList& tl = p.tiles(BM);
-    smem_attrs();
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
-    dim3 grid(unsigned(tl.count), unsigned(cdiv(w, BN)));
-    k_seg_nn<<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
+    const int tbn = tile::tile_for(w);
+    with_tile(tbn, [&](auto TN) {
+        constexpr int N = decltype(TN)::value;
+        constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
+        attr_once<k_seg_nn<N>>(bytes);
+        k_seg_nn<N><<<dim3(unsigned(tl.count), unsigned(cdiv(w, N))), THREADS, bytes, c.stream>>>(g);
+    });
     HG_LAUNCH();
     ++c.launches;
 }
@@ -353,16 +355,23 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     if (w <= 0) return;
     auto& c = current();
     const int rt = cdiv(leaves.max_seg(), BM);
-    smem_attrs();
     const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
     ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + rows * w * (beta != 0.0 ? 3.0 : 2.0)));
     if (prof_enabled()) prof.key(prof_tag("leafmm w=%d tr=%d", w, int(trans)));
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
-    dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, BN)));
-    if (trans)
-        k_leaf_mm<true><<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
-    else
-        k_leaf_mm<false><<<grid, THREADS, SMEM_SHORT, c.stream>>>(g);
+    const int tbn = tile::tile_for(w);
+    with_tile(tbn, [&](auto TN) {
+        constexpr int N = decltype(TN)::value;
+        constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
+        const dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(w, N)));
+        if (trans) {
+            attr_once<k_leaf_mm<true, N>>(bytes);
+            k_leaf_mm<true, N><<<grid, THREADS, bytes, c.stream>>>(g);
+        } else {
+            attr_once<k_leaf_mm<false, N>>(bytes);
+            k_leaf_mm<false, N><<<grid, THREADS, bytes, c.stream>>>(g);
+        }
+    });
     HG_LAUNCH();
     ++c.launches;
 }

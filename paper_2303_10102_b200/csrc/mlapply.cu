@@ -53,20 +53,21 @@ struct ProjArgs {
 
 __device__ __forceinline__ int cdiv_i(int a, int b) { return (a + b - 1) / b; }
 
+template <int TBM, int TBN>
 __global__ void __launch_bounds__(THREADS) k_ml_proj(ProjArgs g) {
     extern __shared__ double smem[];
     const MlItem it = g.items[blockIdx.x];
     const int l = it.level, R = g.L.R[l];
-    const int m0 = (blockIdx.y / g.tiles_n) * BM, n0 = (blockIdx.y % g.tiles_n) * BN;
+    const int m0 = (blockIdx.y / g.tiles_n) * TBM, n0 = (blockIdx.y % g.tiles_n) * TBN;
     if (m0 >= R) return;
-    tile::LoadKC la{g.L.P[l] + it.row0 + i64(m0) * g.n, g.n, it.rows, R - m0};
-    tile::LoadKC lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
-    Acc acc;
+    tile::LoadKCT<TBM> la{g.L.P[l] + it.row0 + i64(m0) * g.n, g.n, it.rows, R - m0};
+    tile::LoadKCT<TBN> lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
+    tile::AccT<TBM / 16, TBN / 16> acc;
     acc.zero();
-    tile::run(la, lb, cdiv_i(it.rows, BK), smem, acc);
+    tile::run_t<tile::STAGES, TBM, TBN>(la, lb, cdiv_i(it.rows, BK), smem, acc);
     const i64 blk = i64(R) * g.s;
     double* o = g.L.ws[l] ? g.L.ws[l] + i64(it.chunk) * blk : g.L.T[l] + i64(it.seg) * blk;
-    tile::for_each(acc, [&](int mi, int ni, double v) {
+    tile::for_each_t<TBM, TBN>(acc, [&](int mi, int ni, double v) {
         const int m = m0 + mi, c = n0 + ni;
         if (m < R && c < g.s) o[m + i64(c) * R] = v;
     });
@@ -107,6 +108,7 @@ struct UpdArgs {
 /// A operand: rows of the update panels, K = concatenated level columns.
 struct LoadUpdA {
     static constexpr bool KC = false;
+    static constexpr int ROWS = BM;
     const MlLevels* L;
     int row0, rows;
     i64 n;
@@ -126,8 +128,10 @@ struct LoadUpdA {
 };
 
 /// B operand: T_l of the sibling segment at each level (k-contiguous, ld R_l).
+template <int TBN>
 struct LoadUpdB {
     static constexpr bool KC = true;
+    static constexpr int ROWS = TBN;
     const MlLevels* L;
     int leaf, tau, s, n0;
     __device__ __forceinline__ void issue(double* S, int kt) const {
@@ -138,7 +142,7 @@ struct LoadUpdB {
         const double* base = L->T[l] + i64(seg) * R * s + i64(n0) * R;
         const int k = threadIdx.x & 15, kk = kb + k;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < TBN / 8; ++q) {
             const int c = (threadIdx.x >> 4) + 8 * q;
             const bool v = kk < R && n0 + c < s;
             tile::cp_async8(S + c * tile::LD_KC + k, v ? base + kk + i64(c) * R : base, v);
@@ -146,6 +150,7 @@ struct LoadUpdB {
     }
 };
 
+template <int TBN>
 __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
     extern __shared__ double smem[];
     __shared__ MlLevels L;
@@ -153,13 +158,13 @@ __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
         reinterpret_cast<int*>(&L)[i] = reinterpret_cast<const int*>(&g.L)[i];
     __syncthreads();
     const WorkItem it = g.items[blockIdx.x];
-    const int n0 = blockIdx.y * BN;
+    const int n0 = blockIdx.y * TBN;
     LoadUpdA la{&L, it.row0, it.rows, g.n};
-    LoadUpdB lb{&L, it.seg, g.tau, g.s, n0};
-    Acc acc;
+    LoadUpdB<TBN> lb{&L, it.seg, g.tau, g.s, n0};
+    tile::AccT<BM / 16, TBN / 16> acc;
     acc.zero();
-    tile::run<2>(la, lb, L.ktoff[L.nl], smem, acc);
-    tile::for_each(acc, [&](int m, int ni, double v) {
+    tile::run_t<2, BM, TBN>(la, lb, L.ktoff[L.nl], smem, acc);
+    tile::for_each_t<BM, TBN>(acc, [&](int m, int ni, double v) {
         const int c = n0 + ni;
         if (c >= g.s || m >= it.rows) return;
         double* p = g.Y + i64(it.row0 + m) + i64(c) * g.ldy;
@@ -247,16 +252,6 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
     return ref;
 }
 
-void ml_attrs() {
-    static bool done = false;
-    if (done) return;
-    HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_ml_proj), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tile::SMEM_BYTES));
-    HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_ml_update),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tile::smem_bytes(2)));
-    done = true;
-}
-
 }  // namespace
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
@@ -279,7 +274,6 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         return;
     }
     if (int(lv.size()) > MAXL) throw std::length_error("hodlr_apply: too many levels");
-    ml_attrs();
     auto& c = current();
     const ItemPlan& ip = item_plan(t, lmin, lmax);
     MlLevels L{};
@@ -311,11 +305,20 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
         prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
     }
-    int max_tiles_m = 1;
-    for (int i = 0; i < L.nl; ++i) max_tiles_m = std::max(max_tiles_m, (L.R[i] + BM - 1) / BM);
-    const int tiles_n = (s + BN - 1) / BN;
+    int rmax = 1;
+    for (int i = 0; i < L.nl; ++i) rmax = std::max(rmax, L.R[i]);
+    const int tbm = tile::tile_for(rmax), tbn = tile::tile_for(s);
+    const int max_tiles_m = (rmax + tbm - 1) / tbm;
+    const int tiles_n = (s + tbn - 1) / tbn;
     ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n};
-    k_ml_proj<<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, tile::SMEM_BYTES, c.stream>>>(pa);
+    with_tile(tbm, [&](auto TM) {
+        with_tile(tbn, [&](auto TN) {
+            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+            attr_once<k_ml_proj<M, N>>(bytes);
+            k_ml_proj<M, N><<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
+        });
+    });
     HG_LAUNCH();
     ++c.launches;
     if (ip.nred) {
@@ -328,7 +331,12 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     const TileList& tl = t.leaves().tiles(BM);
     UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta};
-    k_ml_update<<<dim3(unsigned(tl.count), unsigned(tiles_n)), THREADS, tile::smem_bytes(2), c.stream>>>(ua);
+    with_tile(tbn, [&](auto TN) {
+        constexpr int N = decltype(TN)::value;
+        constexpr int bytes = tile::smem_bytes_t(2, BM, N);
+        attr_once<k_ml_update<N>>(bytes);
+        k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_n)), THREADS, bytes, c.stream>>>(ua);
+    });
     HG_LAUNCH();
     ++c.launches;
 }

@@ -88,6 +88,7 @@ using tile::BN;
 /// shared layout (a computing loader for tile::run).
 struct LoadMatern {
     static constexpr bool KC = false;
+    static constexpr int ROWS = 64;
     const double* x;
     int r0, n;
     Poly P;

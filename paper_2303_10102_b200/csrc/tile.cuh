@@ -1,38 +1,52 @@
 // FP64 tensor-core tile engine shared by every GEMM-shaped kernel.
 //
-// CTA tile 64x64, 4 warps in a 2x2 grid, each warp 32x32 = 4x4 DMMA m8n8k4
-// tiles (mma.sync .f64 — the FP64 tensor path on sm_100a; tcgen05 has no f64
-// kind). K advances 16 at a time through a 3-stage cp.async pipeline.
+// CTA tile TBM x TBN (multiples of 16, 16..96), 4 warps in a 2x2 grid, each
+// warp (TBM/2) x (TBN/2) = (TBM/16) x (TBN/16) DMMA m8n8k4 tiles (mma.sync
+// .f64 — the FP64 tensor path on sm_100a; tcgen05 has no f64 kind). K
+// advances 16 at a time through a multi-stage cp.async pipeline. The tile
+// shape is picked per call from the problem's M and N (tile_for): HODLR
+// ranks and panel widths are 40, 80, 3.. so a fixed 64x64 tile wastes up to
+// 60% of the tensor-core work in padding.
 //
 // Shared layouts follow each operand's global contiguity so that both the
 // cp.async copies and the fragment loads are bank-conflict free:
 //   KC ("k-contiguous", e.g. a column-major panel whose rows are the
 //       reduction index): smem [m][k], row stride 20 doubles;
 //   MC ("m-contiguous", e.g. a column-major panel whose rows are the output
-//       rows): smem [k][m], row stride 68 doubles.
+//       rows): smem [k][m], row stride ROWS + 4 doubles.
 // Both strides are 4 mod 16 doubles: a half-warp's fragment (g = 0..3,
 // t = 0..3) maps to 16 distinct 8-byte bank pairs.
 #pragma once
 
 #include <cstdint>
+#include <stdexcept>
+#include <type_traits>
+
+#include "common.cuh"
 
 namespace hg {
 namespace tile {
 
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
 constexpr int LD_KC = BK + 4;  // 20
-constexpr int LD_MC = BM + 4;  // 68
-constexpr int TILE_ELEMS = (BM * LD_KC > BK * LD_MC) ? BM * LD_KC : BK * LD_MC;  // one operand stage
+constexpr int LD_MC = BM + 4;  // 68 (64-row tiles)
 
-struct Acc {
-    double v[4][4][2];
+/// Shared elements of one operand stage with ROWS tile rows (either layout).
+constexpr int stage_elems(int rows) { return (rows * LD_KC > BK * (rows + 4)) ? rows * LD_KC : BK * (rows + 4); }
+constexpr int TILE_ELEMS = stage_elems(64);
+
+/// Accumulators of one warp: (TBM/16) x (TBN/16) DMMA tiles.
+template <int WM, int WN>
+struct AccT {
+    double v[WM][WN][2];
     __device__ __forceinline__ void zero() {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < WM; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[i][j][0] = v[i][j][1] = 0.0;
+            for (int j = 0; j < WN; ++j) v[i][j][0] = v[i][j][1] = 0.0;
     }
 };
+using Acc = AccT<4, 4>;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -51,44 +65,47 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-/// Fragment element (m, k) of an operand stage in its layout.
-template <bool KC>
+/// Fragment element (m, k) of an operand stage with ROWS rows in its layout.
+template <bool KC, int ROWS>
 __device__ __forceinline__ double frag(const double* S, int m, int k) {
-    return KC ? S[m * LD_KC + k] : S[k * LD_MC + m];
+    return KC ? S[m * LD_KC + k] : S[k * (ROWS + 4) + m];
 }
 
-/// One BK slice: acc += A(:, k) B(:, k)^T over the warp's 32x32 sub-tile.
-template <bool AKC, bool BKC>
-__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, Acc& acc) {
+/// One BK slice: acc += A(:, k) B(:, k)^T over the warp's sub-tile.
+template <bool AKC, bool BKC, int TBM, int TBN>
+__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, AccT<TBM / 16, TBN / 16>& acc) {
+    constexpr int WM = TBM / 16, WN = TBN / 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
-        double a[4], b[4];
+        double a[WM], b[WN];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = frag<AKC>(As, wm + i * 8 + g, k4 + t);
+        for (int i = 0; i < WM; ++i) a[i] = frag<AKC, TBM>(As, wm + i * 8 + g, k4 + t);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = frag<BKC>(Bs, wn + j * 8 + g, k4 + t);
+        for (int j = 0; j < WN; ++j) b[j] = frag<BKC, TBN>(Bs, wn + j * 8 + g, k4 + t);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < WM; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc.v[i][j], a[i], b[j]);
+            for (int j = 0; j < WN; ++j) dmma(acc.v[i][j], a[i], b[j]);
     }
 }
 
-/// Pipelined main loop. Loader objects provide
-///   static constexpr bool KC;
+/// Pipelined main loop over a TBM x TBN tile. Loader objects provide
+///   static constexpr bool KC;  static constexpr int ROWS;
 ///   __device__ void issue(double* stage, int kt);   // cp.async one BK slice
-template <int NS = STAGES, class LA, class LB>
-__device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Acc& acc) {
+template <int NS, int TBM, int TBN, class LA, class LB>
+__device__ __forceinline__ void run_t(LA& la, LB& lb, int ktiles, double* smem, AccT<TBM / 16, TBN / 16>& acc) {
+    static_assert(LA::ROWS == TBM && LB::ROWS == TBN, "loader extents must match the tile");
+    constexpr int AE = stage_elems(TBM), BE = stage_elems(TBN);
     double* As = smem;
-    double* Bs = smem + NS * TILE_ELEMS;
+    double* Bs = smem + NS * AE;
 #pragma unroll
     for (int s = 0; s < NS - 1; ++s) {
         if (s < ktiles) {
-            la.issue(As + s * TILE_ELEMS, s);
-            lb.issue(Bs + s * TILE_ELEMS, s);
+            la.issue(As + s * AE, s);
+            lb.issue(Bs + s * BE, s);
         }
         cp_commit();
     }
@@ -97,23 +114,34 @@ __device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Ac
         __syncthreads();  // tile kt landed; every warp is done with tile kt-1's buffer
         const int nk = kt + NS - 1;
         if (nk < ktiles) {
-            la.issue(As + (nk % NS) * TILE_ELEMS, nk);
-            lb.issue(Bs + (nk % NS) * TILE_ELEMS, nk);
+            la.issue(As + (nk % NS) * AE, nk);
+            lb.issue(Bs + (nk % NS) * BE, nk);
         }
         cp_commit();
         const int st = kt % NS;
-        mma_stage<LA::KC, LB::KC>(As + st * TILE_ELEMS, Bs + st * TILE_ELEMS, acc);
+        mma_stage<LA::KC, LB::KC, TBM, TBN>(As + st * AE, Bs + st * BE, acc);
     }
     cp_wait<0>();
 }
 
-constexpr int smem_bytes(int ns) { return 2 * ns * TILE_ELEMS * int(sizeof(double)); }
+/// 64x64 shorthand (kernels written before the shape-adaptive engine).
+template <int NS = STAGES, class LA, class LB>
+__device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Acc& acc) {
+    run_t<NS, 64, 64>(la, lb, ktiles, smem, acc);
+}
+
+constexpr int smem_bytes_t(int ns, int tbm, int tbn) {
+    return ns * (stage_elems(tbm) + stage_elems(tbn)) * int(sizeof(double));
+}
+constexpr int smem_bytes(int ns) { return smem_bytes_t(ns, 64, 64); }
 constexpr int SMEM_BYTES = smem_bytes(STAGES);
 
 /// Column-major operand whose rows are the reduction index k (k-contiguous):
 /// element (k, m) at base[k + m * ld], valid for k < kmax, m < mmax.
-struct LoadKC {
+template <int R>
+struct LoadKCT {
     static constexpr bool KC = true;
+    static constexpr int ROWS = R;
     const double* base;
     long long ld;
     int kmax, mmax;
@@ -121,46 +149,97 @@ struct LoadKC {
         const int k = threadIdx.x & 15;
         const int kk = kt * BK + k;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < R / 8; ++q) {
             const int m = (threadIdx.x >> 4) + 8 * q;
             const bool v = kk < kmax && m < mmax;
             cp_async8(S + m * LD_KC + k, v ? base + kk + m * ld : base, v);
         }
     }
 };
+using LoadKC = LoadKCT<64>;
 
 /// Column-major operand whose rows are the output index m (m-contiguous):
 /// element (m, k) at base[m + k * ld], valid for m < mmax, k < kmax.
-struct LoadMC {
+template <int R>
+struct LoadMCT {
     static constexpr bool KC = false;
+    static constexpr int ROWS = R;
     const double* base;
     long long ld;
     int mmax, kmax;
     __device__ __forceinline__ void issue(double* S, int kt) const {
-        const int m = threadIdx.x & 63;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int k = (threadIdx.x >> 6) + 2 * q;
+        for (int q = 0; q < R / 8; ++q) {
+            const int e = threadIdx.x + THREADS * q;
+            const int m = e % R, k = e / R;
             const int kk = kt * BK + k;
             const bool v = m < mmax && kk < kmax;
-            cp_async8(S + k * LD_MC + m, v ? base + m + kk * ld : base, v);
+            cp_async8(S + k * (R + 4) + m, v ? base + m + kk * ld : base, v);
         }
     }
 };
+using LoadMC = LoadMCT<64>;
 
 /// Visit every accumulator element owned by this thread: f(m, n, value).
-template <class F>
-__device__ __forceinline__ void for_each(const Acc& acc, F&& f) {
+template <int TBM, int TBN, class F>
+__device__ __forceinline__ void for_each_t(const AccT<TBM / 16, TBN / 16>& acc, F&& f) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TBM / 16; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < TBN / 16; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) f(wm + i * 8 + g, wn + j * 8 + 2 * t + e, acc.v[i][j][e]);
 }
+template <class F>
+__device__ __forceinline__ void for_each(const Acc& acc, F&& f) {
+    for_each_t<64, 64>(acc, f);
+}
+
+/// Tile extent (16..96, multiple of 16) for a problem extent x: the one with
+/// the least padding (ties -> larger tile).
+inline int tile_for(int x) {
+    if (x <= 16) return 16;
+    if (x <= 32) return 32;
+    if (x <= 48) return 48;
+    int best = 64, waste = 1 << 30;
+    for (int t : {96, 80, 64}) {
+        const int w = (x + t - 1) / t * t - x;
+        if (w < waste) {
+            waste = w;
+            best = t;
+        }
+    }
+    return best;
+}
 
 }  // namespace tile
+
+/// Host: run f(std::integral_constant<int, T>) for the tile extent t.
+template <class F>
+void with_tile(int t, F&& f) {
+    switch (t) {
+        case 16: f(std::integral_constant<int, 16>{}); break;
+        case 32: f(std::integral_constant<int, 32>{}); break;
+        case 48: f(std::integral_constant<int, 48>{}); break;
+        case 64: f(std::integral_constant<int, 64>{}); break;
+        case 80: f(std::integral_constant<int, 80>{}); break;
+        case 96: f(std::integral_constant<int, 96>{}); break;
+        default: throw std::logic_error("with_tile: unsupported tile extent");
+    }
+}
+
+/// Host: opt the kernel KFN into `bytes` of dynamic shared memory (once).
+template <auto KFN>
+void attr_once(int bytes) {
+    static bool done = false;
+    if (done) return;
+    if (bytes > 48 * 1024)
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(KFN), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes));
+    done = true;
+}
+
 }  // namespace hg
