@@ -198,21 +198,13 @@ __device__ __forceinline__ void for_each(const Acc& acc, F&& f) {
     for_each_t<64, 64>(acc, f);
 }
 
-/// Tile extent (16..96, multiple of 16) for a problem extent x: the one with
-/// the least padding (ties -> larger tile).
+/// Tile extent (16..96, multiple of 16) for a problem extent x: the smallest
+/// single tile that covers x up to 96; beyond, 64 or 80, whichever pads less
+/// (96-wide tiles over many column blocks cost occupancy: 48 accumulators).
 inline int tile_for(int x) {
-    if (x <= 16) return 16;
-    if (x <= 32) return 32;
-    if (x <= 48) return 48;
-    int best = 64, waste = 1 << 30;
-    for (int t : {96, 80, 64}) {
-        const int w = (x + t - 1) / t * t - x;
-        if (w < waste) {
-            waste = w;
-            best = t;
-        }
-    }
-    return best;
+    if (x <= 96) return (x + 15) / 16 * 16 < 16 ? 16 : (x + 15) / 16 * 16;
+    const int w64 = (x + 63) / 64 * 64 - x, w80 = (x + 79) / 80 * 80 - x;
+    return w80 < w64 ? 80 : 64;
 }
 
 }  // namespace tile
