@@ -158,25 +158,25 @@ protected:
             if (j < 0 && nugget_ != 0.0) panel_axpby(n_, s, nugget_, V, ldv, 1.0, Y, ldy);
             return;
         }
-        const int nch = cdiv(n_, MC_ROWS);
-        const size_t msz = static_cast<size_t>(nch) * static_cast<size_t>(s) * 4;
+        const int nsup = cdiv(n_, MC_TILE);
+        const size_t msz = static_cast<size_t>(nsup) * static_cast<size_t>(s) * 4;
         DVec Lf(msz), Lb(msz), Ff(msz), Fb(msz);
-        MatChunkArgs g{x_.get(), int(n_), nch, s, P.nt, P.lambda, {P.c[0], P.c[1], P.c[2], P.c[3]},
+        MatChunkArgs g{x_.get(), int(n_), nsup, s, P.nt, P.lambda, {P.c[0], P.c[1], P.c[2], P.c[3]},
                        j < 0 ? nugget_ : 0.0, V, ldv, Y, ldy, Lf.get(), Lb.get(), Ff.get(), Fb.get()};
         static bool attr = false;
         if (!attr) {
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_mat_moments),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM_MOMENTS)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM)));
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_mat_apply),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM_APPLY)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM)));
             attr = true;
         }
-        const dim3 grid(unsigned(cdiv(n_, MC_TILE)), unsigned(cdiv(s, MC_COLS)));
-        k_mat_moments<<<grid, MC_TILE, MC_SMEM_MOMENTS, c.stream>>>(g);
+        const dim3 grid(static_cast<unsigned>(nsup), 1u);
+        k_mat_moments<<<grid, MC_TILE, MC_SMEM, c.stream>>>(g);
         HG_LAUNCH();
         k_mat_carry<<<dim3(unsigned(s), 2), MC_CARRY_THREADS, 0, c.stream>>>(g);
         HG_LAUNCH();
-        k_mat_apply<<<grid, MC_TILE, MC_SMEM_APPLY, c.stream>>>(g);
+        k_mat_apply<<<grid, MC_TILE, MC_SMEM, c.stream>>>(g);
         HG_LAUNCH();
         c.launches += 3;
     }
