@@ -8,7 +8,8 @@ namespace hg {
 
 namespace {
 
-constexpr int QNT = 256;
+constexpr int QNT = 512;   // QR: more warps share each step's column updates
+constexpr int FQNT = 256;  // Q formation
 constexpr int MAXW = 512;
 constexpr size_t QR_SMEM = 200 * 1024;
 
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
     }
 }
 
-__global__ void __launch_bounds__(QNT) k_form_q(const QfDesc* descs, int w, int qcols, int smem_elems) {
+__global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int qcols, int smem_elems) {
     extern __shared__ double sm[];
     const QfDesc d = descs[blockIdx.x];
     const int rows = d.rows;
@@ -267,7 +268,7 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     if (prof_enabled()) prof.key(prof_tag("formq w=%d q=%d blocks=%d rows=%d", w, qcols, int(blocks.size()), max_rows));
     HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
-    k_form_q<<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);
+    k_form_q<<<unsigned(blocks.size()), FQNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);
     HG_LAUNCH();
     ++c.launches;
 }
