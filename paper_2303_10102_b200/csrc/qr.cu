@@ -197,12 +197,15 @@ __global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int
         Q[i + c * ldq] = v;
     }
     __syncthreads();
+    double* Es = sm + smem_elems;  // the current Householder vector, staged (rows doubles)
     for (int k = nref - 1; k >= 0; --k) {
         const double tau = d.tau[k];
         if (rows - k == 1) {
             for (int c = tid; c < qcols; c += blockDim.x) Q[k + c * ldq] *= (1.0 - tau);
         } else if (tau != 0.0) {
-            const double* ess = d.A + k * d.lda;
+            for (int i = k + 1 + tid; i < rows; i += blockDim.x) Es[i] = d.A[i + k * d.lda];
+            __syncthreads();
+            const double* ess = Es;
             for (int c = warp; c < qcols; c += nwarps) {
                 double* qc = Q + c * ldq;
                 double t = 0.0;
@@ -259,6 +262,7 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     size_t smem = static_cast<size_t>(max_rows) * qcols * sizeof(double);
     if (smem > QR_SMEM) smem = QR_SMEM;
     const int smem_elems = int(smem / sizeof(double));
+    smem += static_cast<size_t>(max_rows) * sizeof(double);  // staged Householder vector
     DBuf<QfDesc> dd;
     dd.upload(blocks);
     auto& c = current();
