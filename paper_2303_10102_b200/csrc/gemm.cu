@@ -105,12 +105,20 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
     tile::LoadKCT<TBN> lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
     tile::AccT<BM / 16, TBN / 16> acc;
     acc.zero();
+    // The accumulate-into-Y operand is fetched before the (short-K) main loop
+    // so its latency overlaps the GEMM instead of trailing it.
+    tile::AccT<BM / 16, TBN / 16> yv;
+    yv.zero();
+    if (g.beta != 0.0)
+        tile::for_each_slot<BM, TBN>(yv, [&](double& s, int m, int ni) {
+            const int n = n0 + ni;
+            if (n < g.w && m < it.rows) s = g.Y[i64(it.row0 + m) + i64(n) * g.ldy];
+        });
     tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(g.k, BK), smem, acc);
-    tile::for_each_t<BM, TBN>(acc, [&](int m, int ni, double v) {
+    tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
         const int n = n0 + ni;
         if (n >= g.w || m >= it.rows) return;
-        double* p = g.Y + i64(it.row0 + m) + i64(n) * g.ldy;
-        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + g.beta * y;
     });
 }
 

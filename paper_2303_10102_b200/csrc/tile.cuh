@@ -198,6 +198,36 @@ __device__ __forceinline__ void for_each(const Acc& acc, F&& f) {
     for_each_t<64, 64>(acc, f);
 }
 
+/// Same traversal as for_each_t, exposing the accumulator slot:
+/// f(double& slot, m, n) for every element owned by this thread.
+template <int TBM, int TBN, class F>
+__device__ __forceinline__ void for_each_slot(AccT<TBM / 16, TBN / 16>& a, F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < TBM / 16; ++i)
+#pragma unroll
+        for (int j = 0; j < TBN / 16; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) f(a.v[i][j][e], wm + i * 8 + g, wn + j * 8 + 2 * t + e);
+}
+
+/// Paired traversal of two accumulator sets: f(a_slot, b_slot, m, n).
+template <int TBM, int TBN, class F>
+__device__ __forceinline__ void for_each_slot2(const AccT<TBM / 16, TBN / 16>& a, const AccT<TBM / 16, TBN / 16>& b,
+                                               F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < TBM / 16; ++i)
+#pragma unroll
+        for (int j = 0; j < TBN / 16; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) f(a.v[i][j][e], b.v[i][j][e], wm + i * 8 + g, wn + j * 8 + 2 * t + e);
+}
+
 /// Tile extent (16..96, multiple of 16) for a problem extent x: the smallest
 /// single tile that covers x up to 96; beyond, 64 or 80, whichever pads less
 /// (96-wide tiles over many column blocks cost occupancy: 48 accumulators).
