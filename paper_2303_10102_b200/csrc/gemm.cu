@@ -150,6 +150,13 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
     tile::AccT<BM / 16, TBN / 16> acc;
     acc.zero();
+    tile::AccT<BM / 16, TBN / 16> yv;
+    yv.zero();
+    if (g.beta != 0.0)  // fetch the accumulated Y before the main loop (latency overlap)
+        tile::for_each_slot<BM, TBN>(yv, [&](double& y, int mi0, int ni) {
+            const int mi = r0 + mi0, n = n0 + ni;
+            if (n < g.w && mi < m) y = g.Y[i64(lo + mi) + i64(n) * g.ldy];
+        });
     if (!TRANS) {
         tile::LoadMCT<BM> la{Lb + r0, g.ldl, m - r0, m};
         tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
@@ -157,23 +164,22 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
         tile::LoadKCT<BM> la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
         tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
     }
-    tile::for_each_t<BM, TBN>(acc, [&](int mi0, int ni, double v) {
+    tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int mi0, int ni) {
         const int mi = r0 + mi0, n = n0 + ni;
         if (n >= g.w || mi >= m) return;
-        double* p = g.Y + i64(lo + mi) + i64(n) * g.ldy;
-        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        g.Y[i64(lo + mi) + i64(n) * g.ldy] = g.alpha * v + g.beta * y;
     });
 }
 
 // ------------------------------------------------------------ elementwise
+/// Y = alpha X + beta Y; grid (row blocks, column groups), no 64-bit div/mod.
 __global__ void k_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
-    const i64 total = n * w;
-    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
-        const i64 i = e % n, j = e / n;
-        double* y = Y + i + j * ldy;
-        const double x = X ? alpha * X[i + j * ldx] : 0.0;
-        *y = x + (beta != 0.0 ? beta * *y : 0.0);
-    }
+    for (int j = blockIdx.y; j < w; j += gridDim.y)
+        for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+            double* y = Y + i + j * ldy;
+            const double x = X ? alpha * X[i + j * ldx] : 0.0;
+            *y = x + (beta != 0.0 ? beta * *y : 0.0);
+        }
 }
 
 __global__ void k_parity_scale(const WorkItem* items, int w, const double* X, i64 ldx, double ae, double ao,
@@ -201,6 +207,21 @@ __device__ double block_sum(double v) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;  // valid in thread 0
+}
+
+/// Partial sums of sum(A .* B) over n x w: block b owns a fixed row range for
+/// every column (deterministic), one partial per block.
+__global__ void k_dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* partial) {
+    const i64 per = (n + gridDim.x - 1) / gridDim.x;
+    const i64 r0 = i64(blockIdx.x) * per, r1 = min(n, r0 + per);
+    double v = 0.0;
+    for (int j = 0; j < w; ++j) {
+        const double* a = A + j * lda;
+        const double* b = B + j * ldb;
+        for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) v = fma(a[i], b[i], v);
+    }
+    v = block_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
 }
 
 struct DotPanels {
@@ -387,9 +408,9 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
 void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
     if (n <= 0 || w <= 0) return;
     auto& c = current();
-    const i64 total = n * w;
-    const int blocks = int(std::min<i64>((total + 255) / 256, 148 * 16));
-    k_axpby<<<blocks, 256, 0, c.stream>>>(n, w, alpha, X, ldx, beta, Y, ldy);
+    const int bx = int(std::min<i64>((n + 255) / 256, 148 * 8));
+    const int by = std::min(w, std::max(1, (148 * 16) / bx));
+    k_axpby<<<dim3(unsigned(bx), unsigned(by)), 256, 0, c.stream>>>(n, w, alpha, X, ldx, beta, Y, ldy);
     HG_LAUNCH();
     ++c.launches;
 }
@@ -406,7 +427,17 @@ void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 l
 }
 
 void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate) {
-    reduce(DotPanels{n, A, B, lda, ldb}, n * i64(w), out, accumulate);
+    if (n <= 0 || w <= 0) {
+        if (!accumulate) HG_CUDA(cudaMemsetAsync(out, 0, sizeof(double), current().stream));
+        return;
+    }
+    auto& c = current();
+    DVec partial(RED_BLOCKS);
+    k_dot_panels<<<RED_BLOCKS, 256, 0, c.stream>>>(n, w, A, lda, B, ldb, partial.get());
+    HG_LAUNCH();
+    k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), RED_BLOCKS, out, accumulate ? 1 : 0);
+    HG_LAUNCH();
+    c.launches += 2;
 }
 
 void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,

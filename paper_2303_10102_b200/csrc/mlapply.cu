@@ -161,14 +161,19 @@ __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
     const int n0 = blockIdx.y * TBN;
     LoadUpdA la{&L, it.row0, it.rows, g.n};
     LoadUpdB<TBN> lb{&L, it.seg, g.tau, g.s, n0};
-    tile::AccT<BM / 16, TBN / 16> acc;
+    tile::AccT<BM / 16, TBN / 16> acc, yv;
     acc.zero();
+    yv.zero();
+    if (g.beta != 0.0)  // fetch the accumulated Y before the main loop (latency overlap)
+        tile::for_each_slot<BM, TBN>(yv, [&](double& y, int m, int ni) {
+            const int c = n0 + ni;
+            if (c < g.s && m < it.rows) y = g.Y[i64(it.row0 + m) + i64(c) * g.ldy];
+        });
     tile::run_t<2, BM, TBN>(la, lb, L.ktoff[L.nl], smem, acc);
-    tile::for_each_t<BM, TBN>(acc, [&](int m, int ni, double v) {
+    tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
         const int c = n0 + ni;
         if (c >= g.s || m >= it.rows) return;
-        double* p = g.Y + i64(it.row0 + m) + i64(c) * g.ldy;
-        *p = g.alpha * v + (g.beta != 0.0 ? g.beta * *p : 0.0);
+        g.Y[i64(it.row0 + m) + i64(c) * g.ldy] = g.alpha * v + g.beta * y;
     });
 }
 
