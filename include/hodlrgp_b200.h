@@ -134,6 +134,20 @@ hg_status hg_oracle_dense(hg_ctx_t ctx, int64_t n, const double* K, int p, const
 hg_status hg_oracle_matern(hg_ctx_t ctx, int64_t n, const double* x, int nu2, double sigma2, double ell,
                            double nugget, int scan, hg_oracle_t* out);
 hg_status hg_oracle_callback(hg_ctx_t ctx, int64_t n, int p, hg_apply_fn fn, void* user, hg_oracle_t* out);
+/* Forward-model oracles of BASELINE.json configs 2, 3, 5 (the
+ * reference's own models are FEM and out of scope). theta = (sigma2, ell, kappa).
+ * hg_oracle_cokriging: joint [u; f] of -u'' + kappa^2 u = f (FD, Dirichlet) on
+ *   m interior points of [0,1], f Matérn nu = 1/2; n = 2m, rows interleaved
+ *   (2i = u_i, 2i+1 = f_i); nugget added on the diagonal (FP64 needs one: the
+ *   joint covariance's condition number exceeds 1e15 without).
+ * hg_oracle_spde2d: u = (-Lap_h + kappa^2)^-1 f on the nside x nside periodic
+ *   grid, f Matérn nu = 3/2 (spectral), plus a fixed nugget (u alone is
+ *   singular in FP64); n = nside^2; order[i] = grid index iy*nside + ix of
+ *   row i (NULL = natural order), e.g. a KD ordering. */
+hg_status hg_oracle_cokriging(hg_ctx_t ctx, int64_t m, double sigma2, double ell, double kappa, double nugget,
+                              hg_oracle_t* out);
+hg_status hg_oracle_spde2d(hg_ctx_t ctx, int nside, double sigma2, double ell, double kappa, double nugget,
+                           const int64_t* order, hg_oracle_t* out);
 hg_status hg_oracle_set_parameters(hg_oracle_t o, const double* theta, int p);
 hg_status hg_oracle_free(hg_oracle_t o);
 /* apply (j = -1) / apply_derivative (j >= 0) — oracle.hpp:25-35 */

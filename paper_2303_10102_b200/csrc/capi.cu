@@ -403,6 +403,16 @@ hg_status hg_oracle_matern(hg_ctx_t ctx, int64_t n, const double* x, int nu2, do
     return guard(ctx, [&] { *out = new hg_oracle_s{make_matern_oracle(n, x, nu2, sigma2, ell, nugget, scan != 0)}; });
 }
 
+hg_status hg_oracle_cokriging(hg_ctx_t ctx, int64_t m, double sigma2, double ell, double kappa, double nugget,
+                              hg_oracle_t* out) {
+    return guard(ctx, [&] { *out = new hg_oracle_s{make_cokriging_oracle(m, sigma2, ell, kappa, nugget)}; });
+}
+
+hg_status hg_oracle_spde2d(hg_ctx_t ctx, int nside, double sigma2, double ell, double kappa, double nugget,
+                           const int64_t* order, hg_oracle_t* out) {
+    return guard(ctx, [&] { *out = new hg_oracle_s{make_spde2d_oracle(nside, sigma2, ell, kappa, nugget, order)}; });
+}
+
 hg_status hg_oracle_callback(hg_ctx_t ctx, int64_t n, int p, hg_apply_fn fn, void* user, hg_oracle_t* out) {
     return guard(ctx, [&] { *out = new hg_oracle_s{make_callback_oracle(n, p, reinterpret_cast<ApplyFn>(fn), user)}; });
 }

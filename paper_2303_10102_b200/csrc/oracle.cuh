@@ -48,6 +48,16 @@ std::unique_ptr<DOracle> make_dense_oracle(i64 n, const double* K, int p, const 
 std::unique_ptr<DOracle> make_matern_oracle(i64 n, const double* x, int nu2, double sigma2, double ell,
                                             double nugget, bool scan);
 
+/// BASELINE.json C2: joint [u; f] co-kriging covariance (models.cu), n = 2m,
+/// theta = (sigma2, ell, kappa), fixed nugget on the diagonal.
+std::unique_ptr<DOracle> make_cokriging_oracle(i64 m, double sigma2, double ell, double kappa, double nugget);
+
+/// BASELINE.json C3/C5: covariance of u = (-Lap_h + kappa^2)^-1 f on the N x N
+/// periodic grid (models.cu), n = N^2, theta = (sigma2, ell, kappa); row i of
+/// every panel is grid point order[i] (null = natural order).
+std::unique_ptr<DOracle> make_spde2d_oracle(int N, double sigma2, double ell, double kappa, double nugget,
+                                            const std::int64_t* order);
+
 using ApplyFn = int (*)(void* user, int j, const double* V, std::int64_t ldv, std::int64_t s, double* Y,
                         std::int64_t ldy, void* stream);
 std::unique_ptr<DOracle> make_callback_oracle(i64 n, int p, ApplyFn fn, void* user);
