@@ -16,8 +16,10 @@
 //   dK/dkappa: a = A^-1 V_u, b = A^-1 a, z1 = Kf (a + V_f), z2 = Kf b,
 //              Y_u = -2 kappa A^-1 (A^-1 z1 + z2), Y_f = -2 kappa z2
 //   (dA/dkappa = 2 kappa I). A^-1 by the Thomas algorithm with factors
-//   precomputed once per kappa (one thread per column, 64-row tiles staged
-//   through shared memory).
+//   precomputed once per kappa; both sweeps are first-order linear
+//   recurrences evaluated as parallel affine scans on the column resident in
+//   shared memory (one CTA per column), with a serial fallback for columns
+//   longer than shared memory.
 //
 // C3/C5 SPDE (2D): u solves (-Lap_h + kappa^2) u = f on the N x N periodic
 // grid of the unit square (5-point stencil, h = 1/N), f a stationary
@@ -59,11 +61,13 @@ constexpr int TH_R = 64;
 
 /// X = A^-1 D, A = tridiag(a, b, a): d'_0 = d_0 im_0, d'_i = (d_i - a d'_{i-1}) im_i,
 /// x_{n-1} = d'_{n-1}, x_i = d'_i - cp_i x_{i+1} (im_i = 1/m_i, cp_i = a im_i).
-/// One thread per column; 64-row tiles staged through shared memory so the
-/// global traffic stays coalesced. D and X may alias.
+/// One thread per column; 64-row tiles of the panel and of the factors are
+/// staged through shared memory (coalesced global traffic, and the serial
+/// recurrence only touches shared memory). D and X may alias.
 __global__ void __launch_bounds__(32) k_thomas(int n, int s, double a, const double* cp, const double* im,
                                                const double* D, i64 ldd, double* X, i64 ldx) {
     __shared__ double tile[TH_R][33];
+    __shared__ double fac[TH_R];
     const int c0 = blockIdx.x * 32, lane = threadIdx.x;
     double prev = 0.0;
     for (int r0 = 0; r0 < n; r0 += TH_R) {
@@ -72,11 +76,11 @@ __global__ void __launch_bounds__(32) k_thomas(int n, int s, double a, const dou
             const int cl = c0 + cc;
             for (int r = lane; r < rows; r += 32) tile[r][cc] = cl < s ? D[i64(r0 + r) + i64(cl) * ldd] : 0.0;
         }
+        for (int r = lane; r < rows; r += 32) fac[r] = im[r0 + r];
         __syncwarp();
         for (int r = 0; r < rows; ++r) {
-            const int i = r0 + r;
             const double d = tile[r][lane];
-            prev = (i == 0 ? d : d - a * prev) * im[i];
+            prev = (r0 + r == 0 ? d : d - a * prev) * fac[r];
             tile[r][lane] = prev;
         }
         __syncwarp();
@@ -94,10 +98,10 @@ __global__ void __launch_bounds__(32) k_thomas(int n, int s, double a, const dou
             const int cl = c0 + cc;
             for (int r = lane; r < rows; r += 32) tile[r][cc] = cl < s ? X[i64(r0 + r) + i64(cl) * ldx] : 0.0;
         }
+        for (int r = lane; r < rows; r += 32) fac[r] = cp[r0 + r];
         __syncwarp();
         for (int r = rows - 1; r >= 0; --r) {
-            const int i = r0 + r;
-            const double x = i == n - 1 ? tile[r][lane] : tile[r][lane] - cp[i] * next;
+            const double x = r0 + r == n - 1 ? tile[r][lane] : tile[r][lane] - fac[r] * next;
             tile[r][lane] = x;
             next = x;
         }
@@ -109,6 +113,84 @@ __global__ void __launch_bounds__(32) k_thomas(int n, int s, double a, const dou
         }
         __syncwarp();
     }
+}
+
+/// Thomas solve with the column resident in shared memory and both sweeps as
+/// parallel scans: the forward sweep y_i = alpha_i y_{i-1} + im_i d_i
+/// (alpha_i = -a im_i) and the backward sweep x_i = d'_i - cp_i x_{i+1} are
+/// first-order linear recurrences, so each of 256 threads reduces its run of
+/// rows to an affine map (A, B), the maps are combined by a Kogge-Stone scan,
+/// and every run is replayed from its carry-in. One CTA per column.
+constexpr int TS_THR = 256;
+
+__device__ __forceinline__ void affine_scan(double& A, double& B, double* sA, double* sB, bool reverse) {
+    const int t = threadIdx.x;
+    const int me = reverse ? TS_THR - 1 - t : t;  // position in scan order
+    sA[me] = A;
+    sB[me] = B;
+    __syncthreads();
+    for (int off = 1; off < TS_THR; off <<= 1) {
+        double a1 = 1.0, b1 = 0.0;
+        const bool take = me >= off;
+        if (take) {
+            a1 = sA[me - off];
+            b1 = sB[me - off];
+        }
+        __syncthreads();
+        if (take) {  // (A, B) o (a1, b1): x -> A (a1 x + b1) + B
+            sB[me] = A * b1 + B;
+            sA[me] = A * a1;
+            A = sA[me];
+            B = sB[me];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(TS_THR) k_thomas_col(int n, double a, const double* cp, const double* im,
+                                                       const double* D, i64 ldd, double* X, i64 ldx) {
+    extern __shared__ double col[];  // n
+    __shared__ double sA[TS_THR], sB[TS_THR];
+    const int c = blockIdx.x, t = threadIdx.x;
+    const double* d = D + i64(c) * ldd;
+    double* x = X + i64(c) * ldx;
+    for (int i = t; i < n; i += TS_THR) col[i] = d[i];
+    __syncthreads();
+    const int per = (n + TS_THR - 1) / TS_THR;
+    const int r0 = min(n, t * per), r1 = min(n, r0 + per);
+    // forward: y_i = (d_i - a y_{i-1}) im_i
+    double A = 1.0, B = 0.0;
+    for (int i = r0; i < r1; ++i) {
+        const double al = i == 0 ? 0.0 : -a * im[i];
+        A *= al;
+        B = al * B + im[i] * col[i];
+    }
+    affine_scan(A, B, sA, sB, false);
+    double y = t == 0 ? 0.0 : sB[t - 1];  // carry-in: state after the previous run
+    __syncthreads();
+    for (int i = r0; i < r1; ++i) {
+        y = (i == 0 ? col[i] : col[i] - a * y) * im[i];
+        col[i] = y;
+    }
+    __syncthreads();
+    // backward: x_i = d'_i - cp_i x_{i+1}, runs in reverse order
+    A = 1.0;
+    B = 0.0;
+    for (int i = r1 - 1; i >= r0; --i) {
+        const double al = i == n - 1 ? 0.0 : -cp[i];
+        A *= al;
+        B = al * B + col[i];
+    }
+    affine_scan(A, B, sA, sB, true);
+    const int me = TS_THR - 1 - t;
+    double xn = me == 0 ? 0.0 : sB[me - 1];
+    __syncthreads();
+    for (int i = r1 - 1; i >= r0; --i) {
+        xn = i == n - 1 ? col[i] : col[i] - cp[i] * xn;
+        col[i] = xn;
+    }
+    __syncthreads();
+    for (int i = t; i < n; i += TS_THR) x[i] = col[i];
 }
 
 /// Rows 2i (u) and 2i+1 (f) of an interleaved panel <-> two m-row panels.
@@ -208,7 +290,18 @@ private:
     }
     void solve(const double* D, double* X, int s) const {
         auto& c = current();
-        k_thomas<<<unsigned(cdiv(s, 32)), 32, 0, c.stream>>>(int(m_), s, a_, cp_.get(), im_.get(), D, m_, X, m_);
+        const size_t smem = static_cast<size_t>(m_) * sizeof(double);
+        if (smem <= 200 * 1024) {  // column resident: parallel-scan sweeps, one CTA per column
+            static bool attr = false;
+            if (!attr) {
+                HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_thomas_col),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr = true;
+            }
+            k_thomas_col<<<unsigned(s), TS_THR, smem, c.stream>>>(int(m_), a_, cp_.get(), im_.get(), D, m_, X, m_);
+        } else {
+            k_thomas<<<unsigned(cdiv(s, 32)), 32, 0, c.stream>>>(int(m_), s, a_, cp_.get(), im_.get(), D, m_, X, m_);
+        }
         HG_LAUNCH();
         ++c.launches;
     }
