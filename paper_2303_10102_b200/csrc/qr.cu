@@ -3,6 +3,7 @@
 
 #include "prof.cuh"
 #include "qr.cuh"
+#include "tile.cuh"
 
 namespace hg {
 
@@ -225,6 +226,8 @@ __global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int
         }
 }
 
+#include "qr_blocked.cuh"
+
 }  // namespace
 
 void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
@@ -242,7 +245,13 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_QR, 2.0 * rows * w * w, 16.0 * rows * w);
     if (prof_enabled()) prof.key(prof_tag("qr%d w=%d blocks=%d rows=%d", int(pivot), w, int(blocks.size()), max_rows));
-    if (pivot) {
+    if (!pivot && smem_elems < max_rows * w && max_rows <= QB_MAXROWS) {
+        // wide blocks that do not fit shared memory: blocked compact-WY QR
+        const size_t sb = qb_smem(max_rows, w);
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_blocked),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
+        k_qr_blocked<<<unsigned(blocks.size()), QB_THREADS, sb, c.stream>>>(dd.get(), w);
+    } else if (pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<true>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         k_qr<true><<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, smem_elems);
@@ -270,9 +279,16 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_FORM_Q, 4.0 * rows * w * qcols, 8.0 * rows * (w + 2.0 * qcols));
     if (prof_enabled()) prof.key(prof_tag("formq w=%d q=%d blocks=%d rows=%d", w, qcols, int(blocks.size()), max_rows));
-    HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    k_form_q<<<unsigned(blocks.size()), FQNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);
+    if (smem_elems < max_rows * qcols && max_rows <= QB_MAXROWS) {
+        const size_t sb = qb_smem(max_rows, qcols);
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q_blocked),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
+        k_form_q_blocked<<<unsigned(blocks.size()), QB_THREADS, sb, c.stream>>>(dd.get(), w, qcols);
+    } else {
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_form_q<<<unsigned(blocks.size()), FQNT, smem, c.stream>>>(dd.get(), w, qcols, smem_elems);
+    }
     HG_LAUNCH();
     ++c.launches;
 }

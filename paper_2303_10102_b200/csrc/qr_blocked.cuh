@@ -1,0 +1,278 @@
+// Blocked (compact-WY) Householder QR and Q formation for wide blocks
+// (included by qr.cu inside its anonymous namespace, after qr_block_sum /
+// warp_sum and the QrDesc / QfDesc types).
+//
+// The SMEM-resident column-at-a-time kernels (k_qr, k_form_q) stop fitting
+// once rows x w exceeds shared memory (w >~ 150 at the TSQR chunk height 4w),
+// and then ran every Householder step out of global memory. Here a block is
+// processed in panels of 16 columns (LAPACK xGEQRF structure):
+//   1. the panel (rows x 16) is factored column by column in shared memory;
+//   2. T (16 x 16, upper) of the compact WY form H_p ... H_{p+15} = I - V T V^T
+//      is built from G = V^T V (xLARFT, forward, columnwise);
+//   3. the trailing columns get C <- (I - V T^T V^T) C as two DMMA GEMMs
+//      (W = V^T C, then C -= V (T^T W)), C staying in global memory (L2).
+// Same Householder vectors, taus and R as the unblocked kernel in exact
+// arithmetic; only the association of the trailing-update sums differs.
+// Q formation applies the panels right to left: Q <- Q - V (T (V^T Q)).
+
+constexpr int QB_NB = 16;
+constexpr int QB_THREADS = 256;
+constexpr int QB_MAXROWS = 1400;  // panel (rows x 16) in shared memory
+
+__host__ __device__ __forceinline__ int qb_ld(int rows) { return ((rows + 11) / 16) * 16 + 4; }  // 4 mod 16
+__host__ __device__ __forceinline__ size_t qb_smem(int rows, int wmax) {
+    return (static_cast<size_t>(qb_ld(rows)) * QB_NB + 2 * QB_NB * static_cast<size_t>(wmax) + 2 * QB_NB * QB_NB +
+            QB_NB) *
+           sizeof(double);
+}
+
+struct QbSmem {
+    double* P;   // ld x 16 panel, then explicit V
+    double* W1;  // 16 x wmax (a + 16 j)
+    double* W2;  // 16 x wmax
+    double* T;   // 16 x 16 (a + 16 i)
+    double* G;   // 16 x 16
+    double* tau; // 16
+};
+
+__device__ __forceinline__ QbSmem qb_layout(double* sm, int rows, int wmax) {
+    QbSmem s;
+    s.P = sm;
+    s.W1 = s.P + size_t(qb_ld(rows)) * QB_NB;
+    s.W2 = s.W1 + size_t(QB_NB) * wmax;
+    s.T = s.W2 + size_t(QB_NB) * wmax;
+    s.G = s.T + QB_NB * QB_NB;
+    s.tau = s.G + QB_NB * QB_NB;
+    return s;
+}
+
+/// P (nr x jb panel, ld) -> explicit V: zeros above the diagonal, unit
+/// diagonal, zero columns past jb and zero rows past nr (to the padded ld).
+__device__ __forceinline__ void qb_explicit_v(double* P, int ld, int nr, int jb) {
+    for (int e = threadIdx.x; e < ld * QB_NB; e += blockDim.x) {
+        const int r = e % ld, i = e / ld;
+        if (i >= jb || r >= nr || r < i)
+            P[r + i * ld] = 0.0;
+        else if (r == i)
+            P[r + i * ld] = 1.0;
+    }
+}
+
+/// G = V^T V (upper part), then T by xLARFT (forward, columnwise).
+__device__ __forceinline__ void qb_build_t(const QbSmem& S, int ld, int nr, int jb) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int pr = warp; pr < QB_NB * QB_NB; pr += nwarps) {
+        const int a = pr % QB_NB, b = pr / QB_NB;
+        if (a > b) continue;
+        double s = 0.0;
+        if (b < jb)
+            for (int r = lane; r < nr; r += 32) s += S.P[r + a * ld] * S.P[r + b * ld];
+        s = warp_sum(s);
+        if (lane == 0) S.G[a + QB_NB * b] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < QB_NB * QB_NB; ++i) S.T[i] = 0.0;
+        for (int i = 0; i < jb; ++i) {
+            const double ti = S.tau[i];
+            S.T[i + QB_NB * i] = ti;
+            for (int a = 0; a < i; ++a) {
+                double s = 0.0;
+                for (int b = a; b < i; ++b) s += S.T[a + QB_NB * b] * S.G[b + QB_NB * i];
+                S.T[a + QB_NB * i] = -ti * s;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+/// W1 = V^T C (16 x wc) with V the explicit panel (nr rows) and C = Cg[0:nr, 0:wc]
+/// (global, ldc); DMMA over 8x8 tiles, K split in two chains.
+__device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const double* Cg, i64 ldc, int wc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int nct = (wc + 7) / 8, ntiles = 2 * nct;
+    const int K = (nr + 3) & ~3;
+    for (int tl = warp; tl < ntiles; tl += nwarps) {
+        const int a0 = (tl & 1) * 8, j0 = (tl >> 1) * 8;
+        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+        const bool colok = j0 + g8 < wc;
+        const double* Bc = Cg + i64(j0 + g8) * ldc;
+        int k4 = 0;
+        for (; k4 + 8 <= K; k4 += 8) {
+            const int r0 = k4 + t4, r1 = k4 + 4 + t4;
+            const double b0 = (colok && r0 < nr) ? Bc[r0] : 0.0;
+            const double b1 = (colok && r1 < nr) ? Bc[r1] : 0.0;
+            tile::dmma(c0, S.P[r0 + (a0 + g8) * ld], b0);
+            tile::dmma(c1, S.P[r1 + (a0 + g8) * ld], b1);
+        }
+        if (k4 < K) {
+            const int r0 = k4 + t4;
+            const double b0 = (colok && r0 < nr) ? Bc[r0] : 0.0;
+            tile::dmma(c0, S.P[r0 + (a0 + g8) * ld], b0);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = j0 + 2 * t4 + e;
+            if (j < wc) S.W1[(a0 + g8) + QB_NB * j] = c0[e] + c1[e];
+        }
+    }
+}
+
+/// Cg[0:nr, 0:wc] -= V W2 (W2 16 x wc in shared memory).
+__device__ __forceinline__ void qb_c_minus_vw(const QbSmem& S, int ld, int nr, double* Cg, i64 ldc, int wc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int nrt = (nr + 7) / 8, nct = (wc + 7) / 8;
+    for (int tl = warp; tl < nrt * nct; tl += nwarps) {
+        const int r0 = (tl % nrt) * 8, j0 = (tl / nrt) * 8;
+        const int r = r0 + g8;
+        double acc[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = j0 + 2 * t4 + e;
+            acc[e] = (r < nr && j < wc) ? Cg[r + i64(j) * ldc] : 0.0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < QB_NB; kk += 4) {
+            const int jb = j0 + g8;
+            const double b = jb < wc ? S.W2[(kk + t4) + QB_NB * jb] : 0.0;
+            tile::dmma(acc, -S.P[r0 + g8 + (kk + t4) * ld], b);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = j0 + 2 * t4 + e;
+            if (r < nr && j < wc) Cg[r + i64(j) * ldc] = acc[e];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(QB_THREADS) k_qr_blocked(const QrDesc* descs, int w) {
+    extern __shared__ double sm[];
+    __shared__ double s_tau, s_div;
+    __shared__ int s_zero;
+    const QrDesc d = descs[blockIdx.x];
+    const int rows = d.rows, ld = qb_ld(rows);
+    const QbSmem S = qb_layout(sm, rows, w);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int nsz = min(rows, w);
+    double* A = d.A;
+    for (int p0 = 0; p0 < nsz; p0 += QB_NB) {
+        const int jb = min(QB_NB, nsz - p0), nr = rows - p0;
+        // 1. panel into shared memory and its level-2 factorization
+        for (int e = tid; e < nr * jb; e += blockDim.x) {
+            const int r = e % nr, i = e / nr;
+            S.P[r + i * ld] = A[(p0 + r) + i64(p0 + i) * d.lda];
+        }
+        __syncthreads();
+        for (int i = 0; i < jb; ++i) {
+            double part = 0.0;
+            for (int r = i + 1 + tid; r < nr; r += blockDim.x) part += S.P[r + i * ld] * S.P[r + i * ld];
+            const double tail = qr_block_sum(part);
+            if (tid == 0) {
+                const double c0 = S.P[i + i * ld];
+                if (tail <= DBL_MIN) {
+                    s_tau = 0.0;
+                    s_zero = 1;
+                    s_div = 1.0;
+                } else {
+                    double beta = sqrt(c0 * c0 + tail);
+                    if (c0 >= 0.0) beta = -beta;
+                    s_div = c0 - beta;
+                    s_tau = (beta - c0) / beta;
+                    s_zero = 0;
+                    S.P[i + i * ld] = beta;
+                }
+                d.tau[p0 + i] = s_tau;
+                S.tau[i] = s_tau;
+            }
+            __syncthreads();
+            const double tau = s_tau;
+            for (int r = i + 1 + tid; r < nr; r += blockDim.x) S.P[r + i * ld] = s_zero ? 0.0 : S.P[r + i * ld] / s_div;
+            __syncthreads();
+            for (int j = i + 1 + warp; j < jb; j += nwarps) {
+                double* cj = S.P + j * ld;
+                if (nr - i == 1) {
+                    if (lane == 0) cj[i] *= (1.0 - tau);
+                } else if (tau != 0.0) {
+                    double t = 0.0;
+                    for (int r = i + 1 + lane; r < nr; r += 32) t += S.P[r + i * ld] * cj[r];
+                    t = warp_sum(t) + cj[i];
+                    for (int r = i + 1 + lane; r < nr; r += 32) cj[r] -= tau * S.P[r + i * ld] * t;
+                    __syncwarp();
+                    if (lane == 0) cj[i] -= tau * t;
+                }
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < nr * jb; e += blockDim.x) {
+            const int r = e % nr, i = e / nr;
+            A[(p0 + r) + i64(p0 + i) * d.lda] = S.P[r + i * ld];
+        }
+        __syncthreads();
+        const int wc = w - p0 - jb;
+        if (wc <= 0) continue;
+        // 2. explicit V and T
+        qb_explicit_v(S.P, ld, nr, jb);
+        __syncthreads();
+        qb_build_t(S, ld, nr, jb);
+        // 3. C <- C - V (T^T (V^T C))
+        double* C = A + p0 + i64(p0 + jb) * d.lda;
+        qb_vt_c(S, ld, nr, C, d.lda, wc);
+        __syncthreads();
+        for (int e = tid; e < QB_NB * wc; e += blockDim.x) {
+            const int i = e % QB_NB, j = e / QB_NB;
+            double s = 0.0;
+            for (int a = 0; a <= i; ++a) s += S.T[a + QB_NB * i] * S.W1[a + QB_NB * j];
+            S.W2[i + QB_NB * j] = s;
+        }
+        __syncthreads();
+        qb_c_minus_vw(S, ld, nr, C, d.lda, wc);
+        __syncthreads();
+    }
+    if (d.R)
+        for (int e = tid; e < w * w; e += blockDim.x) {
+            const int i = e % w, j = e / w;
+            d.R[i + j * d.ldr] = (i <= j && i < nsz) ? A[i + i64(j) * d.lda] : 0.0;
+        }
+}
+
+__global__ void __launch_bounds__(QB_THREADS) k_form_q_blocked(const QfDesc* descs, int w, int qcols) {
+    extern __shared__ double sm[];
+    const QfDesc d = descs[blockIdx.x];
+    const int rows = d.rows, ld = qb_ld(rows);
+    const QbSmem S = qb_layout(sm, rows, qcols);
+    const int tid = threadIdx.x;
+    const int nref = min(w, rows);
+    for (i64 e = tid; e < i64(rows) * qcols; e += blockDim.x) {
+        const int i = int(e % rows), c = int(e / rows);
+        double v = 0.0;
+        if (i < nref) v = d.Tin ? d.Tin[i + i64(c) * d.ldt] : (i == c ? 1.0 : 0.0);
+        d.Q[i + c * d.ldq] = v;
+    }
+    __syncthreads();
+    for (int p0 = ((nref - 1) / QB_NB) * QB_NB; p0 >= 0; p0 -= QB_NB) {
+        const int jb = min(QB_NB, nref - p0), nr = rows - p0;
+        for (int e = tid; e < nr * jb; e += blockDim.x) {
+            const int r = e % nr, i = e / nr;
+            S.P[r + i * ld] = d.A[(p0 + r) + i64(p0 + i) * d.lda];
+        }
+        if (tid < QB_NB) S.tau[tid] = tid < jb ? d.tau[p0 + tid] : 0.0;
+        __syncthreads();
+        qb_explicit_v(S.P, ld, nr, jb);
+        __syncthreads();
+        qb_build_t(S, ld, nr, jb);
+        double* Qp = d.Q + p0;
+        qb_vt_c(S, ld, nr, Qp, d.ldq, qcols);
+        __syncthreads();
+        for (int e = tid; e < QB_NB * qcols; e += blockDim.x) {  // W2 = T W1
+            const int i = e % QB_NB, j = e / QB_NB;
+            double s = 0.0;
+            for (int a = i; a < QB_NB; ++a) s += S.T[i + QB_NB * a] * S.W1[a + QB_NB * j];
+            S.W2[i + QB_NB * j] = s;
+        }
+        __syncthreads();
+        qb_c_minus_vw(S, ld, nr, Qp, d.ldq, qcols);
+        __syncthreads();
+    }
+}
