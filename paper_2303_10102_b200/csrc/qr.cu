@@ -245,7 +245,7 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_QR, 2.0 * rows * w * w, 16.0 * rows * w);
     if (prof_enabled()) prof.key(prof_tag("qr%d w=%d blocks=%d rows=%d", int(pivot), w, int(blocks.size()), max_rows));
-    if (!pivot && smem_elems < max_rows * w && max_rows <= QB_MAXROWS) {
+    if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS) {
         // wide blocks that do not fit shared memory: blocked compact-WY QR
         const size_t sb = qb_smem(max_rows, w);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_blocked),
@@ -279,7 +279,7 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_FORM_Q, 4.0 * rows * w * qcols, 8.0 * rows * (w + 2.0 * qcols));
     if (prof_enabled()) prof.key(prof_tag("formq w=%d q=%d blocks=%d rows=%d", w, qcols, int(blocks.size()), max_rows));
-    if (smem_elems < max_rows * qcols && max_rows <= QB_MAXROWS) {
+    if ((smem_elems < max_rows * qcols || qcols >= 16) && max_rows <= QB_MAXROWS) {
         const size_t sb = qb_smem(max_rows, qcols);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q_blocked),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
