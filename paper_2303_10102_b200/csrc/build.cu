@@ -630,10 +630,18 @@ void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double*
 }
 
 /// Y = K X - H X with H restricted to levels < l (peeling), full n x s panels.
-void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y) {
+/// zparity: X is zero on the level-(lmax+1) children of that parity (0: the
+/// sketch R_l lives on right children, 1: the bases S, ds, S2 on left ones);
+/// -1: no structure (leaf sampler).
+void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y, int zparity) {
     const i64 n = H.n();
     o.apply(j, X, n, s, Y, n);
-    hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0);
+    ZeroRows z;
+    if (zparity >= 0 && lmax + 1 <= H.tau()) {
+        const Partition& pz = H.tree->part(lmax + 1);
+        z = ZeroRows{pz.dbounds(), pz.nseg(), zparity};
+    }
+    hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
 }
 
 }  // namespace
@@ -715,8 +723,8 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         const double* Rs = plan.level[static_cast<size_t>(l - 1)]->get();
         // Pass 1: Y = K R - H R, dY_j = K_j R - D_j R (sketch.cpp:151-154).
         DVec Y(static_cast<size_t>(n) * k), dY(static_cast<size_t>(n) * std::max(kp, 1));
-        peel(o, -1, out.h, l - 1, Rs, k, Y.get());
-        for (int q = 0; q < p; ++q) peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, Rs, k, dY.get() + i64(q) * k * n);
+        peel(o, -1, out.h, l - 1, Rs, k, Y.get(), 0);
+        for (int q = 0; q < p; ++q) peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, Rs, k, dY.get() + i64(q) * k * n, 0);
         // Range finder per node (sketch.cpp:156-175).
         std::vector<int> qmap(static_cast<size_t>(nodes), -1);
         std::vector<BatchedQR::Block> blocks;
@@ -760,7 +768,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         }
         // Pass 2: Z = K S - H S (sketch.cpp:177-183).
         DVec Z(static_cast<size_t>(n) * k);
-        peel(o, -1, out.h, l - 1, S.get(), k, Z.get());
+        peel(o, -1, out.h, l - 1, S.get(), k, Z.get(), 1);
 
         // q2 residual bases (sketch.cpp:194-233).
         std::vector<int> w2(static_cast<size_t>(nodes), 0);
@@ -833,13 +841,13 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             seg_nn(pc, S.get(), n, k, Om.get(), i64(k) * k, k, TMap::parent(0, 0), ds.get(), n, k, 1.0, 0.0);
             // dZ = K_q S - D_q S + K ds - H ds
             DVec dZ(static_cast<size_t>(n) * k), tmp(static_cast<size_t>(n) * k);
-            peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S.get(), k, dZ.get());
-            peel(o, -1, out.h, l - 1, ds.get(), k, tmp.get());
+            peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S.get(), k, dZ.get(), 1);
+            peel(o, -1, out.h, l - 1, ds.get(), k, tmp.get(), 1);
             panel_axpby(n, k, 1.0, tmp.get(), n, 1.0, dZ.get(), n);
             DVec dZ2;
             if (w2max > 0) {
                 dZ2.alloc(static_cast<size_t>(n) * w2max);
-                peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S2.get(), w2max, dZ2.get());
+                peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S2.get(), w2max, dZ2.get(), 1);
                 k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 1, dw2.get(), w2max, dZ2.get(), n);
                 HG_LAUNCH();
                 ++ctx.launches;
@@ -885,14 +893,14 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
     {
         const int bm = tree->bmax;
         DVec Yl(static_cast<size_t>(n) * bm);
-        peel(o, -1, out.h, tau, plan.leaf->get(), bm, Yl.get());
+        peel(o, -1, out.h, tau, plan.leaf->get(), bm, Yl.get(), -1);
         auto to_leaves = [&](DHodlr& h, double* P) {
             leaves_panel(*tree, h.leaves->get(), P, false);
             h.leaves_zero = false;
         };
         to_leaves(out.h, Yl.get());
         for (int q = 0; q < p; ++q) {
-            peel(o, q, out.deriv[static_cast<size_t>(q)], tau, plan.leaf->get(), bm, Yl.get());
+            peel(o, q, out.deriv[static_cast<size_t>(q)], tau, plan.leaf->get(), bm, Yl.get(), -1);
             to_leaves(out.deriv[static_cast<size_t>(q)], Yl.get());
         }
     }

@@ -49,7 +49,21 @@ struct ProjArgs {
     const double* X;
     i64 ldx, n;
     int s, tiles_n;
+    ZeroRows zero;
 };
+
+/// Segment (of the hint's partition) holding row r.
+__device__ __forceinline__ int seg_of(const int* b, int nseg, int r) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (b[mid] <= r)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
 
 __device__ __forceinline__ int cdiv_i(int a, int b) { return (a + b - 1) / b; }
 
@@ -64,7 +78,13 @@ __global__ void __launch_bounds__(THREADS) k_ml_proj(ProjArgs g) {
     tile::LoadKCT<TBN> lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
     tile::AccT<TBM / 16, TBN / 16> acc;
     acc.zero();
-    tile::run_t<tile::STAGES, TBM, TBN>(la, lb, cdiv_i(it.rows, BK), smem, acc);
+    int kt = cdiv_i(it.rows, BK);
+    if (g.zero.bounds && it.rows > 0) {  // chunk inside a known-zero segment of X: T tile = 0
+        const int s0 = seg_of(g.zero.bounds, g.zero.nseg, it.row0);
+        const int s1 = seg_of(g.zero.bounds, g.zero.nseg, it.row0 + it.rows - 1);
+        if (s0 == s1 && (s0 & 1) == g.zero.parity) kt = 0;
+    }
+    tile::run_t<tile::STAGES, TBM, TBN>(la, lb, kt, smem, acc);
     const i64 blk = i64(R) * g.s;
     double* o = g.L.ws[l] ? g.L.ws[l] + i64(it.chunk) * blk : g.L.T[l] + i64(it.seg) * blk;
     tile::for_each_t<TBM, TBN>(acc, [&](int mi, int ni, double v) {
@@ -260,7 +280,7 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
 }  // namespace
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
-                 bool with_leaves, bool transpose, double beta, double alpha) {
+                 bool with_leaves, bool transpose, double beta, double alpha, ZeroRows zero) {
     if (s <= 0) return;
     const i64 n = h.n();
     const DTree& t = *h.tree;
@@ -315,7 +335,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     const int tbm = tile::tile_for(rmax), tbn = tile::tile_for(s);
     const int max_tiles_m = (rmax + tbm - 1) / tbm;
     const int tiles_n = (s + tbn - 1) / tbn;
-    ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n};
+    ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n, zero};
     with_tile(tbm, [&](auto TM) {
         with_tile(tbn, [&](auto TN) {
             constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
