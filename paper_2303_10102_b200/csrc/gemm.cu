@@ -94,28 +94,28 @@ struct SegNnArgs {
 };
 
 /// Y[rows] = X[rows] T_sel: X m-contiguous (rows = m), T k-contiguous.
-template <int TBN>
+template <int TBM, int TBN>
 __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
     extern __shared__ double smem[];
     const WorkItem it = g.items[blockIdx.x];
     const int n0 = blockIdx.y * TBN;
     const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.map.mult * g.tstride +
                        i64(g.map.add) * g.tstride + ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
-    tile::LoadMCT<BM> la{g.X + it.row0, g.ldx, it.rows, g.k};
+    tile::LoadMCT<TBM> la{g.X + it.row0, g.ldx, it.rows, g.k};
     tile::LoadKCT<TBN> lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
-    tile::AccT<BM / 16, TBN / 16> acc;
+    tile::AccT<TBM / 16, TBN / 16> acc;
     acc.zero();
     // The accumulate-into-Y operand is fetched before the (short-K) main loop
     // so its latency overlaps the GEMM instead of trailing it.
-    tile::AccT<BM / 16, TBN / 16> yv;
+    tile::AccT<TBM / 16, TBN / 16> yv;
     yv.zero();
     if (g.beta != 0.0)
-        tile::for_each_slot<BM, TBN>(yv, [&](double& s, int m, int ni) {
+        tile::for_each_slot<TBM, TBN>(yv, [&](double& s, int m, int ni) {
             const int n = n0 + ni;
             if (n < g.w && m < it.rows) s = g.Y[i64(it.row0 + m) + i64(n) * g.ldy];
         });
-    tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(g.k, BK), smem, acc);
-    tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
+    tile::run_t<NS_SHORT, TBM, TBN>(la, lb, cdiv_d(g.k, BK), smem, acc);
+    tile::for_each_slot2<TBM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
         const int n = n0 + ni;
         if (n >= g.w || m >= it.rows) return;
         g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + g.beta * y;
@@ -366,14 +366,23 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
     if (prof_enabled()) prof.key(prof_tag("nn nseg=%d k=%d w=%d", p.nseg(), k, w));
-    const TileList& tl = p.tiles(BM);
+    // Row tile: 64, or one tile per segment when every segment is short
+    // (e.g. the 2R-row node blocks of the capacitance solves).
+    const int tbm = p.max_seg() <= 96 ? std::max(48, tile::tile_for(p.max_seg())) : BM;
+    const TileList& tl = p.tiles(tbm);
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
     const int tbn = tile::tile_for(w);
-    with_tile(tbn, [&](auto TN) {
-        constexpr int N = decltype(TN)::value;
-        constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
-        attr_once<k_seg_nn<N>>(bytes);
-        k_seg_nn<N><<<dim3(unsigned(tl.count), unsigned(cdiv(w, N))), THREADS, bytes, c.stream>>>(g);
+    with_tile(tbm, [&](auto TM) {
+        with_tile(tbn, [&](auto TN) {
+            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+            if constexpr (M == 64 || M == 80 || M == 96 || M == 48) {
+                constexpr int bytes = tile::smem_bytes_t(NS_SHORT, M, N);
+                attr_once<k_seg_nn<M, N>>(bytes);
+                k_seg_nn<M, N><<<dim3(unsigned(tl.count), unsigned(cdiv(w, N))), THREADS, bytes, c.stream>>>(g);
+            } else {
+                throw std::logic_error("seg_nn: unsupported row tile");
+            }
+        });
     });
     HG_LAUNCH();
     ++c.launches;
