@@ -160,6 +160,24 @@ hg_status hg_oracle_counters(hg_oracle_t o, uint64_t* apply_columns, uint64_t* d
 /* build_hodlr / build_hodlr_with_derivatives with SketchPlan(tree, k, seed)
  * generated on the host by std::mt19937_64 + std::normal_distribution in the
  * reference's fill order — sketch.cpp:10-31, 128-356. */
+/* SketchPlan sampler bytes (sketch.cpp:10-31): level 0 = the leaf sampler
+ * (n x max_leaf_size stacked identities), level l in [1, tau] = the n x k
+ * Gaussian sampler of level l; generated on the host with the reference's
+ * mt19937_64 / normal_distribution fill order, cached on the device. */
+hg_status hg_sketch_sampler(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_t seed, int level, double* out,
+                            int64_t ldo, int loc);
+/* randomized_range(y, k) (sketch.cpp:37-76): rows x k block y -> q (rows x k,
+ * orthonormal), r (k x k upper, diag >= 0, host), perm (k, host; y.col(perm[i])
+ * -> position i), numeric rank (#|r_ii| > 64 eps |r_00|); deficient columns
+ * completed with unit vectors orthogonalised twice. k <= 64. */
+hg_status hg_randomized_range(hg_ctx_t ctx, const double* y, int64_t ldy, int64_t rows, int64_t k, double* q,
+                              int64_t ldq, double* r, int* perm, int64_t* numeric_rank, int loc);
+/* diff_qr(b, db, q, r) (sketch.cpp:78-111): derivative of b = q r under db ->
+ * dq, dq_span = q dOmega (rows x k), dr (k x k, host), ill-conditioned flag
+ * (max/min |r_ii| > 1e12). b itself is not needed (as in the reference). */
+hg_status hg_diff_qr(hg_ctx_t ctx, const double* db, int64_t lddb, const double* q, int64_t ldq, const double* r,
+                     int64_t rows, int64_t k, double* dq, int64_t lddq, double* dq_span, int64_t ldds, double* dr,
+                     int* ill_conditioned, int loc);
 hg_status hg_build(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, int with_derivatives,
                    hg_build_t* out);
 hg_status hg_build_free(hg_build_t b);

@@ -644,7 +644,121 @@ void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, i
     hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
 }
 
+/// diff_qr core (sketch.cpp:78-111) on one k x k problem: Y = G R^-1 (row
+/// substitution, column by column as solve_upper_right), dOmega = skew(strict
+/// lower of Y), dR = triu((Y - dOmega) R), ill = !(dmin > 0) || dmax/dmin > 1e12.
+__global__ void k_diffqr_core(int k, const double* G, const double* R, double* Y, double* Om, double* dR, int* ill) {
+    extern __shared__ double ys[];  // k x k
+    const int t = threadIdx.x;
+    for (int e = t; e < k * k; e += blockDim.x) ys[e] = G[e];
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {  // Y(:, j) = (G(:, j) - sum_{i<j} Y(:, i) R(i, j)) / R(j, j)
+        for (int row = t; row < k; row += blockDim.x) {
+            double x = ys[row + j * k];
+            for (int i = 0; i < j; ++i) {
+                const double rij = R[i + j * k];
+                if (rij != 0.0) x -= ys[row + i * k] * rij;
+            }
+            ys[row + j * k] = x / R[j + j * k];
+        }
+        __syncthreads();
+    }
+    for (int e = t; e < k * k; e += blockDim.x) {
+        const int i = e % k, j = e / k;
+        Y[e] = ys[e];
+        Om[e] = i > j ? ys[e] : (i < j ? -ys[j + i * k] : 0.0);
+    }
+    __syncthreads();
+    for (int e = t; e < k * k; e += blockDim.x) {
+        const int i = e % k, j = e / k;
+        double s = 0.0;
+        if (i <= j)
+            for (int l = 0; l <= j; ++l) {
+                const double yo = ys[i + l * k] - (i > l ? ys[i + l * k] : (i < l ? -ys[l + i * k] : 0.0));
+                s += yo * R[l + j * k];
+            }
+        dR[e] = s;
+    }
+    if (t == 0) {
+        double dmax = 0.0, dmin = 1.0 / 0.0;
+        for (int i = 0; i < k; ++i) {
+            dmax = fmax(dmax, fabs(R[i + i * k]));
+            dmin = fmin(dmin, fabs(R[i + i * k]));
+        }
+        *ill = !(dmin > 0) || dmax / dmin > 1e12;
+    }
+}
+
+/// X <- X R^-1 for an m x k panel (column by column, solve_upper_right).
+__global__ void k_solve_upper_right(int m, int k, const double* R, double* X, i64 ldx) {
+    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < m; row += gridDim.x * blockDim.x)
+        for (int j = 0; j < k; ++j) {
+            double x = X[row + i64(j) * ldx];
+            for (int i = 0; i < j; ++i) {
+                const double rij = R[i + j * k];
+                if (rij != 0.0) x -= X[row + i64(i) * ldx] * rij;
+            }
+            X[row + i64(j) * ldx] = x / R[j + j * k];
+        }
+}
+
 }  // namespace
+
+void diff_qr(const double* dB, i64 lddb, const double* Q, i64 ldq, const double* R, int rows, int k, double* dQ,
+             i64 lddq, double* dQspan, i64 ldds, double* dR, int* ill) {
+    if (k <= 0 || k > 64 || rows < k) throw std::invalid_argument("diff_qr: need rows >= k, 1 <= k <= 64");
+    auto& ctx = current();
+    const Partition one(std::vector<int>{0, rows});
+    DVec G(static_cast<size_t>(k) * k), Y(static_cast<size_t>(k) * k), Om(static_cast<size_t>(k) * k);
+    DVec Rc(static_cast<size_t>(k) * k);
+    HG_CUDA(cudaMemcpyAsync(Rc.get(), R, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx.stream));
+    seg_tn(one, Q, ldq, k, dB, lddb, k, G.get(), i64(k) * k, k);  // q^T dB
+    k_diffqr_core<<<1, 128, sizeof(double) * k * k, ctx.stream>>>(k, G.get(), Rc.get(), Y.get(), Om.get(), dR, ill);
+    HG_LAUNCH();
+    seg_nn(one, Q, ldq, k, Om.get(), 0, k, TMap::same(), dQspan, ldds, k, 1.0, 0.0);  // q dOmega
+    panel_axpby(rows, k, 1.0, dB, lddb, 0.0, dQ, lddq);
+    seg_nn(one, Q, ldq, k, G.get(), 0, k, TMap::same(), dQ, lddq, k, -1.0, 1.0);  // dB - q q^T dB
+    k_solve_upper_right<<<cdiv(rows, 128), 128, 0, ctx.stream>>>(rows, k, Rc.get(), dQ, lddq);
+    HG_LAUNCH();
+    ctx.launches += 2;
+    panel_axpby(rows, k, 1.0, dQspan, ldds, 1.0, dQ, lddq);
+}
+
+void randomized_range(const double* Y, i64 ldy, int rows, int k, double* Q, i64 ldq, double* R, int* perm,
+                      int* nr) {
+    if (k <= 0 || rows < k) throw std::invalid_argument("randomized_range: need rows >= k >= 1");
+    if (k > 64) throw std::length_error("randomized_range: rank above 64 not supported");
+    auto& ctx = current();
+    // one node: the block is the left child, the right child is empty
+    const Partition pc(std::vector<int>{0, rows, rows});
+    const std::vector<int> qmap{rows == k ? -1 : 0};
+    DBuf<int> dqmap;
+    dqmap.upload(qmap);
+    DVec S(static_cast<size_t>(rows) * k), Rn(static_cast<size_t>(k) * k), sign(static_cast<size_t>(k));
+    S.zero();
+    DVec Yc(static_cast<size_t>(rows) * k);  // the QR overwrites its input
+    panel_axpby(rows, k, 1.0, Y, ldy, 0.0, Yc.get(), rows);
+    std::unique_ptr<BatchedQR> qr;
+    if (qmap[0] >= 0) {
+        qr = std::make_unique<BatchedQR>(std::vector<BatchedQR::Block>{{Yc.get(), rows, rows}}, k, true);
+        qr->form_q(k, nullptr, 0, 0, {S.get()}, {rows});
+    }
+    DVec dummyR(1);
+    DBuf<int> dummyP(1), dnr(1), dperm(static_cast<size_t>(k));
+    k_range_post<<<1, 128, 0, ctx.stream>>>(k, dqmap.get(), qr ? qr->R() : dummyR.get(), qr ? qr->perm() : dummyP.get(),
+                                            Rn.get(), dperm.get(), sign.get(), dnr.get());
+    HG_LAUNCH();
+    const TileList& tl = pc.tiles(256);
+    k_q_sign_rows<<<tl.count, 256, 0, ctx.stream>>>(tl.items.get(), pc.dbounds(), k, dqmap.get(), sign.get(), S.get(),
+                                                    rows);
+    HG_LAUNCH();
+    ctx.launches += 2;
+    complete_deficient(pc, k, dnr, S.get(), rows);
+    panel_axpby(rows, k, 1.0, S.get(), rows, 0.0, Q, ldq);
+    HG_CUDA(cudaMemcpyAsync(R, Rn.get(), sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx.stream));
+    HG_CUDA(cudaMemcpyAsync(perm, dperm.get(), sizeof(int) * k, cudaMemcpyDeviceToDevice, ctx.stream));
+    HG_CUDA(cudaMemcpyAsync(nr, dnr.get(), sizeof(int), cudaMemcpyDeviceToDevice, ctx.stream));
+}
 
 DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
     static std::mutex mu;

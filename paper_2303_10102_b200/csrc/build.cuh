@@ -25,6 +25,16 @@ using DSketchPlanP = std::shared_ptr<const DSketchPlan>;
 /// sketch.cpp:10-31 (cached per tree, k, seed).
 DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed);
 
+/// randomized_range (sketch.cpp:37-76) of one rows x k block on the device:
+/// pivoted QR, Q = first k Householder columns, diag(R) >= 0 by sign flip,
+/// numeric rank = #|r_ii| > 64 eps |r_00|, deficient columns completed with
+/// e_0, e_1, ... orthogonalised twice. R, perm, nr are device pointers.
+void randomized_range(const double* Y, i64 ldy, int rows, int k, double* Q, i64 ldq, double* R, int* perm, int* nr);
+
+/// diff_qr (sketch.cpp:78-111) of b = q r under perturbation dB (device).
+void diff_qr(const double* dB, i64 lddb, const double* Q, i64 ldq, const double* R, int rows, int k, double* dQ,
+             i64 lddq, double* dQspan, i64 ldds, double* dR, int* ill);
+
 struct DBuildResult {
     DHodlr h;
     std::vector<DHodlr> deriv;

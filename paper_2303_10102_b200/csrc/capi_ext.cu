@@ -79,6 +79,103 @@ hg_status hg_mle_evaluate(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint6
     });
 }
 
+namespace {
+/// Device copy of a host (loc = HG_HOST) or device rows x cols block.
+struct In {
+    DVec buf;
+    const double* p;
+    i64 ld;
+    In(const double* src, i64 lds, i64 rows, i64 cols, int loc) {
+        if (loc == HG_DEVICE) {
+            p = src;
+            ld = lds;
+            return;
+        }
+        buf.alloc(static_cast<size_t>(rows * cols));
+        if (rows * cols)
+            HG_CUDA(cudaMemcpy2DAsync(buf.get(), sizeof(double) * rows, src, sizeof(double) * lds, sizeof(double) * rows,
+                                      static_cast<size_t>(cols), cudaMemcpyHostToDevice, current().stream));
+        p = buf.get();
+        ld = rows;
+    }
+};
+/// Device destination; copied back to the host by finish().
+struct Out {
+    DVec buf;
+    double* p;
+    i64 ld;
+    double* host;
+    i64 ldh, rows, cols;
+    Out(double* dst, i64 ldd, i64 r, i64 c, int loc) : host(nullptr), ldh(ldd), rows(r), cols(c) {
+        if (loc == HG_DEVICE) {
+            p = dst;
+            ld = ldd;
+            return;
+        }
+        buf.alloc(static_cast<size_t>(r * c));
+        p = buf.get();
+        ld = r;
+        host = dst;
+    }
+    void finish() {
+        if (host && rows * cols)
+            HG_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * ldh, p, sizeof(double) * rows, sizeof(double) * rows,
+                                      static_cast<size_t>(cols), cudaMemcpyDeviceToHost, current().stream));
+    }
+};
+}  // namespace
+
+hg_status hg_randomized_range(hg_ctx_t ctx, const double* y, int64_t ldy, int64_t rows, int64_t k, double* q,
+                              int64_t ldq, double* r, int* perm, int64_t* numeric_rank, int loc) {
+    return capi_guard(ctx, [&] {
+        In Y(y, ldy, rows, k, loc);
+        Out Q(q, ldq, rows, k, loc);
+        DVec R(static_cast<size_t>(k * k));
+        DBuf<int> P(static_cast<size_t>(k)), nr(1);
+        randomized_range(Y.p, Y.ld, int(rows), int(k), Q.p, Q.ld, R.get(), P.get(), nr.get());
+        Q.finish();
+        std::vector<double> rh = R.download();
+        std::vector<int> ph = P.download(), nh = nr.download();
+        std::copy(rh.begin(), rh.end(), r);
+        std::copy(ph.begin(), ph.end(), perm);
+        *numeric_rank = nh[0];
+    });
+}
+
+hg_status hg_diff_qr(hg_ctx_t ctx, const double* db, int64_t lddb, const double* q, int64_t ldq, const double* r,
+                     int64_t rows, int64_t k, double* dq, int64_t lddq, double* dq_span, int64_t ldds, double* dr,
+                     int* ill_conditioned, int loc) {
+    return capi_guard(ctx, [&] {
+        In dB(db, lddb, rows, k, loc), Q(q, ldq, rows, k, loc);
+        DVec R;
+        R.upload(r, static_cast<size_t>(k * k));
+        Out dQ(dq, lddq, rows, k, loc), dS(dq_span, ldds, rows, k, loc);
+        DVec dR(static_cast<size_t>(k * k));
+        DBuf<int> ill(1);
+        diff_qr(dB.p, dB.ld, Q.p, Q.ld, R.get(), int(rows), int(k), dQ.p, dQ.ld, dS.p, dS.ld, dR.get(), ill.get());
+        dQ.finish();
+        dS.finish();
+        std::vector<double> rh = dR.download();
+        std::copy(rh.begin(), rh.end(), dr);
+        *ill_conditioned = ill.download()[0];
+    });
+}
+
+hg_status hg_sketch_sampler(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_t seed, int level, double* out,
+                            int64_t ldo, int loc) {
+    return capi_guard(ctx, [&] {
+        DTreeP tree = get_tree(n, tau);
+        DSketchPlanP plan = get_plan(tree, k, seed);
+        if (level < 0 || level > tau) throw std::invalid_argument("sketch_sampler: level in [0, tau]");
+        const double* src = level == 0 ? plan->leaf->get() : plan->level[static_cast<size_t>(level - 1)]->get();
+        const i64 cols = level == 0 ? tree->bmax : k;
+        Out o(out, ldo, n, cols, loc);
+        panel_axpby(n, int(cols), 1.0, src, n, 0.0, o.p, o.ld);
+        o.finish();
+        sync();
+    });
+}
+
 void hg_prof_enable(int on) { prof_enable(on != 0); }
 
 int hg_prof_read(int reset, double* ms, double* flops, double* bytes, int64_t* launches) {

@@ -99,6 +99,12 @@ Partition::Partition(int nseg, int len) : depth_(-1), nseg_(nseg), max_seg_(len)
     db_.upload(hb_);
 }
 
+Partition::Partition(const std::vector<int>& bounds) : depth_(-1), nseg_(int(bounds.size()) - 1), hb_(bounds) {
+    for (int s = 0; s < nseg_; ++s)
+        max_seg_ = std::max(max_seg_, hb_[static_cast<size_t>(s + 1)] - hb_[static_cast<size_t>(s)]);
+    db_.upload(hb_);
+}
+
 const Partition& uniform_partition(int nseg, int len) {
     static std::mutex mu;
     static std::map<std::tuple<int, int, int>, std::unique_ptr<Partition>> cache;

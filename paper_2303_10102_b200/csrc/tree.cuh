@@ -61,6 +61,8 @@ public:
     Partition(const ClusterTree& t, int d);
     /// nseg equal segments of `len` rows (batched per-node small matrices).
     Partition(int nseg, int len);
+    /// Explicit segment bounds (nseg + 1 nondecreasing row offsets).
+    explicit Partition(const std::vector<int>& bounds);
     int depth() const { return depth_; }
     int nseg() const { return nseg_; }
     const std::vector<int>& hbounds() const { return hb_; }

@@ -63,6 +63,10 @@ _SIGS = {
     "hg_oracle_dense": (C.c_int, [vp, i64, dp, C.c_int, dp, C.POINTER(vp)]),
     "hg_oracle_matern": (C.c_int, [vp, i64, dp, C.c_int, dbl, dbl, dbl, C.c_int, C.POINTER(vp)]),
     "hg_oracle_cokriging": (C.c_int, [vp, i64, dbl, dbl, dbl, dbl, C.POINTER(vp)]),
+    "hg_sketch_sampler": (C.c_int, [vp, i64, C.c_int, i64, C.c_uint64, C.c_int, C.c_void_p, i64, C.c_int]),
+    "hg_randomized_range": (C.c_int, [vp, C.c_void_p, i64, i64, i64, C.c_void_p, i64, dp, ip, C.POINTER(i64), C.c_int]),
+    "hg_diff_qr": (C.c_int, [vp, C.c_void_p, i64, C.c_void_p, i64, dp, i64, i64, C.c_void_p, i64, C.c_void_p, i64, dp,
+                             C.POINTER(C.c_int), C.c_int]),
     "hg_oracle_spde2d": (C.c_int, [vp, C.c_int, dbl, dbl, dbl, dbl, C.c_void_p, C.POINTER(vp)]),
     "hg_oracle_callback": (C.c_int, [vp, i64, C.c_int, vp, vp, C.POINTER(vp)]),
     "hg_oracle_set_parameters": (C.c_int, [vp, dp, C.c_int]),
@@ -647,6 +651,44 @@ def grid_kd_order(nside, leaf):
     coords = np.stack([(ix + 0.5) / nside, (iy + 0.5) / nside], axis=1)
     _, inv, _ = build_kd_ordering(coords, 1, 2)
     return inv, ClusterTree(n, tree_depth(n, leaf, 2 * leaf))
+
+
+# ------------------------------------------------------------ sketching
+def sketch_sampler(n, tau, k, seed, level, ctx=None):
+    """SketchPlan sampler bytes (sketch.cpp:10-31); level 0 = leaf sampler."""
+    ctx = ctx or context()
+    cols = max(hi - lo for lo, hi in ClusterTree(n, tau).leaves()) if level == 0 else k
+    out = np.zeros((n, cols), order="F")
+    _check(lib().hg_sketch_sampler(ctx.ptr, n, tau, k, seed, level, out.ctypes.data, n, HOST))
+    return out
+
+
+def randomized_range(y, k, ctx=None):
+    """sketch.cpp:37-76 -> (q, r, perm, numeric_rank)."""
+    ctx = ctx or context()
+    y = _f(y)
+    m = y.shape[0]
+    q = np.zeros((m, k), order="F")
+    r = np.zeros((k, k), order="F")
+    perm = np.zeros(k, dtype=np.int32)
+    nr = i64()
+    _check(lib().hg_randomized_range(ctx.ptr, y.ctypes.data, m, m, k, q.ctypes.data, m, _d(r),
+                                     perm.ctypes.data_as(ip), C.byref(nr), HOST))
+    return q, r, perm, nr.value
+
+
+def diff_qr(db, q, r, ctx=None):
+    """sketch.cpp:78-111 -> (dq, dq_span, dr, ill_conditioned)."""
+    ctx = ctx or context()
+    db, q, r = _f(db), _f(q), _f(r)
+    m, k = q.shape
+    dq = np.zeros((m, k), order="F")
+    dqs = np.zeros((m, k), order="F")
+    dr = np.zeros((k, k), order="F")
+    ill = C.c_int()
+    _check(lib().hg_diff_qr(ctx.ptr, db.ctypes.data, m, q.ctypes.data, m, _d(r), m, k, dq.ctypes.data, m,
+                            dqs.ctypes.data, m, _d(dr), C.byref(ill), HOST))
+    return dq, dqs, dr, bool(ill.value)
 
 
 # ------------------------------------------------------------------ build
