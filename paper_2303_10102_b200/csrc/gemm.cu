@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(THREADS) k_seg_tn(SegTnArgs g) {
     const int m0 = (blockIdx.y % g.tiles_m) * TBM, n0 = (blockIdx.y / g.tiles_m) * TBN;
     tile::LoadKCT<TBM> la{g.A + it.row0 + i64(m0) * g.lda, g.lda, it.rows, g.ca - m0};
     tile::LoadKCT<TBN> lb{g.B + it.row0 + i64(n0) * g.ldb, g.ldb, it.rows, g.cb - n0};
-    tile::AccT<TBM / 16, TBN / 16> acc;
+    typename tile::Shape<TBM, TBN>::Acc acc;
     acc.zero();
     tile::run_t<tile::STAGES, TBM, TBN>(la, lb, cdiv_d(it.rows, BK), smem, acc);
     double* o = g.out + (g.direct ? i64(it.seg) : i64(blockIdx.x)) * g.ostride;
@@ -103,11 +103,11 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
                        i64(g.map.add) * g.tstride + ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
     tile::LoadMCT<TBM> la{g.X + it.row0, g.ldx, it.rows, g.k};
     tile::LoadKCT<TBN> lb{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
-    tile::AccT<TBM / 16, TBN / 16> acc;
+    typename tile::Shape<TBM, TBN>::Acc acc;
     acc.zero();
     // The accumulate-into-Y operand is fetched before the (short-K) main loop
     // so its latency overlaps the GEMM instead of trailing it.
-    tile::AccT<TBM / 16, TBN / 16> yv;
+    typename tile::Shape<TBM, TBN>::Acc yv;
     yv.zero();
     if (g.beta != 0.0)
         tile::for_each_slot<TBM, TBN>(yv, [&](double& s, int m, int ni) {
@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     const int n0 = blockIdx.y * TBN;
     const double* Lb = g.L + i64(b) * g.lstride;
     tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
-    tile::AccT<BM / 16, TBN / 16> acc;
+    typename tile::Shape<BM, TBN>::Acc acc;
     acc.zero();
-    tile::AccT<BM / 16, TBN / 16> yv;
+    typename tile::Shape<BM, TBN>::Acc yv;
     yv.zero();
     if (g.beta != 0.0)  // fetch the accumulated Y before the main loop (latency overlap)
         tile::for_each_slot<BM, TBN>(yv, [&](double& y, int mi0, int ni) {
@@ -339,9 +339,13 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     with_tile(tbm, [&](auto TM) {
         with_tile(tbn, [&](auto TN) {
             constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
-            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
-            attr_once<k_seg_tn<M, N>>(bytes);
-            k_seg_tn<M, N><<<grid, THREADS, bytes, c.stream>>>(g);
+            if constexpr (tile::shape_ok(M, N)) {
+                constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                attr_once<k_seg_tn<M, N>>(bytes);
+                k_seg_tn<M, N><<<grid, THREADS, bytes, c.stream>>>(g);
+            } else {
+                throw std::logic_error("seg_tn: unsupported tile shape");
+            }
         });
     });
     HG_LAUNCH();
@@ -371,11 +375,11 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     const int tbm = p.max_seg() <= 96 ? std::max(48, tile::tile_for(p.max_seg())) : BM;
     const TileList& tl = p.tiles(tbm);
     SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
-    const int tbn = tile::tile_for(w);
+    const int tbn = tile::tile_for_n(w, tbm);
     with_tile(tbm, [&](auto TM) {
         with_tile(tbn, [&](auto TN) {
             constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
-            if constexpr (M == 64 || M == 80 || M == 96 || M == 48) {
+            if constexpr ((M == 64 || M == 80 || M == 96 || M == 48) && tile::shape_ok(M, N)) {
                 constexpr int bytes = tile::smem_bytes_t(NS_SHORT, M, N);
                 attr_once<k_seg_nn<M, N>>(bytes);
                 k_seg_nn<M, N><<<dim3(unsigned(tl.count), unsigned(cdiv(w, N))), THREADS, bytes, c.stream>>>(g);
@@ -397,7 +401,7 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + rows * w * (beta != 0.0 ? 3.0 : 2.0)));
     if (prof_enabled()) prof.key(prof_tag("leafmm w=%d tr=%d", w, int(trans)));
     LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, Y, ldy, w, alpha, beta};
-    const int tbn = tile::tile_for(w);
+    const int tbn = tile::tile_for_n(w, BM);
     with_tile(tbn, [&](auto TN) {
         constexpr int N = decltype(TN)::value;
         constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(THREADS) k_ml_proj(ProjArgs g) {
     if (m0 >= R) return;
     tile::LoadKCT<TBM> la{g.L.P[l] + it.row0 + i64(m0) * g.n, g.n, it.rows, R - m0};
     tile::LoadKCT<TBN> lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
-    tile::AccT<TBM / 16, TBN / 16> acc;
+    typename tile::Shape<TBM, TBN>::Acc acc;
     acc.zero();
     int kt = cdiv_i(it.rows, BK);
     if (g.zero.bounds && it.rows > 0) {  // chunk inside a known-zero segment of X: T tile = 0
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
     const int n0 = blockIdx.y * TBN;
     LoadUpdA la{&L, it.row0, it.rows, g.n};
     LoadUpdB<TBN> lb{&L, it.seg, g.tau, g.s, n0};
-    tile::AccT<BM / 16, TBN / 16> acc, yv;
+    typename tile::Shape<BM, TBN>::Acc acc, yv;
     acc.zero();
     yv.zero();
     if (g.beta != 0.0)  // fetch the accumulated Y before the main loop (latency overlap)
@@ -332,16 +332,21 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     int rmax = 1;
     for (int i = 0; i < L.nl; ++i) rmax = std::max(rmax, L.R[i]);
-    const int tbm = tile::tile_for(rmax), tbn = tile::tile_for(s);
+    const int tbm = tile::tile_for(rmax), tbn = tile::tile_for_n(s, tbm);
     const int max_tiles_m = (rmax + tbm - 1) / tbm;
     const int tiles_n = (s + tbn - 1) / tbn;
     ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n, zero};
     with_tile(tbm, [&](auto TM) {
         with_tile(tbn, [&](auto TN) {
             constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
-            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
-            attr_once<k_ml_proj<M, N>>(bytes);
-            k_ml_proj<M, N><<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
+            if constexpr (tile::shape_ok(M, N)) {
+                constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                attr_once<k_ml_proj<M, N>>(bytes);
+                k_ml_proj<M, N>
+                    <<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
+            } else {
+                throw std::logic_error("hodlr_apply: unsupported tile shape");
+            }
         });
     });
     HG_LAUNCH();
@@ -356,11 +361,13 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     const TileList& tl = t.leaves().tiles(BM);
     UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta};
-    with_tile(tbn, [&](auto TN) {
+    // the update's N tile may differ from the projection's (its M is always 64)
+    const int tbn_u = tile::tile_for_n(s, BM), tiles_nu = (s + tbn_u - 1) / tbn_u;
+    with_tile(tbn_u, [&](auto TN) {
         constexpr int N = decltype(TN)::value;
         constexpr int bytes = tile::smem_bytes_t(2, BM, N);
         attr_once<k_ml_update<N>>(bytes);
-        k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_n)), THREADS, bytes, c.stream>>>(ua);
+        k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
     });
     HG_LAUNCH();
     ++c.launches;

@@ -48,6 +48,25 @@ struct AccT {
 };
 using Acc = AccT<4, 4>;
 
+/// Warp grid of a TBM x TBN tile (4 warps): WGM x WGN with WGM * WGN = 4,
+/// each warp (TBM / WGM) x (TBN / WGN) = WM x WN DMMA tiles. 2 x 2 when both
+/// extents are multiples of 16; 4 x 1 for N = 40 (M a multiple of 32); 1 x 4
+/// for M = 40 (N a multiple of 32).
+constexpr bool shape_ok(int m, int n) {
+    const int wgn = (m % 16 == 0 && n % 16 == 0) ? 2 : (m % 32 == 0 ? 1 : 4);
+    const int wgm = 4 / wgn;
+    return m % (8 * wgm) == 0 && n % (8 * wgn) == 0;
+}
+
+template <int TBM, int TBN>
+struct Shape {
+    static constexpr int WGN = (TBM % 16 == 0 && TBN % 16 == 0) ? 2 : (TBM % 32 == 0 ? 1 : 4);
+    static constexpr int WGM = 4 / WGN;
+    static constexpr int WM = TBM / (8 * WGM), WN = TBN / (8 * WGN);
+    static_assert(WM * 8 * WGM == TBM && WN * 8 * WGN == TBN, "tile extents do not fit the warp grid");
+    using Acc = AccT<WM, WN>;
+};
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
@@ -73,10 +92,11 @@ __device__ __forceinline__ double frag(const double* S, int m, int k) {
 
 /// One BK slice: acc += A(:, k) B(:, k)^T over the warp's sub-tile.
 template <bool AKC, bool BKC, int TBM, int TBN>
-__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, AccT<TBM / 16, TBN / 16>& acc) {
-    constexpr int WM = TBM / 16, WN = TBN / 16;
+__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, typename Shape<TBM, TBN>::Acc& acc) {
+    using S = Shape<TBM, TBN>;
+    constexpr int WM = S::WM, WN = S::WN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int wm = (warp / S::WGN) * (TBM / S::WGM), wn = (warp % S::WGN) * (TBN / S::WGN);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
@@ -96,7 +116,7 @@ __device__ __forceinline__ void mma_stage(const double* As, const double* Bs, Ac
 ///   static constexpr bool KC;  static constexpr int ROWS;
 ///   __device__ void issue(double* stage, int kt);   // cp.async one BK slice
 template <int NS, int TBM, int TBN, class LA, class LB>
-__device__ __forceinline__ void run_t(LA& la, LB& lb, int ktiles, double* smem, AccT<TBM / 16, TBN / 16>& acc) {
+__device__ __forceinline__ void run_t(LA& la, LB& lb, int ktiles, double* smem, typename Shape<TBM, TBN>::Acc& acc) {
     static_assert(LA::ROWS == TBM && LB::ROWS == TBN, "loader extents must match the tile");
     constexpr int AE = stage_elems(TBM), BE = stage_elems(TBN);
     double* As = smem;
@@ -182,14 +202,15 @@ using LoadMC = LoadMCT<64>;
 
 /// Visit every accumulator element owned by this thread: f(m, n, value).
 template <int TBM, int TBN, class F>
-__device__ __forceinline__ void for_each_t(const AccT<TBM / 16, TBN / 16>& acc, F&& f) {
+__device__ __forceinline__ void for_each_t(const typename Shape<TBM, TBN>::Acc& acc, F&& f) {
+    using S = Shape<TBM, TBN>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int wm = (warp / S::WGN) * (TBM / S::WGM), wn = (warp % S::WGN) * (TBN / S::WGN);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int i = 0; i < TBM / 16; ++i)
+    for (int i = 0; i < S::WM; ++i)
 #pragma unroll
-        for (int j = 0; j < TBN / 16; ++j)
+        for (int j = 0; j < S::WN; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) f(wm + i * 8 + g, wn + j * 8 + 2 * t + e, acc.v[i][j][e]);
 }
@@ -201,29 +222,31 @@ __device__ __forceinline__ void for_each(const Acc& acc, F&& f) {
 /// Same traversal as for_each_t, exposing the accumulator slot:
 /// f(double& slot, m, n) for every element owned by this thread.
 template <int TBM, int TBN, class F>
-__device__ __forceinline__ void for_each_slot(AccT<TBM / 16, TBN / 16>& a, F&& f) {
+__device__ __forceinline__ void for_each_slot(typename Shape<TBM, TBN>::Acc& a, F&& f) {
+    using S = Shape<TBM, TBN>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int wm = (warp / S::WGN) * (TBM / S::WGM), wn = (warp % S::WGN) * (TBN / S::WGN);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int i = 0; i < TBM / 16; ++i)
+    for (int i = 0; i < S::WM; ++i)
 #pragma unroll
-        for (int j = 0; j < TBN / 16; ++j)
+        for (int j = 0; j < S::WN; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) f(a.v[i][j][e], wm + i * 8 + g, wn + j * 8 + 2 * t + e);
 }
 
 /// Paired traversal of two accumulator sets: f(a_slot, b_slot, m, n).
 template <int TBM, int TBN, class F>
-__device__ __forceinline__ void for_each_slot2(const AccT<TBM / 16, TBN / 16>& a, const AccT<TBM / 16, TBN / 16>& b,
-                                               F&& f) {
+__device__ __forceinline__ void for_each_slot2(const typename Shape<TBM, TBN>::Acc& a,
+                                               const typename Shape<TBM, TBN>::Acc& b, F&& f) {
+    using S = Shape<TBM, TBN>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * (TBM / 2), wn = (warp & 1) * (TBN / 2);
+    const int wm = (warp / S::WGN) * (TBM / S::WGM), wn = (warp % S::WGN) * (TBN / S::WGN);
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int i = 0; i < TBM / 16; ++i)
+    for (int i = 0; i < S::WM; ++i)
 #pragma unroll
-        for (int j = 0; j < TBN / 16; ++j)
+        for (int j = 0; j < S::WN; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) f(a.v[i][j][e], b.v[i][j][e], wm + i * 8 + g, wn + j * 8 + 2 * t + e);
 }
@@ -237,6 +260,13 @@ inline int tile_for(int x) {
     return w80 < w64 ? 80 : 64;
 }
 
+/// N extent when the M extent is fixed at tbm: like tile_for, plus 40 (a
+/// 4 x 1 warp grid) for 33..40 columns when tbm is a multiple of 32.
+inline int tile_for_n(int x, int tbm) {
+    if (x > 32 && x <= 40 && tbm % 32 == 0) return 40;
+    return tile_for(x);
+}
+
 }  // namespace tile
 
 /// Host: run f(std::integral_constant<int, T>) for the tile extent t.
@@ -245,6 +275,7 @@ void with_tile(int t, F&& f) {
     switch (t) {
         case 16: f(std::integral_constant<int, 16>{}); break;
         case 32: f(std::integral_constant<int, 32>{}); break;
+        case 40: f(std::integral_constant<int, 40>{}); break;
         case 48: f(std::integral_constant<int, 48>{}); break;
         case 64: f(std::integral_constant<int, 64>{}); break;
         case 80: f(std::integral_constant<int, 80>{}); break;
