@@ -323,7 +323,11 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
     if (prof_enabled()) prof.key(prof_tag("tn nseg=%d ca=%d cb=%d", p.nseg(), ca, cb));
     const TileList& tl = p.tiles(SEG_CHUNK);
-    const int tbm = tile::tile_for(ca), tbn = tile::tile_for(cb);
+    int tbm = tile::tile_for(ca), tbn = tile::tile_for(cb);
+    if (ca > 32 && ca <= 40 && tbn % 32 == 0)  // 1 x 4 warp grid
+        tbm = 40;
+    else if (cb > 32 && cb <= 40 && tbm % 32 == 0)  // 4 x 1 warp grid
+        tbn = 40;
     const int tiles_m = cdiv(ca, tbm), tiles_n = cdiv(cb, tbn);
     SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
     DVec ws;

@@ -70,6 +70,12 @@ struct ZeroRows {
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
                  bool with_leaves, bool transpose, double beta = 0.0, double alpha = 1.0, ZeroRows zero = {});
 
+/// Projections of all levels at once: T_l[s] = P_l[s]^T X[s] (P = U when
+/// transpose, else V) for the first ncol[l-1] columns of X, as nseg_l
+/// blocks of R_l x s (ld R_l). Entries of missing levels are null.
+std::vector<DVecP> hodlr_project(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose,
+                                 const std::vector<int>& ncol);
+
 /// Leaves <-> n x bmax panel (leaf b occupies its rows, columns [0, m_b)).
 void leaves_panel(const DTree& t, double* leaves, double* P, bool to_panel);
 

@@ -37,6 +37,7 @@ struct MlLevels {
     double* T[MAXL];        // per-level projections: nseg_l x R_l x s (ld R_l)
     double* ws[MAXL];       // split-K partial workspace (null when one chunk per segment)
     int item_off[MAXL + 1]; // first projection work item of each level
+    int ncol[MAXL];         // columns of X the level's projection needs (<= s)
 };
 
 struct MlItem {  // projection work item
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(THREADS) k_ml_proj(ProjArgs g) {
     const MlItem it = g.items[blockIdx.x];
     const int l = it.level, R = g.L.R[l];
     const int m0 = (blockIdx.y / g.tiles_n) * TBM, n0 = (blockIdx.y % g.tiles_n) * TBN;
-    if (m0 >= R) return;
+    if (m0 >= R || n0 >= g.L.ncol[l]) return;
     tile::LoadKCT<TBM> la{g.L.P[l] + it.row0 + i64(m0) * g.n, g.n, it.rows, R - m0};
     tile::LoadKCT<TBN> lb{g.X + it.row0 + i64(n0) * g.ldx, g.ldx, it.rows, g.s - n0};
     typename tile::Shape<TBM, TBN>::Acc acc;
@@ -107,7 +108,7 @@ __global__ void k_ml_reduce(ReduceArgs g) {
     const int l = g.seg_level[r], R = g.L.R[l];
     const i64 blk = i64(R) * g.s;
     const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= blk) return;
+    if (e >= blk || e / R >= g.L.ncol[l]) return;
     const double* w = g.L.ws[l];
     double sum = 0.0;
     for (int c = g.first[r]; c < g.first[r] + g.count[r]; ++c) sum += w[i64(c) * blk + e];
@@ -321,6 +322,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         }
         L.T[i] = Tbuf[static_cast<size_t>(i)].get();
         L.ws[i] = Wbuf[static_cast<size_t>(i)].get();
+        L.ncol[i] = s;
         flops += 4.0 * double(n) * R * s;
         bytes += 16.0 * double(n) * R;
     }
@@ -371,6 +373,73 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     });
     HG_LAUNCH();
     ++c.launches;
+}
+
+std::vector<DVecP> hodlr_project(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose,
+                                 const std::vector<int>& ncol) {
+    const i64 n = h.n();
+    const DTree& t = *h.tree;
+    const int tau = h.tau();
+    std::vector<DVecP> out(static_cast<size_t>(tau));
+    if (s <= 0 || tau < 1) return out;
+    if (tau > MAXL) throw std::length_error("hodlr_project: too many levels");
+    auto& c = current();
+    const ItemPlan& ip = item_plan(t, 1, tau);
+    MlLevels L{};
+    L.nl = tau;
+    std::vector<DVec> Wbuf(static_cast<size_t>(tau));
+    double flops = 0;
+    int rmax = 1, cmax = 0;
+    for (int i = 0; i < tau; ++i) {
+        const int l = 1 + i, R = h.Rl(l);
+        const int nc = std::min(s, ncol[static_cast<size_t>(i)]);
+        const Partition& pt = t.part(l);
+        L.depth[i] = l;
+        L.R[i] = nc > 0 ? R : 0;
+        L.P[i] = transpose ? h.Ul(l) : h.Vl(l);
+        L.Q[i] = nullptr;
+        L.ncol[i] = nc;
+        if (L.R[i] > 0) {
+            out[static_cast<size_t>(i)] = make_dvec(static_cast<size_t>(pt.nseg()) * R * s, false);
+            if (ip.nchunks[static_cast<size_t>(i)])
+                Wbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(ip.nchunks[static_cast<size_t>(i)]) * R * s);
+            rmax = std::max(rmax, R);
+            cmax = std::max(cmax, nc);
+        }
+        L.T[i] = out[static_cast<size_t>(i)] ? out[static_cast<size_t>(i)]->get() : nullptr;
+        L.ws[i] = Wbuf[static_cast<size_t>(i)].get();
+        flops += 2.0 * double(n) * L.R[i] * nc;
+    }
+    if (cmax == 0) return out;
+    ProfScope prof(PROF_SEG_TN, flops, 8.0 * double(n) * cmax);
+    if (prof_enabled()) prof.key(prof_tag("mlproject s=%d Rmax=%d tr=%d", s, rmax, int(transpose)));
+    const int tbm = tile::tile_for(rmax), tbn = tile::tile_for_n(cmax, tbm);
+    const int max_tiles_m = (rmax + tbm - 1) / tbm, tiles_n = (cmax + tbn - 1) / tbn;
+    ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n, ZeroRows{}};
+    with_tile(tbm, [&](auto TM) {
+        with_tile(tbn, [&](auto TN) {
+            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+            if constexpr (tile::shape_ok(M, N)) {
+                constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                attr_once<k_ml_proj<M, N>>(bytes);
+                k_ml_proj<M, N>
+                    <<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
+            } else {
+                throw std::logic_error("hodlr_project: unsupported tile shape");
+            }
+        });
+    });
+    HG_LAUNCH();
+    ++c.launches;
+    if (ip.nred) {
+        int maxblk = 0;
+        for (int i = 0; i < L.nl; ++i) maxblk = std::max(maxblk, L.R[i] * s);
+        ReduceArgs ra{L, ip.rl.get(), ip.ri.get(), ip.rf.get(), ip.rc.get(), s};
+        k_ml_reduce<<<dim3(unsigned(cdiv(maxblk, 256)), unsigned(ip.nred)), 256, 0, c.stream>>>(ra);
+        HG_LAUNCH();
+        ++c.launches;
+    }
+    return out;
 }
 
 }  // namespace hg

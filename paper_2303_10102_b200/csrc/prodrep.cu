@@ -147,6 +147,24 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
                 dot_panels(n, cw, corr.Cv->get() + i64(c0) * n, n, Y.get(), n, out, true);
             }
         }
+        int rmax = 0;
+        for (int l = 1; l <= tau; ++l) rmax = std::max(rmax, h.Rl(l));
+        if (rmax <= 16) {  // skinny base: all levels' projections in one pass over Cv / Cu
+            std::vector<int> W(static_cast<size_t>(tau));
+            for (int l = 1; l <= tau; ++l)
+                W[static_cast<size_t>(l - 1)] = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
+            auto P = hodlr_project(h, corr.Cv->get(), n, corr.sumC, true, W);
+            auto Q = hodlr_project(h, corr.Cu->get(), n, corr.sumC, false, W);
+            for (int l = 1; l <= tau; ++l) {
+                const int R = h.Rl(l), w = W[static_cast<size_t>(l - 1)];
+                if (!R || !w) continue;
+                const Partition& p = t.part(l);
+                for (int rep = 0; rep < int(alpha); ++rep)  // alpha in {1, 2}
+                    seg_xor_dot(p.nseg(), 1, P[static_cast<size_t>(l - 1)]->get(), Q[static_cast<size_t>(l - 1)]->get(),
+                                i64(R) * corr.sumC, R, R, w, out, true);
+            }
+            return;
+        }
         for (int l = 1; l <= tau; ++l) {
             const int R = h.Rl(l);
             const int W = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
