@@ -5,6 +5,7 @@
 
 #include "../../include/hodlrgp_b200.h"
 #include "api.cuh"
+#include "fit.cuh"
 #include "prof.cuh"
 
 using namespace hg;
@@ -173,6 +174,45 @@ hg_status hg_sketch_sampler(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_
         panel_axpby(n, int(cols), 1.0, src, n, 0.0, o.p, o.ld);
         o.finish();
         sync();
+    });
+}
+
+hg_status hg_fit_mle(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
+                     const double* ybar, int p, const int* transforms, const double* theta0, int max_iter,
+                     double rel_tol, double* theta_hat, double* fisher, double* ci, int* ci_valid, int* iterations,
+                     int* converged, char* status, int status_len, double* loglik_trace, double* grad_norm_trace,
+                     double* theta_trace, int trace_cap, int* trace_len, uint64_t* columns, double* seconds) {
+    return capi_guard(ctx, [&] {
+        const i64 n = o->o->dim();
+        std::vector<double> r(y, y + n);
+        if (ybar)
+            for (i64 i = 0; i < n; ++i) r[static_cast<size_t>(i)] -= ybar[i];
+        DVec rd;
+        rd.upload(r);
+        FitReport rep = fit_mle(*o->o, get_tree(n, tau), k, seed, rd.get(), std::vector<int>(transforms, transforms + p),
+                                std::vector<double>(theta0, theta0 + p), max_iter, rel_tol);
+        for (int i = 0; i < p; ++i) theta_hat[i] = rep.theta_hat[static_cast<size_t>(i)];
+        for (int i = 0; i < p * p; ++i) fisher[i] = rep.fisher.empty() ? NAN : rep.fisher[static_cast<size_t>(i)];
+        for (int i = 0; i < 2 * p; ++i) ci[i] = rep.ci.empty() ? NAN : rep.ci[static_cast<size_t>(i)];
+        *ci_valid = rep.ci_valid ? 1 : 0;
+        *iterations = rep.iterations;
+        *converged = rep.converged ? 1 : 0;
+        if (status && status_len > 0) {
+            const size_t m = std::min(rep.status.size(), size_t(status_len - 1));
+            std::copy(rep.status.begin(), rep.status.begin() + m, status);
+            status[m] = 0;
+        }
+        const int len = int(std::min<size_t>(rep.loglik_trace.size(), size_t(std::max(trace_cap, 0))));
+        for (int t = 0; t < len; ++t) {
+            if (loglik_trace) loglik_trace[t] = rep.loglik_trace[static_cast<size_t>(t)];
+            if (grad_norm_trace) grad_norm_trace[t] = rep.grad_norm_trace[static_cast<size_t>(t)];
+            if (theta_trace)
+                for (int i = 0; i < p; ++i) theta_trace[i + t * p] = rep.theta_trace[static_cast<size_t>(t)][static_cast<size_t>(i)];
+        }
+        *trace_len = len;
+        columns[0] = rep.apply_columns;
+        columns[1] = rep.derivative_columns;
+        *seconds = rep.seconds;
     });
 }
 

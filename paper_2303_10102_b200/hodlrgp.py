@@ -63,6 +63,9 @@ _SIGS = {
     "hg_oracle_dense": (C.c_int, [vp, i64, dp, C.c_int, dp, C.POINTER(vp)]),
     "hg_oracle_matern": (C.c_int, [vp, i64, dp, C.c_int, dbl, dbl, dbl, C.c_int, C.POINTER(vp)]),
     "hg_oracle_cokriging": (C.c_int, [vp, i64, dbl, dbl, dbl, dbl, C.POINTER(vp)]),
+    "hg_fit_mle": (C.c_int, [vp, vp, C.c_int, i64, C.c_uint64, dp, dp, C.c_int, ip, dp, C.c_int, dbl, dp, dp, dp,
+                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_int, dp, dp, dp,
+                             C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(dbl)]),
     "hg_sketch_sampler": (C.c_int, [vp, i64, C.c_int, i64, C.c_uint64, C.c_int, C.c_void_p, i64, C.c_int]),
     "hg_randomized_range": (C.c_int, [vp, C.c_void_p, i64, i64, i64, C.c_void_p, i64, dp, ip, C.POINTER(i64), C.c_int]),
     "hg_diff_qr": (C.c_int, [vp, C.c_void_p, i64, C.c_void_p, i64, dp, i64, i64, C.c_void_p, i64, C.c_void_p, i64, dp,
@@ -651,6 +654,36 @@ def grid_kd_order(nside, leaf):
     coords = np.stack([(ix + 0.5) / nside, (iy + 0.5) / nside], axis=1)
     _, inv, _ = build_kd_ordering(coords, 1, 2)
     return inv, ClusterTree(n, tree_depth(n, leaf, 2 * leaf))
+
+
+# ---------------------------------------------------------------- fit
+POSITIVE, CORRELATION, UNBOUNDED = 0, 1, 2  # ParamTransform (mle.hpp:37-41)
+
+
+def fit_mle(oracle, tree, k, seed, y, theta0, transforms=None, ybar=None, max_iter=100, rel_tol=1e-6, trace_cap=256):
+    """mle.cpp:188-322 on the device path -> FitReport as a dict."""
+    tau = tree.tau if hasattr(tree, "tau") else int(tree)
+    y = _vec(y)
+    yb = _vec(ybar) if ybar is not None else None
+    th0 = np.ascontiguousarray(theta0, dtype=np.float64)
+    p = len(th0)
+    tr = np.ascontiguousarray(transforms if transforms is not None else [POSITIVE] * p, dtype=np.int32)
+    theta_hat, fisher, ci = np.zeros(p), np.zeros((p, p), order="F"), np.zeros((p, 2), order="F")
+    ci_valid, iters, conv, tlen = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    status = C.create_string_buffer(64)
+    llt, gnt = np.zeros(trace_cap), np.zeros(trace_cap)
+    tht = np.zeros((p, trace_cap), order="F")
+    cols = (C.c_uint64 * 2)()
+    secs = C.c_double()
+    _check(lib().hg_fit_mle(oracle.ctx.ptr, oracle.ptr, tau, k, seed, _d(y), _d(yb) if yb is not None else None, p,
+                            tr.ctypes.data_as(ip), _d(th0), max_iter, rel_tol, _d(theta_hat), _d(fisher), _d(ci),
+                            C.byref(ci_valid), C.byref(iters), C.byref(conv), status, 64, _d(llt), _d(gnt), _d(tht),
+                            trace_cap, C.byref(tlen), cols, C.byref(secs)))
+    m = tlen.value
+    return {"theta_hat": theta_hat, "fisher": fisher, "ci": ci, "ci_valid": bool(ci_valid.value),
+            "iterations": iters.value, "converged": bool(conv.value), "status": status.value.decode(),
+            "loglik_trace": llt[:m].copy(), "grad_norm_trace": gnt[:m].copy(), "theta_trace": tht[:, :m].T.copy(),
+            "apply_columns": cols[0], "derivative_columns": cols[1], "seconds": secs.value}
 
 
 # ------------------------------------------------------------ sketching

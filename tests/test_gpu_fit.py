@@ -1,0 +1,52 @@
+"""fit_mle (mle.cpp:188-322) on the device path vs its CPU restatement
+(oracle/fit.py over the CPU oracle pipeline) on a C1-like problem.
+
+Both drivers follow the same BFGS trajectory; per-iteration objective values
+agree to 1e-8 relative (each evaluation differs only by the pipeline's
+rounding, see test_gpu_build_mle.py), the optimum to 1e-5 and the Fisher
+matrix at the optimum to 1e-6 normwise."""
+import numpy as np
+import pytest
+
+from oracle import fit as F
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2303_10102_b200 import hodlrgp
+
+    return hodlrgp
+
+
+def test_fit_mle_matches_cpu_restatement(H):
+    n, leaf, k, seed = 1024, 64, 16, 0
+    x = np.sort(np.random.default_rng(0).uniform(size=n))
+    tau = O.tree_depth(n, leaf, 2 * leaf)
+    K = O.CovOracle.matern(x, 3, 1.0, 0.2, 1e-4, False).apply(np.eye(n))
+    y = np.linalg.cholesky(K) @ O.randn(n, 1, 1)[:, 0]
+    theta0 = np.array([1.5, 0.1])
+    cpu = F.fit_mle(*F.matern_evaluators(x, 3, 1e-4, tau, k, seed, y), theta0, [F.POSITIVE, F.POSITIVE])
+    dev = H.fit_mle(H.MaternOracle(x, 3, 1.5, 0.1, 1e-4, True), H.ClusterTree(n, tau), k, seed, y, theta0)
+    assert dev["status"] == cpu["status"] and dev["converged"] == cpu["converged"], (dev["status"], cpu["status"])
+    m = min(len(dev["loglik_trace"]), len(cpu["loglik_trace"]))
+    assert m >= 3 and abs(len(dev["loglik_trace"]) - len(cpu["loglik_trace"])) <= 1
+    ll0, ll1 = np.array(cpu["loglik_trace"][:m]), dev["loglik_trace"][:m]
+    assert np.max(np.abs(ll1 - ll0) / np.abs(ll0)) <= 1e-8
+    assert np.max(np.abs(dev["theta_hat"] - cpu["theta_hat"]) / cpu["theta_hat"]) <= 1e-5
+    assert np.linalg.norm(dev["fisher"] - cpu["fisher"]) <= 1e-6 * np.linalg.norm(cpu["fisher"])
+    assert dev["ci_valid"] and cpu["ci_valid"]
+    assert np.allclose(dev["ci"], cpu["ci"], rtol=1e-5)
+    # the optimum brackets the generating parameters within a few standard errors
+    assert np.all(dev["ci"][:, 0] < dev["theta_hat"]) and np.all(dev["theta_hat"] < dev["ci"][:, 1])
+    assert dev["apply_columns"] > 0 and dev["derivative_columns"] > 0
+
+
+def test_confidence_intervals_formula(H):
+    th = np.array([1.0, 0.2])
+    fi = np.array([[50.0, -10.0], [-10.0, 400.0]])
+    ci, ok = F.confidence_intervals(th, fi)
+    hw = 1.959964 * np.sqrt(np.diag(np.linalg.inv(fi)))
+    assert ok and np.allclose(ci[:, 0], th - hw) and np.allclose(ci[:, 1], th + hw)
