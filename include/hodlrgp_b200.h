@@ -28,6 +28,7 @@ typedef enum {
     HG_ELOGIC = 4,    /* std::logic_error     (lower() on symmetric storage) */
     HG_ENOMEM = 5,
     HG_ECUDA = 6,
+    HG_EIO = 7,       /* std::runtime_error of io.cpp (missing/truncated sidecar, bad manifest) */
     HG_EOTHER = 9
 } hg_status;
 
@@ -77,6 +78,15 @@ hg_status hg_hodlr_import(hg_ctx_t ctx, int64_t n, int tau, int symmetric, const
 hg_status hg_hodlr_info(hg_hodlr_t h, int64_t* n, int* tau, int* symmetric, int* R);
 int64_t hg_hodlr_export_size(hg_hodlr_t h);
 hg_status hg_hodlr_export(hg_ctx_t ctx, hg_hodlr_t h, double* flat, int* ranks_up, int* ranks_lo);
+/* write_hodlr_debug / read_hodlr_debug — io.hpp:33-36, io.cpp:171-275. JSON
+ * manifest `dir/name.json` (n, depth, symmetric, per-level upper[/lower]
+ * blocks with node, rows, cols, rank, left/right sidecar names; leaves with
+ * index, rows, file) + row-major little-endian float64 sidecars. The writer
+ * creates `dir`; the reader rebuilds the matrix on the context's device.
+ * Manifest ranges must match ClusterTree(n, depth) (HG_EINVAL); missing or
+ * short files give HG_EIO. */
+hg_status hg_write_hodlr_debug(hg_ctx_t ctx, const char* dir, const char* name, hg_hodlr_t h);
+hg_status hg_read_hodlr_debug(hg_ctx_t ctx, const char* dir, const char* name, hg_hodlr_t* out);
 hg_status hg_hodlr_copy(hg_ctx_t ctx, hg_hodlr_t h, hg_hodlr_t* out);
 hg_status hg_hodlr_free(hg_hodlr_t h);
 /* make_asymmetric — hodlr_matrix.cpp:187-196 */

@@ -7,6 +7,7 @@
 
 #include "../../include/hodlrgp_b200.h"
 #include "api.cuh"
+#include "io.cuh"
 
 using namespace hg;
 
@@ -57,6 +58,9 @@ hg_status guard(hg_ctx_t ctx, F&& f) {
     } catch (const CudaError& e) {
         g_err = e.what();
         return HG_ECUDA;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return HG_EIO;
     } catch (const std::bad_alloc& e) {
         g_err = e.what();
         return HG_ENOMEM;
@@ -243,6 +247,20 @@ int64_t hg_hodlr_export_size(hg_hodlr_t h) { return int64_t(h->h.export_size());
 
 hg_status hg_hodlr_export(hg_ctx_t ctx, hg_hodlr_t h, double* flat, int* ranks_up, int* ranks_lo) {
     return guard(ctx, [&] { h->h.export_panels(flat, ranks_up, ranks_lo); });
+}
+
+hg_status hg_write_hodlr_debug(hg_ctx_t ctx, const char* dir, const char* name, hg_hodlr_t h) {
+    return guard(ctx, [&] {
+        if (!dir || !name || !h) throw std::invalid_argument("write_hodlr_debug: null argument");
+        write_hodlr_debug(dir, name, h->h);
+    });
+}
+
+hg_status hg_read_hodlr_debug(hg_ctx_t ctx, const char* dir, const char* name, hg_hodlr_t* out) {
+    return guard(ctx, [&] {
+        if (!dir || !name || !out) throw std::invalid_argument("read_hodlr_debug: null argument");
+        *out = new hg_hodlr_s{read_hodlr_debug(dir, name)};
+    });
 }
 
 hg_status hg_hodlr_copy(hg_ctx_t ctx, hg_hodlr_t h, hg_hodlr_t* out) {

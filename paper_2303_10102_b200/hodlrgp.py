@@ -41,6 +41,8 @@ _SIGS = {
     "hg_hodlr_export_size": (i64, [vp]),
     "hg_hodlr_export": (C.c_int, [vp, vp, dp, ip, ip]),
     "hg_hodlr_copy": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "hg_write_hodlr_debug": (C.c_int, [vp, C.c_char_p, C.c_char_p, vp]),
+    "hg_read_hodlr_debug": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.POINTER(vp)]),
     "hg_hodlr_free": (C.c_int, [vp]),
     "hg_hodlr_make_asymmetric": (C.c_int, [vp, vp]),
     "hg_hodlr_matvec": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, C.c_int]),
@@ -155,6 +157,11 @@ class HodlrError(RuntimeError):
         self.code = code
 
 
+class SerializationError(HodlrError):
+    """std::runtime_error of io.cpp: unreadable / malformed manifest, missing
+    or truncated sidecar (HG_EIO)."""
+
+
 class NotPositiveDefinite(HodlrError):
     """factorization.hpp:14-16"""
 
@@ -173,6 +180,8 @@ def _check(rc):
         raise TypeError(msg)
     if rc == 5:
         raise MemoryError(msg)
+    if rc == 7:
+        raise SerializationError(rc, msg)
     raise HodlrError(rc, msg)
 
 
@@ -427,6 +436,21 @@ def trace_product(a, b):
 
 
 # --------------------------------------------------------- factorization
+def write_hodlr_debug(dir, name, h):
+    """io.hpp:33-36 / io.cpp:171-233: JSON manifest `dir/name.json` plus
+    row-major little-endian float64 sidecars (creates `dir`)."""
+    _check(lib().hg_write_hodlr_debug(h.ctx.ptr, os.fsencode(dir), os.fsencode(name), h.ptr))
+
+
+def read_hodlr_debug(dir, name, ctx=None):
+    """io.cpp:235-275: rebuild the HodlrMatrix a manifest describes (device
+    resident on `ctx`)."""
+    ctx = ctx or context()
+    h = vp()
+    _check(lib().hg_read_hodlr_debug(ctx.ptr, os.fsencode(dir), os.fsencode(name), C.byref(h)))
+    return HodlrMatrix(h, ctx)
+
+
 class HodlrFactorization:
     """factorization.hpp:45-78"""
 
