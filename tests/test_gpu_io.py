@@ -166,3 +166,22 @@ def test_c1_full_against_golden(H):
     br = H.build_hodlr_with_derivatives(do, H.ClusterTree(g["n"], g["depth"]), g["k"], g["seed"])
     dec, ref = br.decisions(), np.asarray(g["decisions"])
     assert dec.shape == ref.shape and int((dec != ref).any(axis=1).sum()) <= 1
+
+
+def test_bench_csv_schema(tmp_path):  # tools/hodlr_gp.cpp:378-477
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, os.path.join(root, "scripts", "bench_csv.py"), str(tmp_path), "--sizes", "1024",
+                    "--repeats", "2"], check=True, capture_output=True)
+    lines = open(tmp_path / "bench.csv").read().splitlines()
+    assert lines[0] == "n,k,metric,value,repeat"
+    rows = [r.split(",") for r in lines[1:]]
+    metrics = [r[2] for r in rows if r[4] == "0"]
+    assert metrics == ["build_seconds", "build_apply_columns", "build_apply_columns_expected", "build_deriv_seconds",
+                       "deriv_apply_columns", "deriv_derivative_columns", "factorize_seconds", "loglik_seconds",
+                       "score_seconds", "fisher_seconds", "eval_seconds_parallel"]
+    val = {r[2]: float(r[3]) for r in rows if r[4] == "1"}
+    assert val["build_apply_columns"] == val["build_apply_columns_expected"]  # 2 k tau + b
+    assert all(r[0] == "1024" and r[1] == "24" for r in rows)
