@@ -216,20 +216,31 @@ hg_status hg_mle_iteration(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint
  * X, with y/B/X at `loc` (HG_HOST: copied in/out inside the call; HG_DEVICE:
  * device pointers). times[5] = build_deriv, factorize, loglik+solves, score,
  * fisher seconds (device events). */
-/* fit_mle (mle.cpp:188-322; FitOptions{max_iter, rel_tol}, dense = false):
+/* fit_mle (mle.cpp:188-322; FitOptions{max_iter, rel_tol, dense}):
  * BFGS on transformed parameters (transforms[i]: 0 positive theta = exp(u),
  * 1 correlation theta = tanh(u), 2 unbounded) with a backtracking line
  * search; every evaluation is a device build + factorization with the
- * SketchPlan of `seed` fixed for the whole fit. Outputs FitReport: theta_hat
+ * SketchPlan of `seed` fixed for the whole fit (dense != 0: the exact dense
+ * device evaluation of mle.cpp:131-169 instead). Outputs FitReport: theta_hat
  * (p), fisher (p x p, NaN if not SPD), ci (p x 2: lo, hi), status ("converged",
  * "max_iter", "line_search_failed", "not_positive_definite[_at_start]"),
  * traces (up to trace_cap iterations; theta_trace p x cap), columns[2] =
  * oracle apply / derivative columns, seconds. ybar may be NULL (zero mean). */
 hg_status hg_fit_mle(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
                      const double* ybar, int p, const int* transforms, const double* theta0, int max_iter,
-                     double rel_tol, double* theta_hat, double* fisher, double* ci, int* ci_valid, int* iterations,
+                     double rel_tol, int dense, double* theta_hat, double* fisher, double* ci, int* ci_valid, int* iterations,
                      int* converged, char* status, int status_len, double* loglik_trace, double* grad_norm_trace,
                      double* theta_trace, int trace_cap, int* trace_len, uint64_t* columns, double* seconds);
+/* dense_exact — mle.cpp:345-380 (n <= 2^13, HG_ELENGTH above): exact dense
+ * log-likelihood, score and Fisher (p x p column-major) of the oracle at its
+ * current parameters; y, ybar host (ybar may be NULL). */
+hg_status hg_dense_exact(hg_ctx_t ctx, hg_oracle_t o, const double* y, const double* ybar, double* loglik,
+                         double* score, double* fisher);
+/* accuracy_metrics — mle.cpp:382-403: out = {eps_L, eps_S, eps_I, eta_g, eta_I};
+ * HG_EINVAL when the exact Fisher matrix is not SPD. Host arithmetic. */
+hg_status hg_accuracy_metrics(int p, double loglik, const double* score_exact, const double* fisher_exact,
+                              double loglik_approx, const double* score_approx, const double* fisher_approx,
+                              double* out);
 hg_status hg_mle_evaluate(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
                           const double* B, int64_t nrhs, double* X, int loc, double* loglik, double* score,
                           double* fisher, double* times);

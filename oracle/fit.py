@@ -144,3 +144,65 @@ def matern_evaluators(x, nu2, nugget, tau, k, seed, y):
             O.set_solve_association(False)
 
     return value, value_grad, fisher_at
+
+
+LOG2PI = 1.8378770664093454836
+
+
+def dense_exact(K, dKs, r):
+    """mle.cpp:345-380 in numpy: exact log-likelihood, score and Fisher of the
+    dense covariance K with derivatives dKs at residual r = y - ybar."""
+    n = K.shape[0]
+    L = np.linalg.cholesky(K)
+    w = np.linalg.solve(L.T, np.linalg.solve(L, r))
+    ld = 2.0 * np.sum(np.log(np.diag(L)))
+    ll = -0.5 * n * LOG2PI - 0.5 * ld - 0.5 * r @ w
+    M = [np.linalg.solve(L.T, np.linalg.solve(L, kj)) for kj in dKs]
+    s = np.array([-0.5 * np.trace(m) + 0.5 * w @ (kj @ w) for m, kj in zip(M, dKs)])
+    p = len(dKs)
+    f = np.array([[0.5 * np.sum(M[i] * M[j].T) for j in range(p)] for i in range(p)])
+    return ll, s, f
+
+
+def accuracy_metrics(ll, se, fe, lla, sa, fa):
+    """mle.cpp:382-403 in numpy."""
+    se, sa, fe, fa = map(np.asarray, (se, sa, fe, fa))
+    ds, di = se - sa, fe - fa
+    L = np.linalg.cholesky(fe)  # raises LinAlgError when not SPD (the reference: invalid_argument)
+    inv_e = np.linalg.inv(fe)
+    inv_a = np.linalg.inv(fa)
+    return {"eps_L": abs(ll - lla) / abs(ll), "eps_S": np.linalg.norm(ds) / np.linalg.norm(se),
+            "eps_I": np.linalg.norm(di) / np.linalg.norm(fe),
+            "eta_g": float(np.sqrt(ds @ np.linalg.solve(L.T, np.linalg.solve(L, ds)))),
+            "eta_I": float(np.sqrt(max(0.0, np.trace(di @ (inv_e - inv_a)))))}
+
+
+def dense_evaluators(kfun, r):
+    """value / value_grad / fisher_at of fit_mle's dense path (mle.cpp:128-175)
+    for kfun(theta) -> (K, [dK_j])."""
+
+    def value(theta):
+        K, _ = kfun(theta)
+        try:
+            L = np.linalg.cholesky(K)
+        except np.linalg.LinAlgError as e:
+            raise O.NotPositiveDefinite(1, "dense covariance") from e
+        w = np.linalg.solve(L.T, np.linalg.solve(L, r))
+        return -(-0.5 * len(r) * LOG2PI - np.sum(np.log(np.diag(L))) - 0.5 * r @ w)
+
+    def value_grad(theta):
+        K, dKs = kfun(theta)
+        try:
+            L = np.linalg.cholesky(K)
+        except np.linalg.LinAlgError as e:
+            raise O.NotPositiveDefinite(1, "dense covariance") from e
+        w = np.linalg.solve(L.T, np.linalg.solve(L, r))
+        kinv = np.linalg.solve(L.T, np.linalg.solve(L, np.eye(len(r))))
+        g = np.array([-(-0.5 * np.sum(kinv * kj) + 0.5 * w @ (kj @ w)) for kj in dKs])
+        return -(-0.5 * len(r) * LOG2PI - np.sum(np.log(np.diag(L))) - 0.5 * r @ w), g
+
+    def fisher_at(theta):
+        K, dKs = kfun(theta)
+        return dense_exact(K, dKs, r)[2]
+
+    return value, value_grad, fisher_at

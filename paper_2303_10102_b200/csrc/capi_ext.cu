@@ -5,6 +5,7 @@
 
 #include "../../include/hodlrgp_b200.h"
 #include "api.cuh"
+#include "dense.cuh"
 #include "fit.cuh"
 #include "prof.cuh"
 
@@ -179,7 +180,7 @@ hg_status hg_sketch_sampler(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_
 
 hg_status hg_fit_mle(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t seed, const double* y,
                      const double* ybar, int p, const int* transforms, const double* theta0, int max_iter,
-                     double rel_tol, double* theta_hat, double* fisher, double* ci, int* ci_valid, int* iterations,
+                     double rel_tol, int dense, double* theta_hat, double* fisher, double* ci, int* ci_valid, int* iterations,
                      int* converged, char* status, int status_len, double* loglik_trace, double* grad_norm_trace,
                      double* theta_trace, int trace_cap, int* trace_len, uint64_t* columns, double* seconds) {
     return capi_guard(ctx, [&] {
@@ -190,7 +191,7 @@ hg_status hg_fit_mle(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t s
         DVec rd;
         rd.upload(r);
         FitReport rep = fit_mle(*o->o, get_tree(n, tau), k, seed, rd.get(), std::vector<int>(transforms, transforms + p),
-                                std::vector<double>(theta0, theta0 + p), max_iter, rel_tol);
+                                std::vector<double>(theta0, theta0 + p), max_iter, rel_tol, dense != 0);
         for (int i = 0; i < p; ++i) theta_hat[i] = rep.theta_hat[static_cast<size_t>(i)];
         for (int i = 0; i < p * p; ++i) fisher[i] = rep.fisher.empty() ? NAN : rep.fisher[static_cast<size_t>(i)];
         for (int i = 0; i < 2 * p; ++i) ci[i] = rep.ci.empty() ? NAN : rep.ci[static_cast<size_t>(i)];
@@ -213,6 +214,39 @@ hg_status hg_fit_mle(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint64_t s
         columns[0] = rep.apply_columns;
         columns[1] = rep.derivative_columns;
         *seconds = rep.seconds;
+    });
+}
+
+hg_status hg_dense_exact(hg_ctx_t ctx, hg_oracle_t o, const double* y, const double* ybar, double* loglik,
+                         double* score_out, double* fisher) {
+    return capi_guard(ctx, [&] {
+        const i64 n = o->o->dim();
+        std::vector<double> r(y, y + n);
+        if (ybar)
+            for (i64 i = 0; i < n; ++i) r[static_cast<size_t>(i)] -= ybar[i];
+        DVec rd;
+        rd.upload(r);
+        DenseExact d = dense_exact(*o->o, rd.get());
+        *loglik = d.loglik;
+        std::copy(d.score.begin(), d.score.end(), score_out);
+        std::copy(d.fisher.begin(), d.fisher.end(), fisher);
+    });
+}
+
+hg_status hg_accuracy_metrics(int p, double loglik, const double* score_exact, const double* fisher_exact,
+                              double loglik_approx, const double* score_approx, const double* fisher_approx,
+                              double* out) {
+    return capi_guard(nullptr, [&] {
+        const size_t pp = static_cast<size_t>(p) * static_cast<size_t>(p);
+        AccuracyMetrics m = accuracy_metrics(
+            loglik, std::vector<double>(score_exact, score_exact + p), std::vector<double>(fisher_exact, fisher_exact + pp),
+            loglik_approx, std::vector<double>(score_approx, score_approx + p),
+            std::vector<double>(fisher_approx, fisher_approx + pp));
+        out[0] = m.eps_L;
+        out[1] = m.eps_S;
+        out[2] = m.eps_I;
+        out[3] = m.eta_g;
+        out[4] = m.eta_I;
     });
 }
 

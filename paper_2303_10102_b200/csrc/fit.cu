@@ -10,6 +10,7 @@
 
 #include "api.cuh"
 #include "fit.cuh"
+#include "dense.cuh"
 
 namespace hg {
 
@@ -123,15 +124,18 @@ struct Evaluator {
     i64 k;
     const DSketchPlan& plan;
     const double* r;  // device residual y - ybar
+    bool dense;       // FitOptions::dense (mle.cpp:131-169)
 
     double value(const Vec& th) const {  // -loglik (line-search probes)
         o.set_parameters(th.data(), int(th.size()));
+        if (dense) return dense_objective(o, r);
         DBuildResult br = build(o, tree, k, plan, false);
         DFactor f = factorize(br.h, 1);
         return -log_likelihood(f, r);
     }
     double value_grad(const Vec& th, Vec& grad) const {  // accepted iterates
         o.set_parameters(th.data(), int(th.size()));
+        if (dense) return dense_objective_grad(o, r, grad);
         DBuildResult br = build(o, tree, k, plan, true);
         DFactor f = factorize(br.h, 1);
         const double ll = log_likelihood(f, r);
@@ -144,6 +148,7 @@ struct Evaluator {
     }
     Vec fisher_at(const Vec& th) const {
         o.set_parameters(th.data(), int(th.size()));
+        if (dense) return dense_exact(o, r).fisher;
         DBuildResult br = build(o, tree, k, plan, true);
         DFactor f = factorize(br.h, 1);
         std::vector<const DHodlr*> d;
@@ -179,14 +184,15 @@ ConfidenceIntervals confidence_intervals(const Vec& theta, const Vec& fisher) {
 }
 
 FitReport fit_mle(DOracle& o, DTreeP tree, i64 k, std::uint64_t seed, const double* r_dev,
-                  const std::vector<int>& transforms, const Vec& theta0, int max_iter, double rel_tol) {
+                  const std::vector<int>& transforms, const Vec& theta0, int max_iter, double rel_tol,
+                  bool dense) {
     const auto t0 = std::chrono::steady_clock::now();
     const int p = int(theta0.size());
     if (int(transforms.size()) != p) throw std::invalid_argument("fit_mle: transforms must match parameter count");
     if (p != o.num_params()) throw std::invalid_argument("fit_mle: theta0 must have one entry per oracle parameter");
     o.reset_counters();
     DSketchPlanP plan = get_plan(tree, k, seed);
-    Evaluator ev{o, tree, k, *plan, r_dev};
+    Evaluator ev{o, tree, k, *plan, r_dev, dense};
     FitReport rep;
     rep.status = "max_iter";
     Vec u = from_natural(theta0, transforms), theta = theta0, grad_theta(static_cast<size_t>(p));

@@ -35,9 +35,10 @@ ConfidenceIntervals confidence_intervals(const std::vector<double>& theta, const
 /// mle.cpp:188-322: BFGS on the transformed parameters, backtracking line
 /// search (Armijo 1e-4, <= 20 halvings, non-SPD iterates rejected), score-test
 /// stationarity on a failed search, Fisher and 95% intervals at the optimum.
-/// r_dev = y - ybar on the device.
+/// r_dev = y - ybar on the device. dense: FitOptions::dense, the exact dense
+/// evaluation path (dense.cu) instead of the HODLR build.
 FitReport fit_mle(DOracle& o, DTreeP tree, i64 k, std::uint64_t seed, const double* r_dev,
                   const std::vector<int>& transforms, const std::vector<double>& theta0, int max_iter,
-                  double rel_tol);
+                  double rel_tol, bool dense = false);
 
 }  // namespace hg

@@ -65,7 +65,7 @@ _SIGS = {
     "hg_oracle_dense": (C.c_int, [vp, i64, dp, C.c_int, dp, C.POINTER(vp)]),
     "hg_oracle_matern": (C.c_int, [vp, i64, dp, C.c_int, dbl, dbl, dbl, C.c_int, C.POINTER(vp)]),
     "hg_oracle_cokriging": (C.c_int, [vp, i64, dbl, dbl, dbl, dbl, C.POINTER(vp)]),
-    "hg_fit_mle": (C.c_int, [vp, vp, C.c_int, i64, C.c_uint64, dp, dp, C.c_int, ip, dp, C.c_int, dbl, dp, dp, dp,
+    "hg_fit_mle": (C.c_int, [vp, vp, C.c_int, i64, C.c_uint64, dp, dp, C.c_int, ip, dp, C.c_int, dbl, C.c_int, dp, dp, dp,
                              C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_int, dp, dp, dp,
                              C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(dbl)]),
     "hg_sketch_sampler": (C.c_int, [vp, i64, C.c_int, i64, C.c_uint64, C.c_int, C.c_void_p, i64, C.c_int]),
@@ -89,6 +89,8 @@ _SIGS = {
     "hg_fisher_information": (C.c_int, [vp, vp, C.POINTER(vp), C.c_int, dp]),
     "hg_mle_iteration": (C.c_int, [vp, vp, C.c_int, i64, u64, dp, dp, dp, dp, dp]),
     "hg_mle_evaluate": (C.c_int, [vp, vp, C.c_int, i64, u64, vp, vp, i64, vp, C.c_int, dp, dp, dp, dp]),
+    "hg_dense_exact": (C.c_int, [vp, vp, dp, dp, dp, dp, dp]),
+    "hg_accuracy_metrics": (C.c_int, [C.c_int, dbl, dp, dp, dbl, dp, dp, dp]),
     "hg_prof_enable": (None, [C.c_int]),
     "hg_prof_read": (C.c_int, [C.c_int, dp, dp, dp, lp]),
 }
@@ -684,8 +686,10 @@ def grid_kd_order(nside, leaf):
 POSITIVE, CORRELATION, UNBOUNDED = 0, 1, 2  # ParamTransform (mle.hpp:37-41)
 
 
-def fit_mle(oracle, tree, k, seed, y, theta0, transforms=None, ybar=None, max_iter=100, rel_tol=1e-6, trace_cap=256):
-    """mle.cpp:188-322 on the device path -> FitReport as a dict."""
+def fit_mle(oracle, tree, k, seed, y, theta0, transforms=None, ybar=None, max_iter=100, rel_tol=1e-6, trace_cap=256,
+            dense=False):
+    """mle.cpp:188-322 on the device path -> FitReport as a dict. dense:
+    FitOptions::dense (exact dense device evaluation, small n)."""
     tau = tree.tau if hasattr(tree, "tau") else int(tree)
     y = _vec(y)
     yb = _vec(ybar) if ybar is not None else None
@@ -700,7 +704,7 @@ def fit_mle(oracle, tree, k, seed, y, theta0, transforms=None, ybar=None, max_it
     cols = (C.c_uint64 * 2)()
     secs = C.c_double()
     _check(lib().hg_fit_mle(oracle.ctx.ptr, oracle.ptr, tau, k, seed, _d(y), _d(yb) if yb is not None else None, p,
-                            tr.ctypes.data_as(ip), _d(th0), max_iter, rel_tol, _d(theta_hat), _d(fisher), _d(ci),
+                            tr.ctypes.data_as(ip), _d(th0), max_iter, rel_tol, int(dense), _d(theta_hat), _d(fisher), _d(ci),
                             C.byref(ci_valid), C.byref(iters), C.byref(conv), status, 64, _d(llt), _d(gnt), _d(tht),
                             trace_cap, C.byref(tlen), cols, C.byref(secs)))
     m = tlen.value
@@ -708,6 +712,27 @@ def fit_mle(oracle, tree, k, seed, y, theta0, transforms=None, ybar=None, max_it
             "iterations": iters.value, "converged": bool(conv.value), "status": status.value.decode(),
             "loglik_trace": llt[:m].copy(), "grad_norm_trace": gnt[:m].copy(), "theta_trace": tht[:, :m].T.copy(),
             "apply_columns": cols[0], "derivative_columns": cols[1], "seconds": secs.value}
+
+
+def dense_exact(oracle, y, ybar=None):
+    """mle.cpp:345-380 on the device (n <= 2^13) -> (loglik, score, fisher)."""
+    y = _vec(y)
+    yb = _vec(ybar) if ybar is not None else None
+    p = oracle.p
+    ll = C.c_double()
+    s, f = np.zeros(p), np.zeros((p, p), order="F")
+    _check(lib().hg_dense_exact(oracle.ctx.ptr, oracle.ptr, _d(y), _d(yb) if yb is not None else None, C.byref(ll),
+                                _d(s), _d(f)))
+    return ll.value, s, f
+
+
+def accuracy_metrics(loglik, score_exact, fisher_exact, loglik_approx, score_approx, fisher_approx):
+    """mle.cpp:382-403 -> dict(eps_L, eps_S, eps_I, eta_g, eta_I)."""
+    se, sa = _vec(score_exact), _vec(score_approx)
+    fe, fa = _f(fisher_exact), _f(fisher_approx)
+    out = np.zeros(5)
+    _check(lib().hg_accuracy_metrics(len(se), loglik, _d(se), _d(fe), loglik_approx, _d(sa), _d(fa), _d(out)))
+    return dict(zip(["eps_L", "eps_S", "eps_I", "eta_g", "eta_I"], out.tolist()))
 
 
 # ------------------------------------------------------------ sketching
