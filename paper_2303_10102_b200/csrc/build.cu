@@ -639,7 +639,7 @@ void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, i
     ZeroRows z;
     if (zparity >= 0 && lmax + 1 <= H.tau()) {
         const Partition& pz = H.tree->part(lmax + 1);
-        z = ZeroRows{pz.dbounds(), pz.nseg(), zparity};
+        z = ZeroRows{pz.dbounds(), pz.nseg(), zparity, lmax + 1};  // Y is read on the sampler's zero rows only
     }
     hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
 }

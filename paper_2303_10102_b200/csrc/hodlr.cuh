@@ -62,9 +62,14 @@ struct DHodlr {
 /// the depth-`depth` segments whose index parity equals `parity` (the sketch
 /// samplers of the build are zero on one child of every level-l node); the
 /// projections skip chunks that lie entirely in such a segment.
+/// With out_depth >= 0 the caller also declares that it reads Y only on
+/// those same rows (the depth-out_depth segments of that parity): the peel
+/// samples blocks of the still-unknown level from rows where its sampler is
+/// zero, so the level updates skip every other row tile.
 struct ZeroRows {
     const int* bounds = nullptr;  // partition bounds of that depth (device)
     int nseg = 0, parity = 0;
+    int out_depth = -1;
 };
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,

@@ -124,6 +124,7 @@ struct UpdArgs {
     i64 ldy;
     int s;
     double alpha, beta;
+    int out_depth, out_parity;  // rows read by the caller (ZeroRows::out_depth)
 };
 
 /// A operand: rows of the update panels, K = concatenated level columns.
@@ -175,6 +176,7 @@ template <int TBN>
 __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
     extern __shared__ double smem[];
     __shared__ MlLevels L;
+    if (g.out_depth >= 0 && ((g.items[blockIdx.x].seg >> (g.tau - g.out_depth)) & 1) != g.out_parity) return;
     for (int i = threadIdx.x; i < int(sizeof(MlLevels) / sizeof(int)); i += blockDim.x)
         reinterpret_cast<int*>(&L)[i] = reinterpret_cast<const int*>(&g.L)[i];
     __syncthreads();
@@ -362,7 +364,8 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         ++c.launches;
     }
     const TileList& tl = t.leaves().tiles(BM);
-    UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta};
+    UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta,
+               zero.bounds && zero.out_depth <= t.tau() ? zero.out_depth : -1, zero.parity};
     // the update's N tile may differ from the projection's (its M is always 64)
     const int tbn_u = tile::tile_for_n(s, BM), tiles_nu = (s + tbn_u - 1) / tbn_u;
     with_tile(tbn_u, [&](auto TN) {
