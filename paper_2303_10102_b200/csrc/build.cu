@@ -635,11 +635,13 @@ void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double*
 /// -1: no structure (leaf sampler).
 void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y, int zparity) {
     const i64 n = H.n();
-    o.apply(j, X, n, s, Y, n);
     ZeroRows z;
     if (zparity >= 0 && lmax + 1 <= H.tau()) {
         const Partition& pz = H.tree->part(lmax + 1);
         z = ZeroRows{pz.dbounds(), pz.nseg(), zparity, lmax + 1};  // Y is read on the sampler's zero rows only
+        o.apply_masked(j, X, n, s, Y, n, z);
+    } else {
+        o.apply(j, X, n, s, Y, n);
     }
     hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
 }

@@ -5,6 +5,7 @@
 // problem's M and N, K staged 16 at a time through a cp.async pipeline.
 // Split-K partials are reduced in a fixed order so every result is bitwise
 // reproducible run to run.
+#include <cstdlib>
 #include "kernels.cuh"
 #include "prof.cuh"
 #include "tile.cuh"
@@ -120,6 +121,82 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
         if (n >= g.w || m >= it.rows) return;
         g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + g.beta * y;
     });
+}
+
+/// Streaming variant for short K (k <= 48) and wide w: the CTA keeps its
+/// 64-row X tile in shared memory and walks a run of column tiles, staging
+/// the next T and Y tiles with cp.async while the current one is multiplied.
+/// The op is HBM-bound (AI = k/8 flop/B), so the loop keeps a full tile of
+/// Y in flight per CTA instead of paying the load latency once per tile.
+constexpr int SNN_KT = 3;  // k <= 48
+
+template <int TBN>
+struct SnnLayout {
+    static constexpr int XE = SNN_KT * tile::stage_elems(BM);   // X, all k slices
+    static constexpr int TE = SNN_KT * tile::stage_elems(TBN);  // T tile, all k slices
+    static constexpr int YLD = BM + 4;
+    static constexpr int YE = TBN * YLD;                        // Y tile, m-contiguous
+    static constexpr int BYTES = int(sizeof(double)) * (XE + 2 * (TE + YE));
+};
+
+template <int TBN>
+__global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int groups) {
+    using Lay = SnnLayout<TBN>;
+    extern __shared__ double smem[];
+    double* Xs = smem;
+    double* Ts = smem + Lay::XE;           // 2 buffers of TE
+    double* Ys = Ts + 2 * Lay::TE;         // 2 buffers of YE
+    const WorkItem it = g.items[blockIdx.x / groups];
+    const int grp = blockIdx.x % groups;
+    const int ntiles = cdiv_d(g.w, TBN), per = cdiv_d(ntiles, groups);
+    const int j0 = grp * per, j1 = min(ntiles, j0 + per);
+    if (j0 >= j1) return;
+    const double* Tb = g.T + i64((it.seg >> g.map.shift) ^ g.map.xr) * g.map.mult * g.tstride +
+                       i64(g.map.add) * g.tstride + ((it.seg & 1) ? g.map.row_odd : g.map.row_even);
+    const int kt_n = cdiv_d(g.k, BK);
+    tile::LoadMCT<BM> lx{g.X + it.row0, g.ldx, it.rows, g.k};
+    for (int kt = 0; kt < kt_n; ++kt) lx.issue(Xs + kt * tile::stage_elems(BM), kt);
+    const bool ld_y = g.beta != 0.0;
+    auto issue = [&](int j, int buf) {
+        const int n0 = j * TBN;
+        tile::LoadKCT<TBN> lt{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
+        double* T = Ts + buf * Lay::TE;
+        for (int kt = 0; kt < kt_n; ++kt) lt.issue(T + kt * tile::stage_elems(TBN), kt);
+        if (ld_y) {
+            double* Y = Ys + buf * Lay::YE;
+            const double* yb = g.Y + it.row0 + i64(n0) * g.ldy;
+#pragma unroll
+            for (int q = 0; q < BM * TBN / THREADS; ++q) {
+                const int e = threadIdx.x + THREADS * q, m = e % BM, c = e / BM;
+                const bool v = m < it.rows && n0 + c < g.w;
+                tile::cp_async8(Y + c * Lay::YLD + m, v ? yb + m + i64(c) * g.ldy : yb, v);
+            }
+        }
+    };
+    issue(j0, 0);
+    tile::cp_commit();
+    for (int j = j0; j < j1; ++j) {
+        const int buf = (j - j0) & 1;
+        tile::cp_wait<0>();
+        __syncthreads();  // tile j (and X) landed; every warp is done with the other buffer
+        if (j + 1 < j1) issue(j + 1, buf ^ 1);
+        tile::cp_commit();
+        typename tile::Shape<BM, TBN>::Acc acc;
+        acc.zero();
+        const double* T = Ts + buf * Lay::TE;
+        for (int kt = 0; kt < kt_n; ++kt)
+            tile::mma_stage<false, true, BM, TBN>(Xs + kt * tile::stage_elems(BM), T + kt * tile::stage_elems(TBN),
+                                                  acc);
+        const double* Y = Ys + buf * Lay::YE;
+        const int n0 = j * TBN;
+        tile::for_each_slot<BM, TBN>(acc, [&](double& v, int m, int ni) {
+            const int n = n0 + ni;
+            if (n >= g.w || m >= it.rows) return;
+            const double y = ld_y ? g.beta * Y[ni * Lay::YLD + m] : 0.0;
+            g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + y;
+        });
+    }
+    tile::cp_wait<0>();
 }
 
 // ----------------------------------------------------------------- leaf_mm
@@ -374,6 +451,19 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_NN, 2.0 * rows * k * w, 8.0 * rows * (k + (beta != 0.0 ? 2.0 : 1.0) * w));
     if (prof_enabled()) prof.key(prof_tag("nn nseg=%d k=%d w=%d", p.nseg(), k, w));
+    // Short K over many columns: the streaming kernel (X tile resident).
+    if (k <= BK * SNN_KT && w >= 128 && p.max_seg() > 96 && !std::getenv("HG_NO_NN_STREAM")) {
+        constexpr int TN = 32;
+        const TileList& tl = p.tiles(BM);
+        SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
+        const int want = 4 * c.num_sms, ntiles = cdiv(w, TN);
+        const int groups = std::max(1, std::min(ntiles / 4, cdiv(want, tl.count)));
+        attr_once<k_seg_nn_stream<TN>>(SnnLayout<TN>::BYTES);
+        k_seg_nn_stream<TN><<<unsigned(tl.count * groups), THREADS, SnnLayout<TN>::BYTES, c.stream>>>(g, groups);
+        HG_LAUNCH();
+        ++c.launches;
+        return;
+    }
     // Row tile: 64, or one tile per segment when every segment is short
     // (e.g. the 2R-row node blocks of the capacitance solves).
     const int tbm = p.max_seg() <= 96 ? std::max(48, tile::tile_for(p.max_seg())) : BM;

@@ -58,19 +58,6 @@ struct DHodlr {
 /// [lmin, lmax] (and the leaves when with_leaves). lmin = d+1 gives the
 /// block-diagonal of all depth-d sub-blocks at once (sub_matvec,
 /// hodlr_matrix.cpp:228-265); lmin = 1 is the full matvec (:198-222).
-/// Optional input-support hint for hodlr_apply: X is zero on every row of
-/// the depth-`depth` segments whose index parity equals `parity` (the sketch
-/// samplers of the build are zero on one child of every level-l node); the
-/// projections skip chunks that lie entirely in such a segment.
-/// With out_depth >= 0 the caller also declares that it reads Y only on
-/// those same rows (the depth-out_depth segments of that parity): the peel
-/// samples blocks of the still-unknown level from rows where its sampler is
-/// zero, so the level updates skip every other row tile.
-struct ZeroRows {
-    const int* bounds = nullptr;  // partition bounds of that depth (device)
-    int nseg = 0, parity = 0;
-    int out_depth = -1;
-};
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
                  bool with_leaves, bool transpose, double beta = 0.0, double alpha = 1.0, ZeroRows zero = {});

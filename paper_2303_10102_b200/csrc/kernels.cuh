@@ -66,6 +66,20 @@ void leaf_trace(const Partition& leaves, const double* L, i64 lstride, int ldl, 
 void leaf_pair_dot(const Partition& leaves, const double* A, const double* B, i64 lstride, int ldl, double* out,
                    bool accumulate);
 
+/// Optional input-support hint for hodlr_apply / DOracle::apply_masked: X is zero on every row of
+/// the depth-`depth` segments whose index parity equals `parity` (the sketch
+/// samplers of the build are zero on one child of every level-l node); the
+/// projections skip chunks that lie entirely in such a segment.
+/// With out_depth >= 0 the caller also declares that it reads Y only on
+/// those same rows (the depth-out_depth segments of that parity): the peel
+/// samples blocks of the still-unknown level from rows where its sampler is
+/// zero, so the level updates skip every other row tile.
+struct ZeroRows {
+    const int* bounds = nullptr;  // partition bounds of that depth (device)
+    int nseg = 0, parity = 0;
+    int out_depth = -1;
+};
+
 /// Final host read of a device scalar (synchronizes the stream).
 double read_scalar(const double* d);
 

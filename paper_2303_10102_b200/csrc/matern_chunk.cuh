@@ -52,7 +52,27 @@ struct MatChunkArgs {
     double* Lb;  // [col][super][4] super-chunk backward moments
     double* Ff;  // [col][super][4] forward state at the super-chunk's first point
     double* Fb;  // [col][super][4] backward state at the super-chunk's last point
+    // ZeroRows hint (peeling): V is zero on the segments of parity zpar of the
+    // partition zb; with zout the caller reads Y only on those segments.
+    const int* zb;
+    int znseg, zpar, zout;
 };
+
+/// Parity of the single segment of zb holding rows [a, b), or -1 when the
+/// run straddles a boundary (or no hint is given).
+__device__ __forceinline__ int mc_run_parity(const MatChunkArgs& g, int a, int b) {
+    if (!g.zb) return -1;
+    auto seg = [&](int r) {
+        int lo = 0, hi = g.znseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (g.zb[mid] <= r) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    const int s0 = seg(a), s1 = seg(b - 1);
+    return s0 == s1 ? (s0 & 1) : -1;
+}
 
 __device__ __forceinline__ double mc_first(const MatChunkArgs& g, int row0) { return g.x[row0]; }
 __device__ __forceinline__ double mc_last(const MatChunkArgs& g, int row_end) { return g.x[min(g.n, row_end) - 1]; }
@@ -189,6 +209,15 @@ __global__ void __launch_bounds__(MC_TILE) k_mat_moments(MatChunkArgs g) {
     const McTables T = mc_tables(Mb + MC_NCH * MC_COLS * 4);
     const int S = blockIdx.x, r0 = S * MC_TILE;
     const int nchk = min(MC_NCH, (g.n - r0 + MC_ROWS - 1) / MC_ROWS);
+    if (mc_run_parity(g, r0, min(g.n, r0 + MC_TILE)) == g.zpar) {  // V == 0 here: zero moments
+        for (int col = threadIdx.x; col < g.s; col += blockDim.x)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                g.Lf[(i64(col) * g.nsup + S) * 4 + q] = 0.0;
+                g.Lb[(i64(col) * g.nsup + S) * 4 + q] = 0.0;
+            }
+        return;
+    }
     mc_fill_tables(g, r0, T);
     for (int c0 = 0; c0 < g.s; c0 += MC_COLS) {
         mc_stage(g, Vs, r0, c0);
@@ -312,6 +341,10 @@ __global__ void __launch_bounds__(MC_TILE) k_mat_apply(MatChunkArgs g) {
     const McTables T = mc_tables(Mb + MC_NCH * MC_COLS * 4);
     const int S = blockIdx.x, r0 = S * MC_TILE;
     const int nchk = min(MC_NCH, (g.n - r0 + MC_ROWS - 1) / MC_ROWS);
+    if (g.zout) {  // rows the caller never reads
+        const int par = mc_run_parity(g, r0, min(g.n, r0 + MC_TILE));
+        if (par >= 0 && par != g.zpar) return;
+    }
     mc_fill_tables(g, r0, T);
     // per-row kernel values of the own chunk and the state coefficients (once)
     const int i = r0 + threadIdx.x, cl = threadIdx.x >> 5;

@@ -138,6 +138,14 @@ public:
 
 protected:
     void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {
+        run(j, V, ldv, s, Y, ldy, ZeroRows{});
+    }
+    void do_apply_masked(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy, const ZeroRows& z) const override {
+        run(j, V, ldv, s, Y, ldy, z);
+    }
+
+private:
+    void run(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy, const ZeroRows& z) const {
         if (j >= 2) throw std::invalid_argument("apply_derivative: parameter index");
         const Poly P = matern_poly(nu2_, j, sigma2_, ell_);
         auto& c = current();
@@ -162,7 +170,8 @@ protected:
         const size_t msz = static_cast<size_t>(nsup) * static_cast<size_t>(s) * 4;
         DVec Lf(msz), Lb(msz), Ff(msz), Fb(msz);
         MatChunkArgs g{x_.get(), int(n_), nsup, s, P.nt, P.lambda, {P.c[0], P.c[1], P.c[2], P.c[3]},
-                       j < 0 ? nugget_ : 0.0, V, ldv, Y, ldy, Lf.get(), Lb.get(), Ff.get(), Fb.get()};
+                       j < 0 ? nugget_ : 0.0, V, ldv, Y, ldy, Lf.get(), Lb.get(), Ff.get(), Fb.get(),
+                       z.bounds, z.nseg, z.parity, z.out_depth >= 0 ? 1 : 0};
         static bool attr = false;
         if (!attr) {
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_mat_moments),
@@ -181,7 +190,6 @@ protected:
         c.launches += 3;
     }
 
-private:
     int nu2_;
     double sigma2_, ell_, nugget_;
     bool scan_;

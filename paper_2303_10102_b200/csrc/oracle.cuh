@@ -22,6 +22,14 @@ public:
         (j < 0 ? apply_cols_ : deriv_cols_).fetch_add(std::uint64_t(s), std::memory_order_relaxed);
         do_apply(j, V, ldv, s, Y, ldy);
     }
+    /// apply under a ZeroRows hint: V is zero on the depth segments of parity
+    /// z.parity and, with z.out_depth >= 0, the caller reads Y only on those
+    /// rows. Oracles may skip the work this makes dead; default = apply.
+    void apply_masked(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy, const ZeroRows& z) const {
+        if (s <= 0) return;
+        (j < 0 ? apply_cols_ : deriv_cols_).fetch_add(std::uint64_t(s), std::memory_order_relaxed);
+        do_apply_masked(j, V, ldv, s, Y, ldy, z);
+    }
     std::uint64_t apply_columns() const { return apply_cols_.load(); }
     std::uint64_t derivative_columns() const { return deriv_cols_.load(); }
     void reset_counters() const {
@@ -31,6 +39,9 @@ public:
 
 protected:
     virtual void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const = 0;
+    virtual void do_apply_masked(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy, const ZeroRows&) const {
+        do_apply(j, V, ldv, s, Y, ldy);
+    }
     i64 n_;
     int p_;
 

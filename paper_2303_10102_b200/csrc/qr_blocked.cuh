@@ -87,7 +87,10 @@ __device__ __forceinline__ void qb_build_t(const QbSmem& S, int ld, int nr, int 
 }
 
 /// W1 = V^T C (16 x wc) with V the explicit panel (nr rows) and C = Cg[0:nr, 0:wc]
-/// (global, ldc); DMMA over 8x8 tiles, K split in two chains.
+/// (global, ldc); DMMA over 8x8 tiles. C is read straight from global
+/// memory (L2), so the rows are streamed in groups of 32 with the next
+/// group's 8 loads issued before the current group's 8 DMMAs (one L2
+/// latency per group instead of one per DMMA).
 __device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const double* Cg, i64 ldc, int wc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
@@ -97,19 +100,25 @@ __device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const d
         const int a0 = (tl & 1) * 8, j0 = (tl >> 1) * 8;
         double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
         const bool colok = j0 + g8 < wc;
-        const double* Bc = Cg + i64(j0 + g8) * ldc;
-        int k4 = 0;
-        for (; k4 + 8 <= K; k4 += 8) {
-            const int r0 = k4 + t4, r1 = k4 + 4 + t4;
-            const double b0 = (colok && r0 < nr) ? Bc[r0] : 0.0;
-            const double b1 = (colok && r1 < nr) ? Bc[r1] : 0.0;
-            tile::dmma(c0, S.P[r0 + (a0 + g8) * ld], b0);
-            tile::dmma(c1, S.P[r1 + (a0 + g8) * ld], b1);
-        }
-        if (k4 < K) {
-            const int r0 = k4 + t4;
-            const double b0 = (colok && r0 < nr) ? Bc[r0] : 0.0;
-            tile::dmma(c0, S.P[r0 + (a0 + g8) * ld], b0);
+        const double* Bc = Cg + i64(colok ? j0 + g8 : 0) * ldc;
+        const double* Vc = S.P + (a0 + g8) * ld;
+        double nb[8];
+        auto fetch = [&](int k0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int r = k0 + 4 * q + t4;
+                nb[q] = (colok && r < nr) ? Bc[r] : 0.0;
+            }
+        };
+        fetch(0);
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            double b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) b[q] = nb[q];
+            if (k0 + 32 < K) fetch(k0 + 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (k0 + 4 * q < K) tile::dmma((q & 1) ? c1 : c0, Vc[k0 + 4 * q + t4], b[q]);
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -119,20 +128,27 @@ __device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const d
     }
 }
 
-/// Cg[0:nr, 0:wc] -= V W2 (W2 16 x wc in shared memory).
+/// Cg[0:nr, 0:wc] -= V W2 (W2 16 x wc in shared memory); the next tile's C
+/// values are loaded before the current tile's DMMAs.
 __device__ __forceinline__ void qb_c_minus_vw(const QbSmem& S, int ld, int nr, double* Cg, i64 ldc, int wc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
-    const int nrt = (nr + 7) / 8, nct = (wc + 7) / 8;
-    for (int tl = warp; tl < nrt * nct; tl += nwarps) {
-        const int r0 = (tl % nrt) * 8, j0 = (tl / nrt) * 8;
-        const int r = r0 + g8;
-        double acc[2];
+    const int nrt = (nr + 7) / 8, nct = (wc + 7) / 8, ntl = nrt * nct;
+    double nxt[2] = {0.0, 0.0};
+    auto fetch = [&](int tl) {
+        const int r = (tl % nrt) * 8 + g8, j0 = (tl / nrt) * 8;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int j = j0 + 2 * t4 + e;
-            acc[e] = (r < nr && j < wc) ? Cg[r + i64(j) * ldc] : 0.0;
+            nxt[e] = (r < nr && j < wc) ? Cg[r + i64(j) * ldc] : 0.0;
         }
+    };
+    if (warp < ntl) fetch(warp);
+    for (int tl = warp; tl < ntl; tl += nwarps) {
+        const int r0 = (tl % nrt) * 8, j0 = (tl / nrt) * 8;
+        const int r = r0 + g8;
+        double acc[2] = {nxt[0], nxt[1]};
+        if (tl + nwarps < ntl) fetch(tl + nwarps);
 #pragma unroll
         for (int kk = 0; kk < QB_NB; kk += 4) {
             const int jb = j0 + g8;
