@@ -325,7 +325,11 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         L.T[i] = Tbuf[static_cast<size_t>(i)].get();
         L.ws[i] = Wbuf[static_cast<size_t>(i)].get();
         L.ncol[i] = s;
-        flops += 4.0 * double(n) * R * s;
+        // algorithmic flops: the projection reads only the nonzero half of X
+        // under a ZeroRows hint, the update writes only the rows the caller reads
+        const double f = 2.0 * double(n) * R * s;
+        flops += zero.bounds ? 0.5 * f : f;
+        flops += (zero.bounds && zero.out_depth >= 0) ? 0.5 * f : f;
         bytes += 16.0 * double(n) * R;
     }
     ProfScope prof(PROF_SEG_TN, flops, bytes);
