@@ -87,21 +87,28 @@ __device__ __forceinline__ void qb_build_t(const QbSmem& S, int ld, int nr, int 
 }
 
 /// W1 = V^T C (16 x wc) with V the explicit panel (nr rows) and C = Cg[0:nr, 0:wc]
-/// (global, ldc); DMMA over 8x8 tiles. C is read straight from global
-/// memory (L2), so the rows are streamed in groups of 32 with the next
-/// group's 8 loads issued before the current group's 8 DMMAs (one L2
-/// latency per group instead of one per DMMA).
+/// (global, ldc); DMMA over 8-column blocks of C, both 8-row halves of W1 per
+/// warp (the C loads are shared). C is read straight from global memory (L2):
+/// rows are streamed in groups of 32 with the next group's 8 loads issued
+/// before the current group's 16 DMMAs.
 __device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const double* Cg, i64 ldc, int wc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
-    const int nct = (wc + 7) / 8, ntiles = 2 * nct;
+    const int nct = (wc + 7) / 8;
     const int K = (nr + 3) & ~3;
-    for (int tl = warp; tl < ntiles; tl += nwarps) {
-        const int a0 = (tl & 1) * 8, j0 = (tl >> 1) * 8;
-        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    // few column blocks: one W1 half per warp (more warps busy); many: both
+    // halves per warp (each C value loaded once)
+    const bool split = nct < nwarps;
+    const int ntask = split ? 2 * nct : nct;
+    for (int task = warp; task < ntask; task += nwarps) {
+        const int jt = split ? task >> 1 : task;
+        const int h0 = split ? (task & 1) : 0, h1 = split ? h0 : 1;
+        const int j0 = jt * 8;
+        double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
         const bool colok = j0 + g8 < wc;
         const double* Bc = Cg + i64(colok ? j0 + g8 : 0) * ldc;
-        const double* Vc = S.P + (a0 + g8) * ld;
+        const double* V0 = S.P + (8 * h0 + g8) * ld;
+        const double* V1 = S.P + (8 * h1 + g8) * ld;
         double nb[8];
         auto fetch = [&](int k0) {
 #pragma unroll
@@ -118,52 +125,87 @@ __device__ __forceinline__ void qb_vt_c(const QbSmem& S, int ld, int nr, const d
             if (k0 + 32 < K) fetch(k0 + 32);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (k0 + 4 * q < K) tile::dmma((q & 1) ? c1 : c0, Vc[k0 + 4 * q + t4], b[q]);
+                if (k0 + 4 * q < K) {
+                    const int r = k0 + 4 * q + t4;
+                    tile::dmma((q & 1) ? c1 : c0, V0[r], b[q]);
+                    if (!split) tile::dmma((q & 1) ? d1 : d0, V1[r], b[q]);
+                }
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int j = j0 + 2 * t4 + e;
-            if (j < wc) S.W1[(a0 + g8) + QB_NB * j] = c0[e] + c1[e];
+            if (j < wc) {
+                S.W1[(8 * h0 + g8) + QB_NB * j] = c0[e] + c1[e];
+                if (!split) S.W1[(8 + g8) + QB_NB * j] = d0[e] + d1[e];
+            }
         }
     }
 }
 
-/// Cg[0:nr, 0:wc] -= V W2 (W2 16 x wc in shared memory); the next tile's C
-/// values are loaded before the current tile's DMMAs.
-__device__ __forceinline__ void qb_c_minus_vw(const QbSmem& S, int ld, int nr, double* Cg, i64 ldc, int wc) {
+/// Cg[0:nr, 0:wc] -= V W2 (W2 16 x wc in shared memory). Each warp takes 4
+/// 8x8 tiles per step (8 independent loads in flight) and loads the next 4
+/// tiles' C values before the current tiles' DMMAs.
+template <int TB>
+__device__ __forceinline__ void qb_c_minus_vw_t(const QbSmem& S, int ld, int nr, double* Cg, i64 ldc, int wc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
     const int nrt = (nr + 7) / 8, nct = (wc + 7) / 8, ntl = nrt * nct;
-    double nxt[2] = {0.0, 0.0};
-    auto fetch = [&](int tl) {
-        const int r = (tl % nrt) * 8 + g8, j0 = (tl / nrt) * 8;
+    double nxt[TB][2];
+    auto fetch = [&](int base) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int j = j0 + 2 * t4 + e;
-            nxt[e] = (r < nr && j < wc) ? Cg[r + i64(j) * ldc] : 0.0;
+        for (int u = 0; u < TB; ++u) {
+            const int tl = base + u;
+            const int r = (tl % nrt) * 8 + g8, j0 = (tl / nrt) * 8;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = j0 + 2 * t4 + e;
+                nxt[u][e] = (tl < ntl && r < nr && j < wc) ? Cg[r + i64(j) * ldc] : 0.0;
+            }
         }
     };
-    if (warp < ntl) fetch(warp);
-    for (int tl = warp; tl < ntl; tl += nwarps) {
-        const int r0 = (tl % nrt) * 8, j0 = (tl / nrt) * 8;
-        const int r = r0 + g8;
-        double acc[2] = {nxt[0], nxt[1]};
-        if (tl + nwarps < ntl) fetch(tl + nwarps);
+    const int stride = nwarps * TB;
+    if (warp * TB < ntl) fetch(warp * TB);
+    for (int base = warp * TB; base < ntl; base += stride) {
+        double acc[TB][2];
 #pragma unroll
-        for (int kk = 0; kk < QB_NB; kk += 4) {
+        for (int u = 0; u < TB; ++u) acc[u][0] = nxt[u][0], acc[u][1] = nxt[u][1];
+        if (base + stride < ntl) fetch(base + stride);
+#pragma unroll
+        for (int u = 0; u < TB; ++u) {
+            const int tl = base + u;
+            if (tl >= ntl) break;
+            const int r0 = (tl % nrt) * 8, j0 = (tl / nrt) * 8;
             const int jb = j0 + g8;
-            const double b = jb < wc ? S.W2[(kk + t4) + QB_NB * jb] : 0.0;
-            tile::dmma(acc, -S.P[r0 + g8 + (kk + t4) * ld], b);
+#pragma unroll
+            for (int kk = 0; kk < QB_NB; kk += 4) {
+                const double b = jb < wc ? S.W2[(kk + t4) + QB_NB * jb] : 0.0;
+                tile::dmma(acc[u], -S.P[r0 + g8 + (kk + t4) * ld], b);
+            }
         }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int j = j0 + 2 * t4 + e;
-            if (r < nr && j < wc) Cg[r + i64(j) * ldc] = acc[e];
+        for (int u = 0; u < TB; ++u) {
+            const int tl = base + u;
+            if (tl >= ntl) break;
+            const int r = (tl % nrt) * 8 + g8, j0 = (tl / nrt) * 8;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = j0 + 2 * t4 + e;
+                if (r < nr && j < wc) Cg[r + i64(j) * ldc] = acc[u][e];
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(QB_THREADS) k_qr_blocked(const QrDesc* descs, int w) {
+/// Batch 4 tiles per warp step only when every warp gets several batches.
+__device__ __forceinline__ void qb_c_minus_vw(const QbSmem& S, int ld, int nr, double* Cg, i64 ldc, int wc) {
+    const int ntl = ((nr + 7) / 8) * ((wc + 7) / 8);
+    if (ntl >= 4 * 2 * int(blockDim.x >> 5))
+        qb_c_minus_vw_t<4>(S, ld, nr, Cg, ldc, wc);
+    else
+        qb_c_minus_vw_t<1>(S, ld, nr, Cg, ldc, wc);
+}
+
+__global__ void __launch_bounds__(QB_THREADS, 3) k_qr_blocked(const QrDesc* descs, int w) {
     extern __shared__ double sm[];
     __shared__ double s_tau, s_div;
     __shared__ int s_zero;
@@ -253,7 +295,7 @@ __global__ void __launch_bounds__(QB_THREADS) k_qr_blocked(const QrDesc* descs, 
         }
 }
 
-__global__ void __launch_bounds__(QB_THREADS) k_form_q_blocked(const QfDesc* descs, int w, int qcols) {
+__global__ void __launch_bounds__(QB_THREADS, 3) k_form_q_blocked(const QfDesc* descs, int w, int qcols) {
     extern __shared__ double sm[];
     const QfDesc d = descs[blockIdx.x];
     const int rows = d.rows, ld = qb_ld(rows);
