@@ -247,9 +247,9 @@ hg_status hg_mle_evaluate(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint6
 
 /* ---------------------------------------------------- kernel-level ledger */
 /* Per kernel class (seg_tn, seg_nn, leaf_mm, leaf_solve, leaf_factor, cap_lu,
- * cap_solve, qr, form_q, oracle, reduce, other): device ms from CUDA events
+ * cap_solve, qr, form_q, oracle, reduce, other, hmatvec): device ms from CUDA events
  * around each launch, algorithmic flops and bytes, launch count. Off by
- * default; returns the number of classes written (<= 12). */
+ * default; returns the number of classes written (<= 13). */
 void hg_prof_enable(int on);
 int hg_prof_read(int reset, double* ms, double* flops, double* bytes, int64_t* launches);
 

@@ -62,6 +62,11 @@ struct DHodlr {
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
                  bool with_leaves, bool transpose, double beta = 0.0, double alpha = 1.0, ZeroRows zero = {});
 
+/// Streaming path of hodlr_apply for s <= 4 (hmatvec.cu): returns false when
+/// the call is outside its domain (transpose, zero hints, ranks > 256).
+bool hodlr_apply_narrow(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
+                        bool with_leaves, bool transpose, double beta, double alpha, ZeroRows zero);
+
 /// Projections of all levels at once: T_l[s] = P_l[s]^T X[s] (P = U when
 /// transpose, else V) for the first ncol[l-1] columns of X, as nseg_l
 /// blocks of R_l x s (ld R_l). Entries of missing levels are null.

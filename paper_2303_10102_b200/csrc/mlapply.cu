@@ -285,6 +285,7 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
                  bool with_leaves, bool transpose, double beta, double alpha, ZeroRows zero) {
     if (s <= 0) return;
+    if (hodlr_apply_narrow(h, X, ldx, s, Y, ldy, lmin, lmax, with_leaves, transpose, beta, alpha, zero)) return;
     const i64 n = h.n();
     const DTree& t = *h.tree;
     if (with_leaves && !h.leaves_zero) {

@@ -23,6 +23,7 @@ enum ProfCat {
     PROF_ORACLE,
     PROF_REDUCE,
     PROF_OTHER,
+    PROF_MATVEC,
     PROF_NCAT
 };
 

@@ -96,7 +96,7 @@ _SIGS = {
 }
 
 PROF_CATEGORIES = ["seg_tn", "seg_nn", "leaf_mm", "leaf_solve", "leaf_factor", "cap_lu", "cap_solve", "qr",
-                   "form_q", "oracle", "reduce", "other"]
+                   "form_q", "oracle", "reduce", "other", "hmatvec"]
 
 
 def prof_enable(on=True):

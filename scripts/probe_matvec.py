@@ -16,7 +16,7 @@ t0 = time.time()
 h = H.HodlrMatrix.random_spd(H.ClusterTree(n, tau), k, 7, ctx=ctx)
 ctx.synchronize()
 print("random_spd host gen", time.time() - t0, flush=True)
-for s in (64, 1):
+for s in [int(a) for a in sys.argv[1:]] or (64, 4, 2, 1):
     X = torch.randn(s, n, dtype=torch.float64, device="cuda").T
     Y = torch.empty(s, n, dtype=torch.float64, device="cuda").T
     for _ in range(3):
