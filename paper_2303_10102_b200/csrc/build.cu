@@ -266,10 +266,8 @@ __global__ void k_mask_cols(const int* bounds, int odd, const int* wj, int wtot,
     const int c = 2 * j + odd;
     const int lo = bounds[c], m = bounds[c + 1] - lo;
     const int w0 = wj[j];
-    for (int e = threadIdx.x; e < m * (wtot - w0); e += blockDim.x) {
-        const int r = e % m, col = w0 + e / m;
-        P[i64(lo + r) + i64(col) * ldp] = 0.0;
-    }
+    for (int col = w0; col < wtot; ++col)
+        for (int r = threadIdx.x; r < m; r += blockDim.x) P[i64(lo + r) + i64(col) * ldp] = 0.0;
 }
 
 /// diff_qr restricted to the in-span rotation (sketch.cpp:78-111,245-268):

@@ -263,11 +263,16 @@ __global__ void k_parity_scale(const WorkItem* items, int w, const double* X, i6
                                double* Y, i64 ldy, double beta) {
     const WorkItem it = items[blockIdx.x];
     const double a = (it.seg & 1) ? ao : ae;
-    for (int e = threadIdx.x; e < it.rows * w; e += blockDim.x) {
-        const int r = e % it.rows, j = e / it.rows;
-        const i64 row = i64(it.row0) + r;
-        double* y = Y + row + i64(j) * ldy;
-        *y = a * X[row + i64(j) * ldx] + (beta != 0.0 ? beta * *y : 0.0);
+    if (int(threadIdx.x) >= it.rows) return;  // one thread per row (items have <= blockDim rows)
+    const i64 row = i64(it.row0) + threadIdx.x;
+    const double* x = X + row;
+    double* y = Y + row;
+    if (beta != 0.0) {
+#pragma unroll 4
+        for (int j = 0; j < w; ++j) y[i64(j) * ldy] = fma(a, x[i64(j) * ldx], beta * y[i64(j) * ldy]);
+    } else {
+#pragma unroll 4
+        for (int j = 0; j < w; ++j) y[i64(j) * ldy] = a * x[i64(j) * ldx];
     }
 }
 
@@ -363,6 +368,37 @@ struct LeafPair {
         return A[base + c + i64(r) * ldl] * B[base + r + i64(c) * ldl];
     }
 };
+
+constexpr int DOT_BLOCKS = 4 * 148;  // fixed => deterministic
+constexpr int DOT_CH = 4096;          // elements per chunk (16 per thread)
+
+/// Chunks of DOT_CH elements of every segment, block b taking chunks b, b +
+/// DOT_BLOCKS, ... (16 independent loads of each operand per thread in
+/// flight, four accumulators); one partial per block.
+__global__ void __launch_bounds__(256) k_seg_dot(int nseg, int xr, const double* A, i64 gsa, const double* B,
+                                                 i64 gsb, i64 len, double* partial) {
+    const i64 cps = (len + DOT_CH - 1) / DOT_CH, nchunk = cps * nseg;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (i64 c = blockIdx.x; c < nchunk; c += gridDim.x) {
+        const int s = int(c / cps);
+        const i64 e0 = (c - i64(s) * cps) * DOT_CH;
+        const double* a = A + i64(s) * gsa + e0;
+        const double* b = B + i64(s ^ xr) * gsb + e0;
+        const int m = int(min(i64(DOT_CH), len - e0));
+        double av[16], bv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int e = int(threadIdx.x) + k * 256;
+            av[k] = e < m ? __ldcs(a + e) : 0.0;
+            bv[k] = e < m ? __ldcs(b + e) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k & 3] = fma(av[k], bv[k], acc[k & 3]);
+    }
+    double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    v = block_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+}
 
 template <class F>
 __global__ void k_reduce_partial(F f, i64 total, double* partial) {
@@ -533,18 +569,27 @@ void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 l
     ++c.launches;
 }
 
-void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate) {
-    if (n <= 0 || w <= 0) {
-        if (!accumulate) HG_CUDA(cudaMemsetAsync(out, 0, sizeof(double), current().stream));
+void seg_dot(int nseg, int xr, const double* A, i64 gsa, const double* B, i64 gsb, i64 len, double* out,
+             bool accumulate) {
+    auto& c = current();
+    if (nseg <= 0 || len <= 0) {
+        if (!accumulate) HG_CUDA(cudaMemsetAsync(out, 0, sizeof(double), c.stream));
         return;
     }
-    auto& c = current();
-    DVec partial(RED_BLOCKS);
-    k_dot_panels<<<RED_BLOCKS, 256, 0, c.stream>>>(n, w, A, lda, B, ldb, partial.get());
+    ProfScope prof(PROF_REDUCE, 2.0 * double(nseg) * len, 16.0 * double(nseg) * len);
+    DVec partial(DOT_BLOCKS);
+    k_seg_dot<<<DOT_BLOCKS, 256, 0, c.stream>>>(nseg, xr, A, gsa, B, gsb, len, partial.get());
     HG_LAUNCH();
-    k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), RED_BLOCKS, out, accumulate ? 1 : 0);
+    k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), DOT_BLOCKS, out, accumulate ? 1 : 0);
     HG_LAUNCH();
     c.launches += 2;
+}
+
+void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate) {
+    if (lda == n && ldb == n)
+        seg_dot(1, 0, A, 0, B, 0, n * w, out, accumulate);
+    else
+        seg_dot(w, 0, A, lda, B, ldb, n, out, accumulate);
 }
 
 void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, int rb, const double* H, i64 hs,
@@ -554,6 +599,10 @@ void seg_pair_dot(int nseg, int xr, const double* G, i64 gs, int ldg, int ra, in
 
 void seg_xor_dot(int nseg, int xr, const double* G, const double* H, i64 gs, int ld, int ra, int rc, double* out,
                  bool accumulate) {
+    if (ld == ra) {  // contiguous ra x rc blocks
+        seg_dot(nseg, xr, G, gs, H, gs, i64(ra) * rc, out, accumulate);
+        return;
+    }
     reduce(XorDot{ra, rc, xr, ld, gs, G, H}, i64(nseg) * ra * rc, out, accumulate);
 }
 

@@ -260,8 +260,9 @@ void hodlr_trace_product(const DHodlr& a, const DHodlr& b, double* out, bool acc
         const Partition& p = a.tree->part(l);
         DVec G(static_cast<size_t>(p.nseg()) * static_cast<size_t>(RA) * static_cast<size_t>(RB)), H(static_cast<size_t>(p.nseg()) * static_cast<size_t>(RA) * static_cast<size_t>(RB));
         seg_tn(p, b.Vl(l), n, RB, a.Ul(l), n, RA, G.get(), i64(RB) * RA, RB);
-        seg_tn(p, a.Vl(l), n, RA, b.Ul(l), n, RB, H.get(), i64(RA) * RB, RA);
-        seg_pair_dot(p.nseg(), 1, G.get(), i64(RB) * RA, RB, RB, RA, H.get(), i64(RA) * RB, RA, out, true);
+        // H = (V_a^T U_b)^T formed as U_b^T V_a (RB x RA): the pair trace is a contiguous sibling dot
+        seg_tn(p, b.Ul(l), n, RB, a.Vl(l), n, RA, H.get(), i64(RB) * RA, RB);
+        seg_dot(p.nseg(), 1, G.get(), i64(RB) * RA, H.get(), i64(RB) * RA, i64(RB) * RA, out, true);
     }
 }
 

@@ -47,6 +47,11 @@ void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double be
 void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 ldx, double a_even,
                         double a_odd, double* Y, i64 ldy, double beta);
 
+/// out[0] (+)= sum_s sum_{e<len} A[s gsa + e] B[(s^xr) gsb + e] (deterministic
+/// streaming reduction; the HBM-bound core of every trace).
+void seg_dot(int nseg, int xr, const double* A, i64 gsa, const double* B, i64 gsb, i64 len, double* out,
+             bool accumulate);
+
 /// out[0] (+)= sum(A .* B) over n x w (deterministic).
 void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate);
 

@@ -192,8 +192,9 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
         const size_t sz = static_cast<size_t>(p.nseg()) * static_cast<size_t>(W) * static_cast<size_t>(Cf);
         DVec G1(sz), G2(sz);
         seg_tn(p, coarse.Cv->get() + i64(c0) * n, n, W, fine.Cul(f), n, Cf, G1.get(), i64(W) * Cf, W, alpha);
-        seg_tn(p, fine.Cvl(f), n, Cf, coarse.Cu->get() + i64(c0) * n, n, W, G2.get(), i64(W) * Cf, Cf);
-        seg_pair_dot(p.nseg(), 0, G1.get(), i64(W) * Cf, W, W, Cf, G2.get(), i64(W) * Cf, Cf, out, true);
+        // G2 = (Cv_f^T Cu_c)^T formed directly as Cu_c^T Cv_f: tr(G1 G2) is then a contiguous dot
+        seg_tn(p, coarse.Cu->get() + i64(c0) * n, n, W, fine.Cvl(f), n, Cf, G2.get(), i64(W) * Cf, W);
+        seg_dot(1, 0, G1.get(), 0, G2.get(), 0, i64(p.nseg()) * W * Cf, out, true);
     };
     for (int f = 1; f <= tau; ++f) {
         const int cf = pb.coff[static_cast<size_t>(f - 1)];
