@@ -435,13 +435,17 @@ void seg_tn(const Partition& p, const double* A, i64 lda, int ca, const double* 
     const double rows = double(p.hbounds().back() - p.hbounds().front());
     ProfScope prof(PROF_SEG_TN, 2.0 * rows * ca * cb, 8.0 * (rows * (ca + cb) + double(p.nseg()) * ca * cb));
     if (prof_enabled()) prof.key(prof_tag("tn nseg=%d ca=%d cb=%d", p.nseg(), ca, cb));
-    const TileList& tl = p.tiles(SEG_CHUNK);
     int tbm = tile::tile_for(ca), tbn = tile::tile_for(cb);
     if (ca > 32 && ca <= 40 && tbn % 32 == 0)  // 1 x 4 warp grid
         tbm = 40;
     else if (cb > 32 && cb <= 40 && tbm % 32 == 0)  // 4 x 1 warp grid
         tbn = 40;
     const int tiles_m = cdiv(ca, tbm), tiles_n = cdiv(cb, tbn);
+    // Split-K chunk: the shortest (from SEG_CHUNK rows, doubling) that still
+    // gives >= 8 CTAs per SM; longer chunks write fewer ca x cb partials.
+    int chunk = SEG_CHUNK;
+    while (chunk < p.max_seg() && (i64(rows) / (2 * chunk)) * tiles_m * tiles_n >= 8 * c.num_sms) chunk *= 2;
+    const TileList& tl = p.tiles(chunk);
     SegTnArgs g{A, lda, ca, B, ldb, cb, tl.items.get(), tiles_m, T, tstride, ldt, 1, alpha, beta};
     DVec ws;
     if (!tl.one_per_seg) {

@@ -210,16 +210,16 @@ struct ItemPlan {
     int nred = 0;
 };
 
-const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
+const ItemPlan& item_plan(const DTree& t, int lmin, int lmax, int chunk_rows) {
     static std::mutex mu;
-    static std::map<std::tuple<const DTree*, int, int>, std::unique_ptr<ItemPlan>> cache;
+    static std::map<std::tuple<const DTree*, int, int, int>, std::unique_ptr<ItemPlan>> cache;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(&t, lmin, lmax);
+    auto key = std::make_tuple(&t, lmin, lmax, chunk_rows);
     auto itc = cache.find(key);
     if (itc != cache.end()) return *itc->second;
     auto p = std::make_unique<ItemPlan>();
     const int nl = lmax - lmin + 1;
-    // Per level: chunks of at most ML_CHUNK rows that never cross a segment.
+    // Per level: chunks of at most chunk_rows rows that never cross a segment.
     std::vector<std::vector<MlItem>> per(static_cast<size_t>(nl));
     std::vector<int> rl, ri, rf, rc;
     p->nchunks.assign(static_cast<size_t>(nl), 0);
@@ -228,13 +228,13 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
         const auto& hb = pt.hbounds();
         bool multi = false;
         for (int sgi = 0; sgi < pt.nseg(); ++sgi)
-            if (hb[static_cast<size_t>(sgi + 1)] - hb[static_cast<size_t>(sgi)] > ML_CHUNK) multi = true;
+            if (hb[static_cast<size_t>(sgi + 1)] - hb[static_cast<size_t>(sgi)] > chunk_rows) multi = true;
         int chunk = 0;
         for (int sgi = 0; sgi < pt.nseg(); ++sgi) {
             const int lo = hb[static_cast<size_t>(sgi)], hi = hb[static_cast<size_t>(sgi + 1)];
             const int first = chunk;
-            for (int r = lo; r < hi || r == lo; r += ML_CHUNK) {
-                per[static_cast<size_t>(i)].push_back(MlItem{i, sgi, r, std::min(ML_CHUNK, hi - r), chunk++});
+            for (int r = lo; r < hi || r == lo; r += chunk_rows) {
+                per[static_cast<size_t>(i)].push_back(MlItem{i, sgi, r, std::min(chunk_rows, hi - r), chunk++});
                 if (hi == lo) break;
             }
             if (multi) {
@@ -280,6 +280,15 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax) {
     return ref;
 }
 
+/// Projection chunk: from ML_CHUNK rows, doubled while >= 8 CTAs per SM remain
+/// (fewer split-K partials to write and fold).
+int proj_chunk(const DTree& t, int nl, int tiles) {
+    int chunk = ML_CHUNK;
+    const i64 n = t.n();
+    while (chunk < t.part(1).max_seg() && (n / (2 * chunk)) * nl * tiles >= 8 * current().num_sms) chunk *= 2;
+    return chunk;
+}
+
 }  // namespace
 
 void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i64 ldy, int lmin, int lmax,
@@ -304,7 +313,13 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     if (int(lv.size()) > MAXL) throw std::length_error("hodlr_apply: too many levels");
     auto& c = current();
-    const ItemPlan& ip = item_plan(t, lmin, lmax);
+    int rmax0 = 1;
+    for (int l = lmin; l <= lmax; ++l) rmax0 = std::max(rmax0, h.Rl(l));
+    const int tbm0 = tile::tile_for(rmax0), tbn0 = tile::tile_for_n(s, tbm0);
+    int chunk = proj_chunk(t, lmax - lmin + 1, cdiv(rmax0, tbm0) * cdiv(s, tbn0));
+    if (zero.bounds)  // keep chunks inside the hint's segments so zero chunks are still skipped
+        while (chunk > ML_CHUNK && chunk > n / std::max(zero.nseg, 1)) chunk /= 2;
+    const ItemPlan& ip = item_plan(t, lmin, lmax, chunk);
     MlLevels L{};
     L.nl = lmax - lmin + 1;
     std::vector<DVec> Tbuf(static_cast<size_t>(L.nl)), Wbuf(static_cast<size_t>(L.nl));
@@ -392,7 +407,13 @@ std::vector<DVecP> hodlr_project(const DHodlr& h, const double* X, i64 ldx, int 
     if (s <= 0 || tau < 1) return out;
     if (tau > MAXL) throw std::length_error("hodlr_project: too many levels");
     auto& c = current();
-    const ItemPlan& ip = item_plan(t, 1, tau);
+    int rmax0 = 1, cmax0 = 1;
+    for (int l = 1; l <= tau; ++l) {
+        rmax0 = std::max(rmax0, h.Rl(l));
+        cmax0 = std::max(cmax0, std::min(s, ncol[static_cast<size_t>(l - 1)]));
+    }
+    const int tbm0 = tile::tile_for(rmax0), tbn0 = tile::tile_for_n(cmax0, tbm0);
+    const ItemPlan& ip = item_plan(t, 1, tau, proj_chunk(t, tau, cdiv(rmax0, tbm0) * cdiv(cmax0, tbn0)));
     MlLevels L{};
     L.nl = tau;
     std::vector<DVec> Wbuf(static_cast<size_t>(tau));
