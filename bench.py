@@ -282,8 +282,18 @@ def main():
     dom = max(prof, key=lambda c: prof[c]["ms"])
     d = prof[dom]
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    traffic = None
+    try:  # DRAM bytes of the class from the committed ncu capture (profiles/r1_traffic_seg_tn_class.json)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic_seg_tn_class.json")))
+        if dom == "seg_tn":
+            traffic = sum(v["dram_bytes"] for v in tj.values()) / max(d["launches"], 1)
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": "tensor", "kernel": f"k_{dom}", "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per call (ncu dram__bytes_read+write over one step's k_seg_tn/k_ml_proj/"
+                                "k_ml_update launches / calls)",
+                "algorithmic_bytes_per_call": d["bytes"] / max(d["launches"], 1),
                 "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                 "launches": d["launches"], "share_of_step": d["ms"] / sum(v["ms"] for v in prof.values())}
     ledger = {c: {"ms": round(v["ms"], 3), "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3),

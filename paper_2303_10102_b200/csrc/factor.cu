@@ -76,10 +76,11 @@ __device__ bool dev_llt(double* W, int ldw, int m) {
         const double d = W[k + i64(k) * ldw];
         for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) W[i + i64(k) * ldw] /= d;
         __syncthreads();
-        const int rem = m - k - 1;
-        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-            const int i = k + 1 + e % rem, j = k + 1 + e / rem;
-            if (i >= j) W[i + i64(j) * ldw] -= W[i + i64(k) * ldw] * W[j + i64(k) * ldw];
+        // trailing update of the lower triangle: warp per column, lanes down the rows
+        const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int j = k + 1 + int(threadIdx.x >> 5); j < m; j += nw) {
+            const double wjk = W[j + i64(k) * ldw];
+            for (int i = j + lane; i < m; i += 32) W[i + i64(j) * ldw] -= W[i + i64(k) * ldw] * wjk;
         }
         __syncthreads();
     }
@@ -151,19 +152,15 @@ __global__ void __launch_bounds__(FNT) k_leaf_factor(LeafFacArgs g) {
     double* W = g.use_smem ? sm : g.fac + b * ls;
     const int ldw = g.use_smem ? m : g.bmax;
     int* piv = g.piv + i64(b) * g.bmax;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int i = e % m, j = e / m;
-        W[i + i64(j) * ldw] = A[i + i64(j) * g.bmax];
-    }
+    for (int j = 0; j < m; ++j)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) W[i + i64(j) * ldw] = A[i + i64(j) * g.bmax];
     __syncthreads();
     bool llt = false;
     if (g.prefer_llt) llt = dev_llt(W, ldw, m);
     int nswap = 0;
     if (!llt) {
-        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-            const int i = e % m, j = e / m;
-            W[i + i64(j) * ldw] = A[i + i64(j) * g.bmax];
-        }
+        for (int j = 0; j < m; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) W[i + i64(j) * ldw] = A[i + i64(j) * g.bmax];
         __syncthreads();
         nswap = dev_lu(W, ldw, m, piv);
     }
@@ -188,10 +185,8 @@ __global__ void __launch_bounds__(FNT) k_leaf_factor(LeafFacArgs g) {
     if (g.use_smem) {
         __syncthreads();
         double* F = g.fac + b * ls;
-        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-            const int i = e % m, j = e / m;
-            F[i + i64(j) * g.bmax] = W[i + i64(j) * ldw];
-        }
+        for (int j = 0; j < m; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) F[i + i64(j) * g.bmax] = W[i + i64(j) * ldw];
     }
 }
 
