@@ -32,6 +32,7 @@ struct MlLevels {
     int depth[MAXL];        // partition depth of level l (= l)
     int R[MAXL];            // rank capacity
     int ktoff[MAXL + 1];    // prefix of ceil(R/BK) (update kernel K tiles)
+    int coff[MAXL + 1];     // prefix of R (packed update K: levels back to back)
     const double* P[MAXL];  // projection operand (V_l, or U_l when transposed)
     const double* Q[MAXL];  // update operand (U_l, or V_l when transposed)
     double* T[MAXL];        // per-level projections: nseg_l x R_l x s (ld R_l)
@@ -171,6 +172,88 @@ struct LoadUpdB {
         }
     }
 };
+
+constexpr int PACK_MAX = 2048;  // packed update K held as a (level, column) table in shared memory
+
+/// Packed A operand: K runs over the levels' columns back to back (no
+/// per-level padding to BK); tab[c] = level << 16 | column for c < coff[nl].
+struct LoadUpdAPacked {
+    static constexpr bool KC = false;
+    static constexpr int ROWS = BM;
+    const MlLevels* L;
+    const int* tab;
+    int row0, rows;
+    i64 n;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        const int m = threadIdx.x & 63, ktot = L->coff[L->nl];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = (threadIdx.x >> 6) + 2 * q, cc = kt * BK + k;
+            const bool v = m < rows && cc < ktot;
+            const int e = v ? tab[cc] : 0, l = e >> 16, j = e & 0xffff;
+            const double* src = L->Q[l] + row0 + m + i64(j) * n;
+            tile::cp_async8(S + k * tile::LD_MC + m, v ? src : L->Q[0], v);
+        }
+    }
+};
+
+template <int TBN>
+struct LoadUpdBPacked {
+    static constexpr bool KC = true;
+    static constexpr int ROWS = TBN;
+    const MlLevels* L;
+    const int* tab;
+    int leaf, tau, s, n0;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        const int k = threadIdx.x & 15, cc = kt * BK + k, ktot = L->coff[L->nl];
+        const bool kv = cc < ktot;
+        const int e = kv ? tab[cc] : 0, l = e >> 16, j = e & 0xffff, R = L->R[l];
+        const int seg = (leaf >> (tau - L->depth[l])) ^ 1;
+        const double* base = L->T[l] + i64(seg) * R * s + i64(n0) * R + j;
+#pragma unroll
+        for (int q = 0; q < TBN / 8; ++q) {
+            const int c = (threadIdx.x >> 4) + 8 * q;
+            const bool v = kv && n0 + c < s;
+            tile::cp_async8(S + c * tile::LD_KC + k, v ? base + i64(c) * R : L->T[0], v);
+        }
+    }
+};
+
+template <int TBN>
+__global__ void __launch_bounds__(THREADS) k_ml_update_packed(UpdArgs g) {
+    extern __shared__ double smem[];
+    __shared__ MlLevels L;
+    __shared__ int tab[PACK_MAX];
+    if (g.out_depth >= 0 && ((g.items[blockIdx.x].seg >> (g.tau - g.out_depth)) & 1) != g.out_parity) return;
+    for (int i = threadIdx.x; i < int(sizeof(MlLevels) / sizeof(int)); i += blockDim.x)
+        reinterpret_cast<int*>(&L)[i] = reinterpret_cast<const int*>(&g.L)[i];
+    __syncthreads();
+    const int ktot = L.coff[L.nl];
+    for (int c = threadIdx.x; c < ktot; c += blockDim.x) {
+        int l = 0;
+        while (c >= L.coff[l + 1]) ++l;
+        tab[c] = (l << 16) | (c - L.coff[l]);
+    }
+    __syncthreads();
+    const WorkItem it = g.items[blockIdx.x];
+    const int n0 = blockIdx.y * TBN;
+    LoadUpdAPacked la{&L, tab, it.row0, it.rows, g.n};
+    LoadUpdBPacked<TBN> lb{&L, tab, it.seg, g.tau, g.s, n0};
+    typename tile::Shape<BM, TBN>::Acc acc, yv;
+    acc.zero();
+    yv.zero();
+    if (g.beta != 0.0)
+        tile::for_each_slot<BM, TBN>(yv, [&](double& y, int m, int ni) {
+            const int c = n0 + ni;
+            if (c < g.s && m < it.rows) y = g.Y[i64(it.row0 + m) + i64(c) * g.ldy];
+        });
+    tile::run_t<2, BM, TBN>(la, lb, (ktot + BK - 1) / BK, smem, acc);
+    tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
+        const int c = n0 + ni;
+        if (c >= g.s || m >= it.rows) return;
+        g.Y[i64(it.row0 + m) + i64(c) * g.ldy] = g.alpha * v + g.beta * y;
+    });
+}
 
 template <int TBN>
 __global__ void __launch_bounds__(THREADS) k_ml_update(UpdArgs g) {
@@ -325,12 +408,14 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     std::vector<DVec> Tbuf(static_cast<size_t>(L.nl)), Wbuf(static_cast<size_t>(L.nl));
     double flops = 0, bytes = 8.0 * double(n) * (s + 2.0 * s);
     L.ktoff[0] = 0;
+    L.coff[0] = 0;
     for (int i = 0; i < L.nl; ++i) {
         const int l = lmin + i, R = h.Rl(l);
         const Partition& pt = t.part(l);
         L.depth[i] = l;
         L.R[i] = R;
         L.ktoff[i + 1] = L.ktoff[i] + (R + BK - 1) / BK;
+        L.coff[i + 1] = L.coff[i] + R;
         L.P[i] = transpose ? h.Ul(l) : h.Vl(l);
         L.Q[i] = transpose ? h.Vl(l) : h.Ul(l);
         if (R > 0) {
@@ -356,7 +441,9 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     int rmax = 1;
     for (int i = 0; i < L.nl; ++i) rmax = std::max(rmax, L.R[i]);
-    const int tbm = tile::tile_for(rmax), tbn = tile::tile_for_n(s, tbm);
+    int tbm = tile::tile_for(rmax);
+    const int tbn = tile::tile_for_n(s, tbm);
+    if (rmax > 32 && rmax <= 40 && tbn % 32 == 0) tbm = 40;  // 1 x 4 warp grid: no padding of rank-40 levels
     const int max_tiles_m = (rmax + tbm - 1) / tbm;
     const int tiles_n = (s + tbn - 1) / tbn;
     ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n, zero};
@@ -388,11 +475,21 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
                zero.bounds && zero.out_depth <= t.tau() ? zero.out_depth : -1, zero.parity};
     // the update's N tile may differ from the projection's (its M is always 64)
     const int tbn_u = tile::tile_for_n(s, BM), tiles_nu = (s + tbn_u - 1) / tbn_u;
+    const bool packed = L.coff[L.nl] <= PACK_MAX && (L.coff[L.nl] + BK - 1) / BK < L.ktoff[L.nl];
     with_tile(tbn_u, [&](auto TN) {
         constexpr int N = decltype(TN)::value;
         constexpr int bytes = tile::smem_bytes_t(2, BM, N);
-        attr_once<k_ml_update<N>>(bytes);
-        k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
+        if (packed) {
+            static bool once = [] {  // static table + dynamic stages exceed the default 48 KB
+                HG_CUDA(cudaFuncSetAttribute(k_ml_update_packed<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+                return true;
+            }();
+            (void)once;
+            k_ml_update_packed<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
+        } else {
+            attr_once<k_ml_update<N>>(bytes);
+            k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
+        }
     });
     HG_LAUNCH();
     ++c.launches;
