@@ -124,28 +124,27 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
 }
 
 /// Streaming variant for short K (k <= 48) and wide w: the CTA keeps its
-/// 64-row X tile in shared memory and walks a run of column tiles, staging
-/// the next T and Y tiles with cp.async while the current one is multiplied.
-/// The op is HBM-bound (AI = k/8 flop/B), so the loop keeps a full tile of
-/// Y in flight per CTA instead of paying the load latency once per tile.
+/// 64-row X tile in shared memory and walks a run of column tiles. The op is
+/// HBM-bound (AI = k/8 flop/B): T tiles are staged one ahead with cp.async,
+/// and the accumulated Y tile goes straight to registers in the accumulator
+/// layout one tile ahead (no shared staging, so three CTAs fit per SM and
+/// more of Y is in flight).
 constexpr int SNN_KT = 3;  // k <= 48
 
 template <int TBN>
 struct SnnLayout {
     static constexpr int XE = SNN_KT * tile::stage_elems(BM);   // X, all k slices
     static constexpr int TE = SNN_KT * tile::stage_elems(TBN);  // T tile, all k slices
-    static constexpr int YLD = BM + 4;
-    static constexpr int YE = TBN * YLD;                        // Y tile, m-contiguous
-    static constexpr int BYTES = int(sizeof(double)) * (XE + 2 * (TE + YE));
+    static constexpr int BYTES = int(sizeof(double)) * (XE + 2 * TE);
 };
 
 template <int TBN>
 __global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int groups) {
     using Lay = SnnLayout<TBN>;
+    using Acc = typename tile::Shape<BM, TBN>::Acc;
     extern __shared__ double smem[];
     double* Xs = smem;
-    double* Ts = smem + Lay::XE;           // 2 buffers of TE
-    double* Ys = Ts + 2 * Lay::TE;         // 2 buffers of YE
+    double* Ts = smem + Lay::XE;  // 2 buffers of TE
     const WorkItem it = g.items[blockIdx.x / groups];
     const int grp = blockIdx.x % groups;
     const int ntiles = cdiv_d(g.w, TBN), per = cdiv_d(ntiles, groups);
@@ -157,44 +156,45 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int grou
     tile::LoadMCT<BM> lx{g.X + it.row0, g.ldx, it.rows, g.k};
     for (int kt = 0; kt < kt_n; ++kt) lx.issue(Xs + kt * tile::stage_elems(BM), kt);
     const bool ld_y = g.beta != 0.0;
-    auto issue = [&](int j, int buf) {
+    auto issue_t = [&](int j, int buf) {
         const int n0 = j * TBN;
         tile::LoadKCT<TBN> lt{Tb + i64(n0) * g.ldt, g.ldt, g.k, g.w - n0};
         double* T = Ts + buf * Lay::TE;
         for (int kt = 0; kt < kt_n; ++kt) lt.issue(T + kt * tile::stage_elems(TBN), kt);
-        if (ld_y) {
-            double* Y = Ys + buf * Lay::YE;
-            const double* yb = g.Y + it.row0 + i64(n0) * g.ldy;
-#pragma unroll
-            for (int q = 0; q < BM * TBN / THREADS; ++q) {
-                const int e = threadIdx.x + THREADS * q, m = e % BM, c = e / BM;
-                const bool v = m < it.rows && n0 + c < g.w;
-                tile::cp_async8(Y + c * Lay::YLD + m, v ? yb + m + i64(c) * g.ldy : yb, v);
-            }
-        }
     };
-    issue(j0, 0);
+    auto load_y = [&](int j, Acc& y) {
+        const int n0 = j * TBN;
+        tile::for_each_slot<BM, TBN>(y, [&](double& v, int m, int ni) {
+            const int n = n0 + ni;
+            v = (n < g.w && m < it.rows) ? g.Y[i64(it.row0 + m) + i64(n) * g.ldy] : 0.0;
+        });
+    };
+    Acc ycur, ynext;
+    if (ld_y) load_y(j0, ycur);
+    issue_t(j0, 0);
     tile::cp_commit();
     for (int j = j0; j < j1; ++j) {
         const int buf = (j - j0) & 1;
         tile::cp_wait<0>();
         __syncthreads();  // tile j (and X) landed; every warp is done with the other buffer
-        if (j + 1 < j1) issue(j + 1, buf ^ 1);
+        if (j + 1 < j1) {
+            issue_t(j + 1, buf ^ 1);
+            if (ld_y) load_y(j + 1, ynext);
+        }
         tile::cp_commit();
-        typename tile::Shape<BM, TBN>::Acc acc;
+        Acc acc;
         acc.zero();
         const double* T = Ts + buf * Lay::TE;
         for (int kt = 0; kt < kt_n; ++kt)
             tile::mma_stage<false, true, BM, TBN>(Xs + kt * tile::stage_elems(BM), T + kt * tile::stage_elems(TBN),
                                                   acc);
-        const double* Y = Ys + buf * Lay::YE;
         const int n0 = j * TBN;
-        tile::for_each_slot<BM, TBN>(acc, [&](double& v, int m, int ni) {
+        tile::for_each_slot2<BM, TBN>(acc, ycur, [&](double v, double y, int m, int ni) {
             const int n = n0 + ni;
             if (n >= g.w || m >= it.rows) return;
-            const double y = ld_y ? g.beta * Y[ni * Lay::YLD + m] : 0.0;
-            g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + y;
+            g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + (ld_y ? g.beta * y : 0.0);
         });
+        if (ld_y) ycur = ynext;
     }
     tile::cp_wait<0>();
 }
