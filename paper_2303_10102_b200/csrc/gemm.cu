@@ -129,18 +129,18 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn(SegNnArgs g) {
 /// and the accumulated Y tile goes straight to registers in the accumulator
 /// layout one tile ahead (no shared staging, so three CTAs fit per SM and
 /// more of Y is in flight).
-constexpr int SNN_KT = 3;  // k <= 48
+constexpr int SNN_KT = 5;  // k <= 80 (k slices of X / T held in shared memory)
 
-template <int TBN>
+template <int TBN, int KT>
 struct SnnLayout {
-    static constexpr int XE = SNN_KT * tile::stage_elems(BM);   // X, all k slices
-    static constexpr int TE = SNN_KT * tile::stage_elems(TBN);  // T tile, all k slices
+    static constexpr int XE = KT * tile::stage_elems(BM);   // X, all k slices
+    static constexpr int TE = KT * tile::stage_elems(TBN);  // T tile, all k slices
     static constexpr int BYTES = int(sizeof(double)) * (XE + 2 * TE);
 };
 
-template <int TBN>
+template <int TBN, int KT>
 __global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int groups) {
-    using Lay = SnnLayout<TBN>;
+    using Lay = SnnLayout<TBN, KT>;
     using Acc = typename tile::Shape<BM, TBN>::Acc;
     extern __shared__ double smem[];
     double* Xs = smem;
@@ -498,8 +498,15 @@ void seg_nn(const Partition& p, const double* X, i64 ldx, int k, const double* T
         SegNnArgs g{X, ldx, k, T, tstride, ldt, map, Y, ldy, w, tl.items.get(), alpha, beta};
         const int want = 4 * c.num_sms, ntiles = cdiv(w, TN);
         const int groups = std::max(1, std::min(ntiles / 4, cdiv(want, tl.count)));
-        attr_once<k_seg_nn_stream<TN>>(SnnLayout<TN>::BYTES);
-        k_seg_nn_stream<TN><<<unsigned(tl.count * groups), THREADS, SnnLayout<TN>::BYTES, c.stream>>>(g, groups);
+        if (k <= 3 * BK) {
+            attr_once<k_seg_nn_stream<TN, 3>>(SnnLayout<TN, 3>::BYTES);
+            k_seg_nn_stream<TN, 3>
+                <<<unsigned(tl.count * groups), THREADS, SnnLayout<TN, 3>::BYTES, c.stream>>>(g, groups);
+        } else {
+            attr_once<k_seg_nn_stream<TN, 5>>(SnnLayout<TN, 5>::BYTES);
+            k_seg_nn_stream<TN, 5>
+                <<<unsigned(tl.count * groups), THREADS, SnnLayout<TN, 5>::BYTES, c.stream>>>(g, groups);
+        }
         HG_LAUNCH();
         ++c.launches;
         return;
