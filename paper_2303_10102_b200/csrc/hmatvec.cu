@@ -69,6 +69,7 @@ struct MvArgs {
     i64 ldy;
     double alpha, beta;
     int* ticket;
+    int dleft;  // pass 2 covers levels of depth <= dleft (deeper ones finish inside a CTA)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -104,11 +105,11 @@ __device__ __forceinline__ double tr_reduce(double (&v)[V], int lane) {
 }
 
 /// Row k of this thread within the leaf. NT = 64 threads own row pairs
-/// (2t, 2t+1: 16-byte loads, half the instructions per byte); otherwise
-/// rows t + k NT.
+/// (2t, 2t+1: 16-byte loads, half the instructions per byte; t = thread
+/// index within its 64-thread leaf group); otherwise rows t + k NT.
 template <int NT, int RPT>
 __device__ __forceinline__ int mv_row(int k) {
-    return NT == 64 ? 2 * int(threadIdx.x) + k : int(threadIdx.x) + k * NT;
+    return NT == 64 ? 2 * int(threadIdx.x & 63) + k : int(threadIdx.x) + k * NT;
 }
 
 /// v[k][jj] = P[row_k, j0 + jj] (0 outside the leaf / past R).
@@ -116,7 +117,7 @@ template <int NT, int RPT>
 __device__ __forceinline__ void load_blk(double (&v)[RPT][8], const double* P, i64 n, int lo, int m, int j0, int R) {
     if constexpr (NT == 64) {
         static_assert(RPT == 2, "row pairs");
-        const int r = 2 * int(threadIdx.x);
+        const int r = 2 * int(threadIdx.x & 63);  // 64-thread group per leaf (multi-leaf CTAs)
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
             const double* p = P + i64(lo) + r + i64(j0 + jj) * n;
@@ -372,6 +373,134 @@ __global__ void __launch_bounds__(NT) k_mv_sweep(const __grid_constant__ MvArgs 
     }
 }
 
+/// Multi-leaf sweep (row pairs, LPC leaves per CTA = one node of depth
+/// tau - log2 LPC): the levels below that node finish inside the CTA —
+/// both children's projections are folded in shared memory and both halves
+/// updated (rows re-read from L2) — so neither publication nor the second
+/// pass touches them; the levels above behave as in k_mv_sweep with the CTA
+/// node as the chunk.
+template <int S, int LPC>
+__global__ void __launch_bounds__(64 * LPC) k_mv_sweep_multi(const __grid_constant__ MvArgs g) {
+    constexpr int NTH = 64 * LPC, NW = NTH / 32;
+    constexpr int J = LPC == 2 ? 1 : LPC == 4 ? 2 : 3;
+    extern __shared__ double sm[];
+    __shared__ int s_ord[MV_MAXL], s_nleft, s_nin, s_b;
+    if (threadIdx.x == 0) s_b = atomicAdd(g.ticket, 1);
+    __syncthreads();
+    const int cta = s_b, tc = g.tau - J;
+    const int slot = threadIdx.x >> 6;
+    const int b = cta * LPC + slot;
+    const int lo = g.lb[b], m = g.lb[b + 1] - lo;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int rmax = 0;
+    for (int li = 0; li < g.nl; ++li) rmax = max(rmax, g.L[li].R);
+    const int RSM = rmax * S;
+    double* red = sm;                    // 2 x NW x RSM
+    double* part = red + 2 * NW * RSM;   // RSM (warp 0)
+    double* tw = part + RSM;             // NW x RSM
+    double* tloc = tw + NW * RSM;        // LPC x RSM (children inside the CTA)
+    double* xs = tloc + LPC * RSM;       // LPC x 128 x S
+    if (threadIdx.x == 0) {  // order: cross levels as left child, in-CTA levels, cross levels as right child
+        int k = 0;
+        for (int li = 0; li < g.nl; ++li)
+            if (g.L[li].depth <= tc && !((cta >> (tc - g.L[li].depth)) & 1)) s_ord[k++] = li;
+        s_nleft = k;
+        for (int li = 0; li < g.nl; ++li)
+            if (g.L[li].depth > tc) s_ord[k++] = li;
+        s_nin = k;
+        for (int li = 0; li < g.nl; ++li)
+            if (g.L[li].depth <= tc && ((cta >> (tc - g.L[li].depth)) & 1)) s_ord[k++] = li;
+    }
+    double x[2][S], yacc[2][S];
+    double* xl = xs + slot * 128 * S;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = mv_row<64, 2>(k);
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+            x[k][c] = (r < m && c < g.s) ? g.X[i64(lo) + r + i64(c) * g.ldx] : 0.0;
+            yacc[k][c] = 0.0;
+            if (r < m) xl[r * S + c] = x[k][c];
+        }
+    }
+    __syncthreads();
+    const int nleft = s_nleft, nin = s_nin;
+    for (int i = 0; i <= g.nl; ++i) {
+        if (i == nin && g.leaves) {  // leaf block of this thread's leaf
+            const double* Lb = g.leaves + i64(b) * g.lstride;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int r = mv_row<64, 2>(k);
+                if (r >= m) continue;
+                double acc[S];
+#pragma unroll
+                for (int c = 0; c < S; ++c) acc[c] = 0.0;
+#pragma unroll 16
+                for (int q = 0; q < m; ++q) {
+                    const double lv = Lb[r + i64(q) * g.bmax];
+#pragma unroll
+                    for (int c = 0; c < S; ++c) acc[c] = fma(lv, xl[q * S + c], acc[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < S; ++c) yacc[k][c] += acc[c];
+            }
+        }
+        if (i == g.nl) break;
+        const MvLevel& L = g.L[s_ord[i]];
+        const int R = L.R, RS = R * S;
+        double* rb = red + (i & 1) * NW * RSM;
+        if (i >= nleft && i < nin) {  // level inside the CTA node
+            sweep_level<S, 2, 64, false>(L, g.n, lo, m, x, nullptr, rb, yacc);
+            __syncthreads();
+            const int sh = g.tau - L.depth, nch = LPC >> sh, wpc = 2 << sh;  // children, warps per child
+            for (int q = threadIdx.x; q < nch * RS; q += NTH) {
+                const int c = q / RS, e = q - c * RS;
+                double acc = rb[(c * wpc) * RS + e];
+                for (int w = 1; w < wpc; ++w) acc += rb[(c * wpc + w) * RS + e];
+                tloc[c * RS + e] = acc;
+            }
+            __syncthreads();
+            update<S, 2, 64>(L.Q, g.n, lo, m, R, tloc + ((slot >> sh) ^ 1) * RS, yacc);
+            continue;
+        }
+        const int anc = cta >> (tc - L.depth);
+        if (anc & 1) {
+            double* tv = tw + warp * RSM;
+            if (lane == 0)
+                while (ld_acquire(L.ready + (anc ^ 1)) == 0) __nanosleep(32);
+            __syncwarp();
+            const double* t = L.T + i64(anc ^ 1) * RS;
+            for (int q = lane; q < RS; q += 32) tv[q] = __ldcg(t + q);
+            __syncwarp();
+            sweep_level<S, 2, 64, true>(L, g.n, lo, m, x, tv, rb, yacc);
+        } else {
+            sweep_level<S, 2, 64, false>(L, g.n, lo, m, x, nullptr, rb, yacc);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            for (int q = lane; q < RS; q += 32) {
+                double acc = rb[q];
+#pragma unroll
+                for (int w = 1; w < NW; ++w) acc += rb[w * RS + q];
+                part[q] = acc;
+            }
+            __syncwarp();
+            publish_warp<S>(L, tc, cta, anc, part);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = mv_row<64, 2>(k);
+        if (r >= m) continue;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+            if (c >= g.s) continue;
+            double* yp = g.Y + i64(lo) + r + i64(c) * g.ldy;
+            *yp = g.beta == 0.0 ? g.alpha * yacc[k][c] : fma(g.alpha, yacc[k][c], g.beta * *yp);
+        }
+    }
+}
+
 template <int S, int RPT, int NT>
 __global__ void __launch_bounds__(NT) k_mv_left(const __grid_constant__ MvArgs g) {
     extern __shared__ double sm[];
@@ -386,7 +515,7 @@ __global__ void __launch_bounds__(NT) k_mv_left(const __grid_constant__ MvArgs g
     for (int li = 0; li < g.nl; ++li) {
         const MvLevel& L = g.L[li];
         const int anc = b >> (g.tau - L.depth);
-        if (anc & 1) continue;
+        if ((anc & 1) || L.depth > g.dleft) continue;
         any = true;
         const int R = L.R;
         const double* t = L.T + i64(anc ^ 1) * R * S;
@@ -412,17 +541,33 @@ __global__ void __launch_bounds__(NT) k_mv_left(const __grid_constant__ MvArgs g
 /// Pass 2 for the register sweep's shapes: each left level's rows are loaded
 /// at once; T of the right sibling is read with warp-uniform (broadcast) loads.
 template <int S, int RPT, int NT>
-void launch(const MvArgs& a, int nleaves, int rmax, int bmax) {
+void launch(MvArgs& a, int nleaves, int rmax, int bmax) {
     auto& c = current();
     constexpr int NW = NT / 32;
-    const int sm1 = int(sizeof(double)) * ((3 * NW + 1) * rmax * S + bmax * S);
     const int sm2 = int(sizeof(double)) * (rmax * S > 0 ? rmax * S : 1);
-    static bool once = [] {
-        HG_CUDA(cudaFuncSetAttribute(k_mv_sweep<S, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        return true;
-    }();
-    (void)once;
-    k_mv_sweep<S, RPT, NT><<<unsigned(nleaves), NT, size_t(sm1), c.stream>>>(a);
+    constexpr int LPC = 4;
+    if (NT == 64 && a.tau >= 2) {  // row pairs: 4 leaves per CTA, the two deepest levels finish in-CTA
+        constexpr int NTH = 64 * LPC, NWM = NTH / 32;
+        const int sm1 = int(sizeof(double)) * ((3 * NWM + 1 + LPC) * rmax * S + LPC * 128 * S);
+        static bool once = [] {
+            HG_CUDA(cudaFuncSetAttribute(k_mv_sweep_multi<S, LPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         100 * 1024));
+            return true;
+        }();
+        (void)once;
+        a.dleft = a.tau - 2;
+        k_mv_sweep_multi<S, LPC><<<unsigned(nleaves / LPC), NTH, size_t(sm1), c.stream>>>(a);
+    } else {
+        const int sm1 = int(sizeof(double)) * ((3 * NW + 1) * rmax * S + bmax * S);
+        static bool once = [] {
+            HG_CUDA(cudaFuncSetAttribute(k_mv_sweep<S, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         100 * 1024));
+            return true;
+        }();
+        (void)once;
+        a.dleft = a.tau;
+        k_mv_sweep<S, RPT, NT><<<unsigned(nleaves), NT, size_t(sm1), c.stream>>>(a);
+    }
     HG_LAUNCH();
     ++c.launches;
     if (a.nl > 0) {
