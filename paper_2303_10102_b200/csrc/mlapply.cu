@@ -396,13 +396,6 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
     }
     if (int(lv.size()) > MAXL) throw std::length_error("hodlr_apply: too many levels");
     auto& c = current();
-    int rmax0 = 1;
-    for (int l = lmin; l <= lmax; ++l) rmax0 = std::max(rmax0, h.Rl(l));
-    const int tbm0 = tile::tile_for(rmax0), tbn0 = tile::tile_for_n(s, tbm0);
-    int chunk = proj_chunk(t, lmax - lmin + 1, cdiv(rmax0, tbm0) * cdiv(s, tbn0));
-    if (zero.bounds)  // keep chunks inside the hint's segments so zero chunks are still skipped
-        while (chunk > ML_CHUNK && chunk > n / std::max(zero.nseg, 1)) chunk /= 2;
-    const ItemPlan& ip = item_plan(t, lmin, lmax, chunk);
     MlLevels L{};
     L.nl = lmax - lmin + 1;
     std::vector<DVec> Tbuf(static_cast<size_t>(L.nl)), Wbuf(static_cast<size_t>(L.nl));
@@ -418,13 +411,9 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         L.coff[i + 1] = L.coff[i] + R;
         L.P[i] = transpose ? h.Ul(l) : h.Vl(l);
         L.Q[i] = transpose ? h.Vl(l) : h.Ul(l);
-        if (R > 0) {
-            Tbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(pt.nseg()) * R * s);
-            if (ip.nchunks[static_cast<size_t>(i)])
-                Wbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(ip.nchunks[static_cast<size_t>(i)]) * R * s);
-        }
+        if (R > 0) Tbuf[static_cast<size_t>(i)].alloc(static_cast<size_t>(pt.nseg()) * R * s);
         L.T[i] = Tbuf[static_cast<size_t>(i)].get();
-        L.ws[i] = Wbuf[static_cast<size_t>(i)].get();
+        L.ws[i] = nullptr;
         L.ncol[i] = s;
         // algorithmic flops: the projection reads only the nonzero half of X
         // under a ZeroRows hint, the update writes only the rows the caller reads
@@ -439,36 +428,70 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
         prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
     }
-    int rmax = 1;
-    for (int i = 0; i < L.nl; ++i) rmax = std::max(rmax, L.R[i]);
-    int tbm = tile::tile_for(rmax);
-    const int tbn = tile::tile_for_n(s, tbm);
-    if (rmax > 32 && rmax <= 40 && tbn % 32 == 0) tbm = 40;  // 1 x 4 warp grid: no padding of rank-40 levels
-    const int max_tiles_m = (rmax + tbm - 1) / tbm;
-    const int tiles_n = (s + tbn - 1) / tbn;
-    ProjArgs pa{L, ip.items.get(), X, ldx, n, s, tiles_n, zero};
-    with_tile(tbm, [&](auto TM) {
-        with_tile(tbn, [&](auto TN) {
-            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
-            if constexpr (tile::shape_ok(M, N)) {
-                constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
-                attr_once<k_ml_proj<M, N>>(bytes);
-                k_ml_proj<M, N>
-                    <<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
-            } else {
-                throw std::logic_error("hodlr_apply: unsupported tile shape");
-            }
+    // Projections in runs of consecutive levels sharing an M tile (a derivative
+    // HODLR has ranks 4..8 on most levels and ~45 on the deepest two: one tile
+    // for all would pad the thin levels up to 12x).
+    auto proj_tile = [&](int R) { return tile::tile_for(std::max(R, 1)); };
+    for (int a = 0; a < L.nl;) {
+        int e = a, tb = -1;  // run [a, e): levels with one projection tile (empty levels join any run)
+        for (; e < L.nl; ++e) {
+            if (L.R[e] == 0) continue;
+            if (tb < 0)
+                tb = proj_tile(L.R[e]);
+            else if (proj_tile(L.R[e]) != tb)
+                break;
+        }
+        const int b = e - 1;
+        int rmax = 1;
+        for (int i = a; i <= b; ++i) rmax = std::max(rmax, L.R[i]);
+        int tbm = tile::tile_for(rmax);
+        const int tbn = tile::tile_for_n(s, tbm);
+        if (rmax > 32 && rmax <= 40 && tbn % 32 == 0) tbm = 40;  // 1 x 4 warp grid: no padding of rank-40 levels
+        const int max_tiles_m = (rmax + tbm - 1) / tbm;
+        const int tiles_n = (s + tbn - 1) / tbn;
+        int chunk = proj_chunk(t, b - a + 1, max_tiles_m * tiles_n);
+        if (zero.bounds)  // keep chunks inside the hint's segments so zero chunks are still skipped
+            while (chunk > ML_CHUNK && chunk > n / std::max(zero.nseg, 1)) chunk /= 2;
+        const ItemPlan& ip = item_plan(t, lmin + a, lmin + b, chunk);
+        MlLevels Ls{};
+        Ls.nl = b - a + 1;
+        for (int i = 0; i < Ls.nl; ++i) {
+            const int j = a + i;
+            Ls.depth[i] = L.depth[j];
+            Ls.R[i] = L.R[j];
+            Ls.P[i] = L.P[j];
+            Ls.Q[i] = L.Q[j];
+            Ls.T[i] = L.T[j];
+            Ls.ncol[i] = s;
+            if (L.R[j] > 0 && ip.nchunks[static_cast<size_t>(i)])
+                Wbuf[static_cast<size_t>(j)].alloc(static_cast<size_t>(ip.nchunks[static_cast<size_t>(i)]) * L.R[j] * s);
+            Ls.ws[i] = Wbuf[static_cast<size_t>(j)].get();
+        }
+        ProjArgs pa{Ls, ip.items.get(), X, ldx, n, s, tiles_n, zero};
+        with_tile(tbm, [&](auto TM) {
+            with_tile(tbn, [&](auto TN) {
+                constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+                if constexpr (tile::shape_ok(M, N)) {
+                    constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                    attr_once<k_ml_proj<M, N>>(bytes);
+                    k_ml_proj<M, N>
+                        <<<dim3(unsigned(ip.count), unsigned(max_tiles_m * tiles_n)), THREADS, bytes, c.stream>>>(pa);
+                } else {
+                    throw std::logic_error("hodlr_apply: unsupported tile shape");
+                }
+            });
         });
-    });
-    HG_LAUNCH();
-    ++c.launches;
-    if (ip.nred) {
-        int maxblk = 0;
-        for (int i = 0; i < L.nl; ++i) maxblk = std::max(maxblk, L.R[i] * s);
-        ReduceArgs ra{L, ip.rl.get(), ip.ri.get(), ip.rf.get(), ip.rc.get(), s};
-        k_ml_reduce<<<dim3(unsigned(cdiv(maxblk, 256)), unsigned(ip.nred)), 256, 0, c.stream>>>(ra);
         HG_LAUNCH();
         ++c.launches;
+        if (ip.nred) {
+            int maxblk = 0;
+            for (int i = 0; i < Ls.nl; ++i) maxblk = std::max(maxblk, Ls.R[i] * s);
+            ReduceArgs ra{Ls, ip.rl.get(), ip.ri.get(), ip.rf.get(), ip.rc.get(), s};
+            k_ml_reduce<<<dim3(unsigned(cdiv(maxblk, 256)), unsigned(ip.nred)), 256, 0, c.stream>>>(ra);
+            HG_LAUNCH();
+            ++c.launches;
+        }
+        a = e;
     }
     const TileList& tl = t.leaves().tiles(BM);
     UpdArgs ua{L, tl.items.get(), t.tau(), n, Y, ldy, s, alpha, beta,
