@@ -8,6 +8,7 @@
 //                  written once.
 // Reference: HodlrMatrix::matvec / sub_matvec (hodlr_matrix.cpp:198-265).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "hodlr.cuh"
@@ -363,6 +364,116 @@ const ItemPlan& item_plan(const DTree& t, int lmin, int lmax, int chunk_rows) {
     return ref;
 }
 
+// ------------------------------------------------ concatenated thin projections
+// hodlr_project for thin bases (sum of the level ranks <= CAT_MAX): instead of
+// one GEMM per level over the same rows of X (13 re-reads of every X chunk
+// through L2, which bounded the cross terms of the sigma^2 derivative), one
+// GEMM per row span with N = all levels' columns side by side, so each CTA
+// reads its X tile once. A level's accumulators are flushed whenever the
+// K loop crosses one of its segment boundaries (uniform trees: segments of
+// n >> depth rows); levels wider than the span leave per-span partials that
+// a fixed-order reduction folds.
+constexpr int CAT_MAX = 96;
+
+struct CatArgs {
+    const double* X;
+    i64 ldx, n;
+    int s, nl, ncat, span;
+    int tiles_m, tau, leaf;
+    const double* P[MAXL];
+    int R[MAXL], coff[MAXL + 1], ncol[MAXL], depth[MAXL];
+    double* T[MAXL];
+    double* ws[MAXL];
+};
+
+template <int TBN>
+struct LoadCat {
+    static constexpr bool KC = true;
+    static constexpr int ROWS = TBN;
+    const double* const* colp;  // per concatenated column: panel column base (null = absent)
+    const double* dummy;
+    int row0, kmax;
+    __device__ __forceinline__ void issue(double* S, int kt) const {
+        const int k = threadIdx.x & 15, kk = kt * BK + k;
+#pragma unroll
+        for (int q = 0; q < TBN / 8; ++q) {
+            const int c = (threadIdx.x >> 4) + 8 * q;
+            const double* p = colp[c];
+            const bool v = p != nullptr && kk < kmax;
+            tile::cp_async8(S + c * tile::LD_KC + k, v ? p + row0 + kk : dummy, v);
+        }
+    }
+};
+
+template <int TBM, int TBN>
+__global__ void __launch_bounds__(THREADS) k_proj_cat(const __grid_constant__ CatArgs g) {
+    extern __shared__ double smem[];
+    __shared__ const double* colp[TBN];
+    __shared__ int collev[TBN];
+    const int sp = blockIdx.x, row0 = sp * g.span;
+    const int m0 = blockIdx.y * TBM;
+    for (int j = threadIdx.x; j < TBN; j += blockDim.x) {
+        int l = -1;
+        const double* p = nullptr;
+        if (j < g.ncat) {
+            l = 0;
+            while (j >= g.coff[l + 1]) ++l;
+            if (m0 < g.ncol[l]) p = g.P[l] + i64(j - g.coff[l]) * g.n;
+        }
+        collev[j] = l;
+        colp[j] = p;
+    }
+    __syncthreads();
+    tile::LoadKCT<TBM> la{g.X + row0 + i64(m0) * g.ldx, g.ldx, g.span, g.s - m0};
+    LoadCat<TBN> lb{colp, g.X, row0, g.span};
+    typename tile::Shape<TBM, TBN>::Acc acc;
+    acc.zero();
+    const int ktiles = g.span / BK;
+    auto flush = [&](int li, int seg, bool direct) {
+        const int R = g.R[li], c0 = g.coff[li], nc = g.ncol[li];
+        double* o = direct ? g.T[li] + i64(seg) * R * g.s : g.ws[li] + i64(sp) * R * g.s;
+        tile::for_each_slot<TBM, TBN>(acc, [&](double& v, int m, int j) {
+            if (collev[j] != li) return;
+            const int c = m0 + m;
+            if (c < nc) o[(j - c0) + i64(c) * R] = v;
+            v = 0.0;
+        });
+    };
+    // flush schedule in leaf units (bit tests only): a depth-d segment spans
+    // 2^(tau - d) leaves of g.leaf rows
+    const int leaf_kt = g.leaf / BK, leaf0 = row0 / g.leaf;
+    int kc = 0, ld = 0;
+    tile::run_t_hook<tile::STAGES, TBM, TBN>(la, lb, ktiles, smem, acc, [&](int kt) {
+        if (++kc < leaf_kt) return;
+        kc = 0;
+        ++ld;
+        for (int li = 0; li < g.nl; ++li) {
+            if (g.R[li] == 0 || m0 >= g.ncol[li]) continue;
+            const int sh = g.tau - g.depth[li];
+            if ((i64(g.leaf) << sh) <= g.span) {
+                if ((ld & ((1 << sh) - 1)) == 0) flush(li, ((leaf0 + ld) >> sh) - 1, true);
+            } else if (kt + 1 == ktiles) {
+                flush(li, 0, false);
+            }
+        }
+    });
+}
+
+/// T_l[seg] = sum of the per-span partials of levels wider than the span.
+__global__ void k_cat_reduce(const __grid_constant__ CatArgs g, int li) {
+    const int seg = blockIdx.y;
+    const int R = g.R[li];
+    const i64 blk = i64(R) * g.s;
+    const i64 S = g.n >> g.depth[li];
+    const int cps = int(S / g.span);
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < blk; e += i64(gridDim.x) * blockDim.x) {
+        if (e / R >= g.ncol[li]) continue;
+        double acc = 0.0;
+        for (int c = 0; c < cps; ++c) acc += g.ws[li][i64(seg * cps + c) * blk + e];
+        g.T[li][i64(seg) * blk + e] = acc;
+    }
+}
+
 /// Projection chunk: from ML_CHUNK rows, doubled while >= 8 CTAs per SM remain
 /// (fewer split-K partials to write and fold).
 int proj_chunk(const DTree& t, int nl, int tiles) {
@@ -527,6 +638,84 @@ std::vector<DVecP> hodlr_project(const DHodlr& h, const double* X, i64 ldx, int 
     if (s <= 0 || tau < 1) return out;
     if (tau > MAXL) throw std::length_error("hodlr_project: too many levels");
     auto& c = current();
+    {  // thin bases: one pass over X for all levels (k_proj_cat)
+        int ncat = 0, cmax = 0;
+        for (int l = 1; l <= tau; ++l)
+            if (std::min(s, ncol[static_cast<size_t>(l - 1)]) > 0) {
+                ncat += h.Rl(l);
+                cmax = std::max(cmax, std::min(s, ncol[static_cast<size_t>(l - 1)]));
+            }
+        const i64 leaf = n >> tau;
+        if (ncat > 0 && ncat <= CAT_MAX && tau >= 1 && n % (i64(1) << tau) == 0 && leaf % BK == 0 &&
+            n < (i64(1) << 31) && !std::getenv("HG_NO_PROJ_CAT")) {
+            const int tbm = tile::tile_for(cmax), tbn = tile::tile_for(ncat);
+            const int tiles_m = cdiv(cmax, tbm);
+            i64 span = n;
+            while (span > leaf && (n / span) * tiles_m < 4 * c.num_sms) span /= 2;
+            CatArgs a{};
+            a.X = X;
+            a.ldx = ldx;
+            a.n = n;
+            a.s = s;
+            a.nl = tau;
+            a.ncat = ncat;
+            a.span = int(span);
+            a.tiles_m = tiles_m;
+            a.tau = tau;
+            a.leaf = int(leaf);
+            a.coff[0] = 0;
+            std::vector<DVec> wsb(static_cast<size_t>(tau));
+            double flops = 0;
+            for (int i = 0; i < tau; ++i) {
+                const int l = i + 1, nc = std::min(s, ncol[static_cast<size_t>(i)]);
+                const int R = nc > 0 ? h.Rl(l) : 0;
+                a.P[i] = transpose ? h.Ul(l) : h.Vl(l);
+                a.R[i] = R;
+                a.coff[i + 1] = a.coff[i] + R;
+                a.ncol[i] = nc;
+                a.depth[i] = l;
+                if (R > 0) {
+                    out[static_cast<size_t>(i)] = make_dvec(static_cast<size_t>(t.part(l).nseg()) * R * s, false);
+                    a.T[i] = out[static_cast<size_t>(i)]->get();
+                    if ((n >> l) > span) {
+                        wsb[static_cast<size_t>(i)].alloc(static_cast<size_t>(n / span) * R * s);
+                        a.ws[i] = wsb[static_cast<size_t>(i)].get();
+                    }
+                }
+                flops += 2.0 * double(n) * R * nc;
+            }
+            ProfScope prof(PROF_SEG_TN, flops, 8.0 * double(n) * (cmax + ncat));
+            if (prof_enabled()) prof.key(prof_tag("projcat s=%d ncat=%d span=%d", s, ncat, int(span)));
+            with_tile(tbm, [&](auto TM) {
+                with_tile(tbn, [&](auto TN) {
+                    constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+                    if constexpr (tile::shape_ok(M, N)) {
+                        constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                        static bool once = [] {
+                            HG_CUDA(cudaFuncSetAttribute(k_proj_cat<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         bytes));
+                            return true;
+                        }();
+                        (void)once;
+                        k_proj_cat<M, N><<<dim3(unsigned(n / span), unsigned(tiles_m)), THREADS, bytes, c.stream>>>(a);
+                    } else {
+                        throw std::logic_error("hodlr_project: unsupported tile shape");
+                    }
+                });
+            });
+            HG_LAUNCH();
+            ++c.launches;
+            for (int i = 0; i < tau; ++i)
+                if (a.ws[i]) {
+                    const int nseg = int(n / (n >> (i + 1)));
+                    k_cat_reduce<<<dim3(unsigned(cdiv(i64(a.R[i]) * s, 256 * 4)), unsigned(nseg)), 256, 0, c.stream>>>(a,
+                                                                                                                    i);
+                    HG_LAUNCH();
+                    ++c.launches;
+                }
+            return out;
+        }
+    }
     int rmax0 = 1, cmax0 = 1;
     for (int l = 1; l <= tau; ++l) {
         rmax0 = std::max(rmax0, h.Rl(l));

@@ -144,6 +144,39 @@ __device__ __forceinline__ void run_t(LA& la, LB& lb, int ktiles, double* smem, 
     cp_wait<0>();
 }
 
+/// run_t with a hook called after the MMA of every K tile (flushes of
+/// segmented accumulators).
+template <int NS, int TBM, int TBN, class LA, class LB, class H>
+__device__ __forceinline__ void run_t_hook(LA& la, LB& lb, int ktiles, double* smem,
+                                           typename Shape<TBM, TBN>::Acc& acc, H&& hook) {
+    static_assert(LA::ROWS == TBM && LB::ROWS == TBN, "loader extents must match the tile");
+    constexpr int AE = stage_elems(TBM), BE = stage_elems(TBN);
+    double* As = smem;
+    double* Bs = smem + NS * AE;
+#pragma unroll
+    for (int s = 0; s < NS - 1; ++s) {
+        if (s < ktiles) {
+            la.issue(As + s * AE, s);
+            lb.issue(Bs + s * BE, s);
+        }
+        cp_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_wait<NS - 2>();
+        __syncthreads();
+        const int nk = kt + NS - 1;
+        if (nk < ktiles) {
+            la.issue(As + (nk % NS) * AE, nk);
+            lb.issue(Bs + (nk % NS) * BE, nk);
+        }
+        cp_commit();
+        const int st = kt % NS;
+        mma_stage<LA::KC, LB::KC, TBM, TBN>(As + st * AE, Bs + st * BE, acc);
+        hook(kt);
+    }
+    cp_wait<0>();
+}
+
 /// 64x64 shorthand (kernels written before the shape-adaptive engine).
 template <int NS = STAGES, class LA, class LB>
 __device__ __forceinline__ void run(LA& la, LB& lb, int ktiles, double* smem, Acc& acc) {
