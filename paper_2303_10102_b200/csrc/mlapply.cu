@@ -474,6 +474,93 @@ __global__ void k_cat_reduce(const __grid_constant__ CatArgs g, int li) {
     }
 }
 
+/// k_proj_cat applies: uniform tree (leaves of n >> tau rows, a multiple of
+/// BK), levels [l0, l1] with at most CAT_MAX columns side by side.
+bool proj_cat_ok(const DHodlr& h, int l0, int l1, const int* nc, int ncat) {
+    const i64 n = h.n();
+    const int tau = h.tau();
+    if (ncat <= 0 || ncat > CAT_MAX || tau < 1 || l1 - l0 + 1 > MAXL || n >= (i64(1) << 31)) return false;
+    if (n % (i64(1) << tau) != 0 || (n >> tau) % BK != 0 || std::getenv("HG_NO_PROJ_CAT")) return false;
+    (void)nc;
+    return true;
+}
+
+/// T_l[seg] (R_l x nc_l, ld R_l, segment stride R_l s) = P_l[seg]^T X[seg] for
+/// l in [l0, l1] in one pass over X (P = U when transpose, else V).
+void proj_cat(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose, int l0, int l1, const int* nc,
+              double* const* tout) {
+    auto& c = current();
+    const i64 n = h.n();
+    const int tau = h.tau(), nl = l1 - l0 + 1;
+    const i64 leaf = n >> tau;
+    int ncat = 0, cmax = 0;
+    for (int i = 0; i < nl; ++i)
+        if (nc[i] > 0) {
+            ncat += h.Rl(l0 + i);
+            cmax = std::max(cmax, nc[i]);
+        }
+    const int tbm = tile::tile_for(cmax), tbn = tile::tile_for(ncat);
+    const int tiles_m = cdiv(cmax, tbm);
+    i64 span = n;
+    while (span > leaf && (n / span) * tiles_m < 4 * c.num_sms) span /= 2;
+    CatArgs a{};
+    a.X = X;
+    a.ldx = ldx;
+    a.n = n;
+    a.s = s;
+    a.nl = nl;
+    a.ncat = ncat;
+    a.span = int(span);
+    a.tiles_m = tiles_m;
+    a.tau = tau;
+    a.leaf = int(leaf);
+    a.coff[0] = 0;
+    std::vector<DVec> wsb(static_cast<size_t>(nl));
+    double flops = 0;
+    for (int i = 0; i < nl; ++i) {
+        const int l = l0 + i;
+        const int R = nc[i] > 0 ? h.Rl(l) : 0;
+        a.P[i] = transpose ? h.Ul(l) : h.Vl(l);
+        a.R[i] = R;
+        a.coff[i + 1] = a.coff[i] + R;
+        a.ncol[i] = nc[i];
+        a.depth[i] = l;
+        a.T[i] = tout[i];
+        if (R > 0 && (n >> l) > span) {
+            wsb[static_cast<size_t>(i)].alloc(static_cast<size_t>(n / span) * R * s);
+            a.ws[i] = wsb[static_cast<size_t>(i)].get();
+        }
+        flops += 2.0 * double(n) * R * nc[i];
+    }
+    ProfScope prof(PROF_SEG_TN, flops, 8.0 * double(n) * (cmax + ncat));
+    if (prof_enabled()) prof.key(prof_tag("projcat l=%d..%d s=%d ncat=%d span=%d", l0, l1, s, ncat, int(span)));
+    with_tile(tbm, [&](auto TM) {
+        with_tile(tbn, [&](auto TN) {
+            constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
+            if constexpr (tile::shape_ok(M, N)) {
+                constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
+                static bool once = [] {
+                    HG_CUDA(cudaFuncSetAttribute(k_proj_cat<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+                    return true;
+                }();
+                (void)once;
+                k_proj_cat<M, N><<<dim3(unsigned(n / span), unsigned(tiles_m)), THREADS, bytes, c.stream>>>(a);
+            } else {
+                throw std::logic_error("proj_cat: unsupported tile shape");
+            }
+        });
+    });
+    HG_LAUNCH();
+    ++c.launches;
+    for (int i = 0; i < nl; ++i)
+        if (a.ws[i]) {
+            const int nseg = int(i64(1) << (l0 + i));
+            k_cat_reduce<<<dim3(unsigned(cdiv(i64(a.R[i]) * s, 256 * 4)), unsigned(nseg)), 256, 0, c.stream>>>(a, i);
+            HG_LAUNCH();
+            ++c.launches;
+        }
+}
+
 /// Projection chunk: from ML_CHUNK rows, doubled while >= 8 CTAs per SM remain
 /// (fewer split-K partials to write and fold).
 int proj_chunk(const DTree& t, int nl, int tiles) {
@@ -553,8 +640,19 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
                 break;
         }
         const int b = e - 1;
-        int rmax = 1;
-        for (int i = a; i <= b; ++i) rmax = std::max(rmax, L.R[i]);
+        int rmax = 1, ncat = 0;
+        for (int i = a; i <= b; ++i) {
+            rmax = std::max(rmax, L.R[i]);
+            ncat += L.R[i];
+        }
+        if (!zero.bounds && rmax <= 16) {  // thin run: all its levels in one pass over X
+            std::vector<int> nc(static_cast<size_t>(b - a + 1), s);
+            if (proj_cat_ok(h, lmin + a, lmin + b, nc.data(), ncat)) {
+                proj_cat(h, X, ldx, s, transpose, lmin + a, lmin + b, nc.data(), L.T + a);
+                a = e;
+                continue;
+            }
+        }
         int tbm = tile::tile_for(rmax);
         const int tbn = tile::tile_for_n(s, tbm);
         if (rmax > 32 && rmax <= 40 && tbn % 32 == 0) tbm = 40;  // 1 x 4 warp grid: no padding of rank-40 levels
@@ -639,80 +737,21 @@ std::vector<DVecP> hodlr_project(const DHodlr& h, const double* X, i64 ldx, int 
     if (tau > MAXL) throw std::length_error("hodlr_project: too many levels");
     auto& c = current();
     {  // thin bases: one pass over X for all levels (k_proj_cat)
-        int ncat = 0, cmax = 0;
-        for (int l = 1; l <= tau; ++l)
-            if (std::min(s, ncol[static_cast<size_t>(l - 1)]) > 0) {
-                ncat += h.Rl(l);
-                cmax = std::max(cmax, std::min(s, ncol[static_cast<size_t>(l - 1)]));
-            }
-        const i64 leaf = n >> tau;
-        if (ncat > 0 && ncat <= CAT_MAX && tau >= 1 && n % (i64(1) << tau) == 0 && leaf % BK == 0 &&
-            n < (i64(1) << 31) && !std::getenv("HG_NO_PROJ_CAT")) {
-            const int tbm = tile::tile_for(cmax), tbn = tile::tile_for(ncat);
-            const int tiles_m = cdiv(cmax, tbm);
-            i64 span = n;
-            while (span > leaf && (n / span) * tiles_m < 4 * c.num_sms) span /= 2;
-            CatArgs a{};
-            a.X = X;
-            a.ldx = ldx;
-            a.n = n;
-            a.s = s;
-            a.nl = tau;
-            a.ncat = ncat;
-            a.span = int(span);
-            a.tiles_m = tiles_m;
-            a.tau = tau;
-            a.leaf = int(leaf);
-            a.coff[0] = 0;
-            std::vector<DVec> wsb(static_cast<size_t>(tau));
-            double flops = 0;
-            for (int i = 0; i < tau; ++i) {
-                const int l = i + 1, nc = std::min(s, ncol[static_cast<size_t>(i)]);
-                const int R = nc > 0 ? h.Rl(l) : 0;
-                a.P[i] = transpose ? h.Ul(l) : h.Vl(l);
-                a.R[i] = R;
-                a.coff[i + 1] = a.coff[i] + R;
-                a.ncol[i] = nc;
-                a.depth[i] = l;
-                if (R > 0) {
-                    out[static_cast<size_t>(i)] = make_dvec(static_cast<size_t>(t.part(l).nseg()) * R * s, false);
-                    a.T[i] = out[static_cast<size_t>(i)]->get();
-                    if ((n >> l) > span) {
-                        wsb[static_cast<size_t>(i)].alloc(static_cast<size_t>(n / span) * R * s);
-                        a.ws[i] = wsb[static_cast<size_t>(i)].get();
-                    }
-                }
-                flops += 2.0 * double(n) * R * nc;
-            }
-            ProfScope prof(PROF_SEG_TN, flops, 8.0 * double(n) * (cmax + ncat));
-            if (prof_enabled()) prof.key(prof_tag("projcat s=%d ncat=%d span=%d", s, ncat, int(span)));
-            with_tile(tbm, [&](auto TM) {
-                with_tile(tbn, [&](auto TN) {
-                    constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
-                    if constexpr (tile::shape_ok(M, N)) {
-                        constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
-                        static bool once = [] {
-                            HG_CUDA(cudaFuncSetAttribute(k_proj_cat<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         bytes));
-                            return true;
-                        }();
-                        (void)once;
-                        k_proj_cat<M, N><<<dim3(unsigned(n / span), unsigned(tiles_m)), THREADS, bytes, c.stream>>>(a);
-                    } else {
-                        throw std::logic_error("hodlr_project: unsupported tile shape");
-                    }
-                });
-            });
-            HG_LAUNCH();
-            ++c.launches;
+        std::vector<int> nc(static_cast<size_t>(tau));
+        std::vector<double*> tout(static_cast<size_t>(tau), nullptr);
+        int ncat = 0;
+        for (int i = 0; i < tau; ++i) {
+            nc[static_cast<size_t>(i)] = std::min(s, ncol[static_cast<size_t>(i)]);
+            if (nc[static_cast<size_t>(i)] > 0) ncat += h.Rl(i + 1);
+        }
+        if (proj_cat_ok(h, 1, tau, nc.data(), ncat)) {
             for (int i = 0; i < tau; ++i)
-                if (a.ws[i]) {
-                    const int nseg = int(n / (n >> (i + 1)));
-                    k_cat_reduce<<<dim3(unsigned(cdiv(i64(a.R[i]) * s, 256 * 4)), unsigned(nseg)), 256, 0, c.stream>>>(a,
-                                                                                                                    i);
-                    HG_LAUNCH();
-                    ++c.launches;
+                if (nc[static_cast<size_t>(i)] > 0 && h.Rl(i + 1) > 0) {
+                    out[static_cast<size_t>(i)] =
+                        make_dvec(static_cast<size_t>(t.part(i + 1).nseg()) * h.Rl(i + 1) * s, false);
+                    tout[static_cast<size_t>(i)] = out[static_cast<size_t>(i)]->get();
                 }
+            proj_cat(h, X, ldx, s, transpose, 1, tau, nc.data(), tout.data());
             return out;
         }
     }
