@@ -640,6 +640,7 @@ void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, i
         o.apply_masked(j, X, n, s, Y, n, z);
     } else {
         o.apply(j, X, n, s, Y, n);
+        z.leaf_identity = zparity == -1 && s == H.bmax();  // the leaf sampler
     }
     hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
 }

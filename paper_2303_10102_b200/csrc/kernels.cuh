@@ -83,6 +83,10 @@ struct ZeroRows {
     const int* bounds = nullptr;  // partition bounds of that depth (device)
     int nseg = 0, parity = 0;
     int out_depth = -1;
+    /// hodlr_apply only: X is the leaf sampler, the stacked identities
+    /// X[lo_b + c, c] = 1 (sketch.cpp:25-30), so a level's projection is the
+    /// sum of its panel's leaf blocks over each segment (no GEMM).
+    bool leaf_identity = false;
 };
 
 /// Final host read of a device scalar (synchronizes the stream).

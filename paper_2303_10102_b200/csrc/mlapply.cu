@@ -561,6 +561,94 @@ void proj_cat(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose, 
         }
 }
 
+// ------------------------------------------------ leaf-sampler projections
+constexpr int LID_GL = 256;  // leaves per CTA
+
+struct LeafIdArgs {
+    const int* lb;  // leaf bounds
+    i64 n;
+    int tau, nl, s;
+    const double* P[MAXL];
+    int R[MAXL], depth[MAXL];
+    double* T[MAXL];
+    double* ws[MAXL];  // levels whose segments exceed LID_GL leaves: per-group partials
+};
+
+/// T_l[seg](j, c) = sum over the leaves b of seg of P_l[lo_b + c, j] (c < m_b).
+__global__ void k_leafid_proj(const __grid_constant__ LeafIdArgs a) {
+    const int li = blockIdx.y, R = a.R[li];
+    if (R == 0) return;
+    const int g = blockIdx.x, b0 = g * LID_GL, nleaves = 1 << a.tau;
+    const int Ls = 1 << (a.tau - a.depth[li]);  // leaves per segment
+    const i64 blk = i64(R) * a.s;
+    const double* P = a.P[li];
+    for (int e = threadIdx.x; e < R * a.s; e += blockDim.x) {
+        const int j = e / a.s, c = e - j * a.s;
+        const double* pj = P + i64(j) * a.n + c;
+        if (Ls >= LID_GL) {
+            double acc = 0.0;
+            for (int b = b0; b < min(b0 + LID_GL, nleaves); ++b)
+                if (c < a.lb[b + 1] - a.lb[b]) acc += pj[a.lb[b]];
+            double* o = Ls == LID_GL ? a.T[li] + i64(b0 / Ls) * blk : a.ws[li] + i64(g) * blk;
+            o[j + i64(c) * R] = acc;
+        } else {
+            for (int s0 = b0; s0 < min(b0 + LID_GL, nleaves); s0 += Ls) {
+                double acc = 0.0;
+                for (int b = s0; b < s0 + Ls; ++b)
+                    if (c < a.lb[b + 1] - a.lb[b]) acc += pj[a.lb[b]];
+                a.T[li][i64(s0 / Ls) * blk + j + i64(c) * R] = acc;
+            }
+        }
+    }
+}
+
+__global__ void k_leafid_fold(const __grid_constant__ LeafIdArgs a, int li) {
+    const int seg = blockIdx.y, R = a.R[li];
+    const i64 blk = i64(R) * a.s;
+    const int gps = (1 << (a.tau - a.depth[li])) / LID_GL;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < blk; e += i64(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int q = 0; q < gps; ++q) acc += a.ws[li][i64(seg * gps + q) * blk + e];
+        a.T[li][i64(seg) * blk + e] = acc;
+    }
+}
+
+/// Projections of the leaf sampler for levels [l0, l0 + nl) into T[] (one
+/// streaming pass over each panel instead of a GEMM with an identity stack).
+void leafid_proj(const DHodlr& h, bool transpose, int l0, int nl, int s, double* const* T) {
+    auto& c = current();
+    const DTree& t = *h.tree;
+    const int tau = t.tau(), nleaves = 1 << tau;
+    LeafIdArgs a{};
+    a.lb = t.leaves().dbounds();
+    a.n = h.n();
+    a.tau = tau;
+    a.nl = nl;
+    a.s = s;
+    std::vector<DVec> wsb(static_cast<size_t>(nl));
+    for (int i = 0; i < nl; ++i) {
+        const int l = l0 + i;
+        a.P[i] = transpose ? h.Ul(l) : h.Vl(l);
+        a.R[i] = h.Rl(l);
+        a.depth[i] = l;
+        a.T[i] = T[i];
+        if (a.R[i] > 0 && (nleaves >> l) > LID_GL) {
+            wsb[static_cast<size_t>(i)].alloc(static_cast<size_t>(cdiv(nleaves, LID_GL)) * a.R[i] * s);
+            a.ws[i] = wsb[static_cast<size_t>(i)].get();
+        }
+    }
+    k_leafid_proj<<<dim3(unsigned(cdiv(nleaves, LID_GL)), unsigned(nl)), 256, 0, c.stream>>>(a);
+    HG_LAUNCH();
+    ++c.launches;
+    for (int i = 0; i < nl; ++i)
+        if (a.ws[i]) {
+            k_leafid_fold<<<dim3(unsigned(cdiv(i64(a.R[i]) * s, 1024)), unsigned(1 << (l0 + i))), 256, 0, c.stream>>>(
+                a, i);
+            HG_LAUNCH();
+            ++c.launches;
+        }
+}
+
 /// Projection chunk: from ML_CHUNK rows, doubled while >= 8 CTAs per SM remain
 /// (fewer split-K partials to write and fold).
 int proj_chunk(const DTree& t, int nl, int tiles) {
@@ -616,7 +704,8 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         // algorithmic flops: the projection reads only the nonzero half of X
         // under a ZeroRows hint, the update writes only the rows the caller reads
         const double f = 2.0 * double(n) * R * s;
-        flops += zero.bounds ? 0.5 * f : f;
+        if (!(zero.leaf_identity && s == h.bmax()))  // leaf sampler: the projection is a sum, not a GEMM
+            flops += zero.bounds ? 0.5 * f : f;
         flops += (zero.bounds && zero.out_depth >= 0) ? 0.5 * f : f;
         bytes += 16.0 * double(n) * R;
     }
@@ -626,11 +715,16 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
         prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
     }
+    const bool zero_was_leafid = zero.leaf_identity && s == h.bmax();
+    if (zero_was_leafid) {
+        leafid_proj(h, transpose, lmin, L.nl, s, L.T);
+        zero = ZeroRows{};
+    }
     // Projections in runs of consecutive levels sharing an M tile (a derivative
     // HODLR has ranks 4..8 on most levels and ~45 on the deepest two: one tile
     // for all would pad the thin levels up to 12x).
     auto proj_tile = [&](int R) { return tile::tile_for(std::max(R, 1)); };
-    for (int a = 0; a < L.nl;) {
+    for (int a = (zero_was_leafid ? L.nl : 0); a < L.nl;) {
         int e = a, tb = -1;  // run [a, e): levels with one projection tile (empty levels join any run)
         for (; e < L.nl; ++e) {
             if (L.R[e] == 0) continue;
