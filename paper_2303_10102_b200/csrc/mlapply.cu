@@ -562,7 +562,8 @@ void proj_cat(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose, 
 }
 
 // ------------------------------------------------ leaf-sampler projections
-constexpr int LID_GL = 256;  // leaves per CTA
+constexpr int LID_GL = 32;  // leaves per CTA
+constexpr int LID_J = 8;    // panel columns per CTA (independent accumulators per thread)
 
 struct LeafIdArgs {
     const int* lb;  // leaf bounds
@@ -575,30 +576,34 @@ struct LeafIdArgs {
 };
 
 /// T_l[seg](j, c) = sum over the leaves b of seg of P_l[lo_b + c, j] (c < m_b).
-__global__ void k_leafid_proj(const __grid_constant__ LeafIdArgs a) {
+/// Thread = column c of the leaf block, LID_J panel columns per CTA.
+__global__ void __launch_bounds__(128) k_leafid_proj(const __grid_constant__ LeafIdArgs a) {
     const int li = blockIdx.y, R = a.R[li];
-    if (R == 0) return;
+    const int j0 = blockIdx.z * LID_J;
+    if (j0 >= R) return;
     const int g = blockIdx.x, b0 = g * LID_GL, nleaves = 1 << a.tau;
     const int Ls = 1 << (a.tau - a.depth[li]);  // leaves per segment
     const i64 blk = i64(R) * a.s;
-    const double* P = a.P[li];
-    for (int e = threadIdx.x; e < R * a.s; e += blockDim.x) {
-        const int j = e / a.s, c = e - j * a.s;
-        const double* pj = P + i64(j) * a.n + c;
-        if (Ls >= LID_GL) {
-            double acc = 0.0;
-            for (int b = b0; b < min(b0 + LID_GL, nleaves); ++b)
-                if (c < a.lb[b + 1] - a.lb[b]) acc += pj[a.lb[b]];
-            double* o = Ls == LID_GL ? a.T[li] + i64(b0 / Ls) * blk : a.ws[li] + i64(g) * blk;
-            o[j + i64(c) * R] = acc;
-        } else {
-            for (int s0 = b0; s0 < min(b0 + LID_GL, nleaves); s0 += Ls) {
-                double acc = 0.0;
-                for (int b = s0; b < s0 + Ls; ++b)
-                    if (c < a.lb[b + 1] - a.lb[b]) acc += pj[a.lb[b]];
-                a.T[li][i64(s0 / Ls) * blk + j + i64(c) * R] = acc;
-            }
+    const int c = threadIdx.x;
+    const double* P = a.P[li] + i64(j0) * a.n + c;
+    const int b1 = min(b0 + LID_GL, nleaves);
+    const int seglen = Ls < LID_GL ? Ls : LID_GL;
+    for (int s0 = b0; s0 < b1; s0 += seglen) {
+        double acc[LID_J];
+#pragma unroll
+        for (int q = 0; q < LID_J; ++q) acc[q] = 0.0;
+        for (int b = s0; b < min(s0 + seglen, b1); ++b) {
+            const int lo = a.lb[b], m = a.lb[b + 1] - lo;
+            if (c >= m || c >= a.s) continue;
+#pragma unroll
+            for (int q = 0; q < LID_J; ++q)
+                if (j0 + q < R) acc[q] += P[lo + i64(q) * a.n];
         }
+        if (c >= a.s) continue;
+        double* o = Ls <= LID_GL ? a.T[li] + i64(s0 / Ls) * blk : a.ws[li] + i64(g) * blk;
+#pragma unroll
+        for (int q = 0; q < LID_J; ++q)
+            if (j0 + q < R) o[(j0 + q) + i64(c) * R] = acc[q];
     }
 }
 
@@ -637,7 +642,11 @@ void leafid_proj(const DHodlr& h, bool transpose, int l0, int nl, int s, double*
             a.ws[i] = wsb[static_cast<size_t>(i)].get();
         }
     }
-    k_leafid_proj<<<dim3(unsigned(cdiv(nleaves, LID_GL)), unsigned(nl)), 256, 0, c.stream>>>(a);
+    int rmax = 1;
+    for (int i = 0; i < nl; ++i) rmax = std::max(rmax, a.R[i]);
+    if (s > 128) throw std::logic_error("leafid_proj: leaves wider than 128 rows");
+    k_leafid_proj<<<dim3(unsigned(cdiv(nleaves, LID_GL)), unsigned(nl), unsigned(cdiv(rmax, LID_J))), 128, 0,
+                    c.stream>>>(a);
     HG_LAUNCH();
     ++c.launches;
     for (int i = 0; i < nl; ++i)
@@ -704,7 +713,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         // algorithmic flops: the projection reads only the nonzero half of X
         // under a ZeroRows hint, the update writes only the rows the caller reads
         const double f = 2.0 * double(n) * R * s;
-        if (!(zero.leaf_identity && s == h.bmax()))  // leaf sampler: the projection is a sum, not a GEMM
+        if (!(zero.leaf_identity && s == h.bmax() && s <= 128))  // leaf sampler: the projection is a sum, not a GEMM
             flops += zero.bounds ? 0.5 * f : f;
         flops += (zero.bounds && zero.out_depth >= 0) ? 0.5 * f : f;
         bytes += 16.0 * double(n) * R;
@@ -715,7 +724,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
         prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
     }
-    const bool zero_was_leafid = zero.leaf_identity && s == h.bmax();
+    const bool zero_was_leafid = zero.leaf_identity && s == h.bmax() && s <= 128;
     if (zero_was_leafid) {
         leafid_proj(h, transpose, lmin, L.nl, s, L.T);
         zero = ZeroRows{};
