@@ -147,12 +147,21 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
                 dot_panels(n, cw, corr.Cv->get() + i64(c0) * n, n, Y.get(), n, out, true);
             }
         }
-        int rmax = 0;
-        for (int l = 1; l <= tau; ++l) rmax = std::max(rmax, h.Rl(l));
-        if (rmax <= 16) {  // skinny base: all levels' projections in one pass over Cv / Cu
-            std::vector<int> W(static_cast<size_t>(tau));
-            for (int l = 1; l <= tau; ++l)
-                W[static_cast<size_t>(l - 1)] = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
+        // Thin levels (rank <= 16: the sigma^2 derivative everywhere, the ell
+        // derivative on all but its deepest levels) take their projections of
+        // Cv / Cu together in one pass (hodlr_project -> k_proj_cat); wider
+        // levels one segmented GEMM pair each.
+        std::vector<int> W(static_cast<size_t>(tau), 0);
+        bool any_thin = false;
+        for (int l = 1; l <= tau; ++l) {
+            const int R = h.Rl(l);
+            const int w = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
+            if (R > 0 && R <= 16 && w > 0) {
+                W[static_cast<size_t>(l - 1)] = w;
+                any_thin = true;
+            }
+        }
+        if (any_thin) {
             auto P = hodlr_project(h, corr.Cv->get(), n, corr.sumC, true, W);
             auto Q = hodlr_project(h, corr.Cu->get(), n, corr.sumC, false, W);
             for (int l = 1; l <= tau; ++l) {
@@ -163,18 +172,17 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
                     seg_xor_dot(p.nseg(), 1, P[static_cast<size_t>(l - 1)]->get(), Q[static_cast<size_t>(l - 1)]->get(),
                                 i64(R) * corr.sumC, R, R, w, out, true);
             }
-            return;
         }
         for (int l = 1; l <= tau; ++l) {
             const int R = h.Rl(l);
-            const int W = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
-            if (!R || !W) continue;
+            const int Wl = corr.coff[static_cast<size_t>(l - 1)] + corr.C[static_cast<size_t>(l - 1)];
+            if (!R || !Wl || W[static_cast<size_t>(l - 1)]) continue;
             const Partition& p = t.part(l);
-            const size_t sz = static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(W);
+            const size_t sz = static_cast<size_t>(p.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(Wl);
             DVec P(sz), Q(sz);
-            seg_tn(p, h.Ul(l), n, R, corr.Cv->get(), n, W, P.get(), i64(R) * W, R, alpha);
-            seg_tn(p, h.Vl(l), n, R, corr.Cu->get(), n, W, Q.get(), i64(R) * W, R);
-            seg_xor_dot(p.nseg(), 1, P.get(), Q.get(), i64(R) * W, R, R, W, out, true);
+            seg_tn(p, h.Ul(l), n, R, corr.Cv->get(), n, Wl, P.get(), i64(R) * Wl, R, alpha);
+            seg_tn(p, h.Vl(l), n, R, corr.Cu->get(), n, Wl, Q.get(), i64(R) * Wl, R);
+            seg_xor_dot(p.nseg(), 1, P.get(), Q.get(), i64(R) * Wl, R, R, Wl, out, true);
         }
     };
     if (same) {
