@@ -69,16 +69,27 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
     const double downdate_thr = sqrt(DBL_EPSILON);
     for (int k = 0; k < nsz; ++k) {
         if (PIVOT) {
-            if (tid == 0) {
+            if (warp == 0) {  // first index of the largest norm (Eigen's maxCoeff), warp argmax
                 int best = k;
-                double bv = nu[k];
-                for (int j = k + 1; j < w; ++j)
+                double bv = -1.0;
+                for (int j = k + lane; j < w; j += 32)
                     if (nu[j] > bv) {
                         bv = nu[j];
                         best = j;
                     }
-                s_best = best;
-                trans[k] = best;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, best, o);
+                    if (ov > bv || (ov == bv && oi < best)) {
+                        bv = ov;
+                        best = oi;
+                    }
+                }
+                if (lane == 0) {
+                    s_best = best;
+                    trans[k] = best;
+                }
             }
             __syncthreads();
             const int best = s_best;
