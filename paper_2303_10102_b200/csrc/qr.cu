@@ -18,16 +18,11 @@ __device__ double qr_block_sum(double v) {
     __shared__ double sh[32];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
+    __syncthreads();  // sh free (previous call's readers are done)
     if (lane == 0) sh[wid] = v;
     __syncthreads();
-    double t = 0.0;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
-    __syncthreads();
-    if (threadIdx.x == 0) sh[0] = t;
-    __syncthreads();
-    t = sh[0];
+    double t = 0.0;  // every thread folds the warp sums in the same order (identical result)
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
     return t;
 }
 
@@ -256,6 +251,9 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_QR, 2.0 * rows * w * w, 16.0 * rows * w);
     if (prof_enabled()) prof.key(prof_tag("qr%d w=%d blocks=%d rows=%d", int(pivot), w, int(blocks.size()), max_rows));
+    // short blocks: fewer threads per CTA (more CTAs per SM, cheaper barriers)
+    // (the trailing update runs a warp per column: wide blocks keep 16 warps)
+    const int qnt = max_rows <= 64 ? 128 : (max_rows <= 256 && w <= 48) ? 256 : QNT;
     if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS) {
         // wide blocks that do not fit shared memory: blocked compact-WY QR
         const size_t sb = qb_smem(max_rows, w);
@@ -265,11 +263,11 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     } else if (pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<true>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_qr<true><<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, smem_elems);
+        k_qr<true><<<unsigned(blocks.size()), qnt, smem, c.stream>>>(dd.get(), w, smem_elems);
     } else {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<false>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_qr<false><<<unsigned(blocks.size()), QNT, smem, c.stream>>>(dd.get(), w, smem_elems);
+        k_qr<false><<<unsigned(blocks.size()), qnt, smem, c.stream>>>(dd.get(), w, smem_elems);
     }
     HG_LAUNCH();
     ++c.launches;
