@@ -248,6 +248,41 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     });
 }
 
+__device__ double block_sum(double v);
+
+/// Partial sums of sum((L_b X) .* Z) over the leaves: the leaf products are
+/// never stored (the cross-term leaf part of trace_pair, product_rep.cpp:212-224).
+/// Each CTA runs `tiles_per` column tiles of one 64-row leaf tile and writes
+/// one partial (fixed order => deterministic).
+template <int TBN>
+__global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, const double* Z, i64 ldz, int tiles_per,
+                                                         double* partial) {
+    extern __shared__ double smem[];
+    const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * BM;
+    double part = 0.0;
+    if (r0 < m) {
+        const double* Lb = g.L + i64(b) * g.lstride;
+        const int ntiles = cdiv_d(g.w, TBN);
+        const int t1 = min(ntiles, int(blockIdx.y + 1) * tiles_per);
+        for (int tn = int(blockIdx.y) * tiles_per; tn < t1; ++tn) {
+            const int n0 = tn * TBN;
+            tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
+            tile::LoadMCT<BM> la{Lb + r0, g.ldl, m - r0, m};
+            typename tile::Shape<BM, TBN>::Acc acc;
+            acc.zero();
+            tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
+            __syncthreads();  // every warp is done with the stages before the next tile refills them
+            tile::for_each_slot<BM, TBN>(acc, [&](double& v, int mi0, int ni) {
+                const int mi = r0 + mi0, n = n0 + ni;
+                if (n < g.w && mi < m) part = fma(v, Z[i64(lo + mi) + i64(n) * ldz], part);
+            });
+        }
+    }
+    part = block_sum(part);
+    if (threadIdx.x == 0) partial[blockIdx.x + i64(blockIdx.y) * gridDim.x] = g.alpha * part;
+}
+
 // ------------------------------------------------------------ elementwise
 /// Y = alpha X + beta Y; grid (row blocks, column groups), no 64-bit div/mod.
 __global__ void k_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
@@ -557,6 +592,34 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
     });
     HG_LAUNCH();
     ++c.launches;
+}
+
+void leaf_mm_dot(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
+                 const double* Z, i64 ldz, int w, double alpha, double* out, bool accumulate) {
+    if (w <= 0) {
+        if (!accumulate) HG_CUDA(cudaMemsetAsync(out, 0, sizeof(double), current().stream));
+        return;
+    }
+    auto& c = current();
+    const int rt = cdiv(leaves.max_seg(), BM);
+    const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
+    ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + 2.0 * rows * w));
+    if (prof_enabled()) prof.key(prof_tag("leafmmdot w=%d", w));
+    LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, nullptr, 0, w, alpha, 0.0};
+    const int tbn = tile::tile_for_n(w, BM);
+    with_tile(tbn, [&](auto TN) {
+        constexpr int N = decltype(TN)::value;
+        constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
+        const int ntiles = cdiv(w, N), tiles_per = std::min(ntiles, 4);
+        const dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(ntiles, tiles_per)));
+        DVec partial(static_cast<size_t>(grid.x) * grid.y);
+        attr_once<k_leaf_mm_dot<N>>(bytes);
+        k_leaf_mm_dot<N><<<grid, THREADS, bytes, c.stream>>>(g, Z, ldz, tiles_per, partial.get());
+        HG_LAUNCH();
+        k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), int(grid.x * grid.y), out, accumulate ? 1 : 0);
+        HG_LAUNCH();
+        c.launches += 2;
+    });
 }
 
 void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {

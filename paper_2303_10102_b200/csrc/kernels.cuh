@@ -52,6 +52,10 @@ void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 l
 void seg_dot(int nseg, int xr, const double* A, i64 gsa, const double* B, i64 gsb, i64 len, double* out,
              bool accumulate);
 
+/// out[0] (+)= alpha sum((L_b X) .* Z) over the leaves (no n x w product stored).
+void leaf_mm_dot(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
+                 const double* Z, i64 ldz, int w, double alpha, double* out, bool accumulate);
+
 /// out[0] (+)= sum(A .* B) over n x w (deterministic).
 void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate);
 

@@ -137,16 +137,9 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
     // (two projections per level and a sibling dot; no n x C products).
     auto cross = [&](const DHodlr& h, const DProductRep& corr, double alpha) {
         if (!corr.sumC) return;
-        if (!h.leaves_zero) {
-            constexpr int CH = 256;
-            DVec Y(static_cast<size_t>(n) * static_cast<size_t>(std::min(corr.sumC, CH)));
-            for (int c0 = 0; c0 < corr.sumC; c0 += CH) {
-                const int cw = std::min(CH, corr.sumC - c0);
-                leaf_mm(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), false, corr.Cu->get() + i64(c0) * n, n,
-                        Y.get(), n, cw, alpha, 0.0);
-                dot_panels(n, cw, corr.Cv->get() + i64(c0) * n, n, Y.get(), n, out, true);
-            }
-        }
+        if (!h.leaves_zero)  // tr(Cv^T Leaves Cu), the leaf products reduced in the GEMM epilogue
+            leaf_mm_dot(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), corr.Cu->get(), n, corr.Cv->get(), n,
+                        corr.sumC, alpha, out, true);
         // Thin levels (rank <= 16: the sigma^2 derivative everywhere, the ell
         // derivative on all but its deepest levels) take their projections of
         // Cv / Cu together in one pass (hodlr_project -> k_proj_cat); wider
