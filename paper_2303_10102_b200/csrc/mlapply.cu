@@ -577,7 +577,7 @@ struct LeafIdArgs {
 
 /// T_l[seg](j, c) = sum over the leaves b of seg of P_l[lo_b + c, j] (c < m_b).
 /// Thread = column c of the leaf block, LID_J panel columns per CTA.
-__global__ void __launch_bounds__(128) k_leafid_proj(const __grid_constant__ LeafIdArgs a) {
+__global__ void __launch_bounds__(256) k_leafid_proj(const __grid_constant__ LeafIdArgs a) {
     const int li = blockIdx.y, R = a.R[li];
     const int j0 = blockIdx.z * LID_J;
     if (j0 >= R) return;
@@ -644,8 +644,9 @@ void leafid_proj(const DHodlr& h, bool transpose, int l0, int nl, int s, double*
     }
     int rmax = 1;
     for (int i = 0; i < nl; ++i) rmax = std::max(rmax, a.R[i]);
-    if (s > 128) throw std::logic_error("leafid_proj: leaves wider than 128 rows");
-    k_leafid_proj<<<dim3(unsigned(cdiv(nleaves, LID_GL)), unsigned(nl), unsigned(cdiv(rmax, LID_J))), 128, 0,
+    if (s > 256) throw std::logic_error("leafid_proj: leaves wider than 256 rows");
+    const int nt = (s + 31) / 32 * 32;  // thread = column of the leaf block
+    k_leafid_proj<<<dim3(unsigned(cdiv(nleaves, LID_GL)), unsigned(nl), unsigned(cdiv(rmax, LID_J))), nt, 0,
                     c.stream>>>(a);
     HG_LAUNCH();
     ++c.launches;
@@ -713,7 +714,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         // algorithmic flops: the projection reads only the nonzero half of X
         // under a ZeroRows hint, the update writes only the rows the caller reads
         const double f = 2.0 * double(n) * R * s;
-        if (!(zero.leaf_identity && s == h.bmax() && s <= 128))  // leaf sampler: the projection is a sum, not a GEMM
+        if (!(zero.leaf_identity && s == h.bmax() && s <= 256))  // leaf sampler: the projection is a sum, not a GEMM
             flops += zero.bounds ? 0.5 * f : f;
         flops += (zero.bounds && zero.out_depth >= 0) ? 0.5 * f : f;
         bytes += 16.0 * double(n) * R;
@@ -724,7 +725,7 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         for (int l = lmin; l <= lmax; ++l) rmax = std::max(rmax, h.Rl(l));
         prof.key(prof_tag("mlapply l=%d..%d s=%d Rmax=%d tr=%d", lmin, lmax, s, rmax, int(transpose)));
     }
-    const bool zero_was_leafid = zero.leaf_identity && s == h.bmax() && s <= 128;
+    const bool zero_was_leafid = zero.leaf_identity && s == h.bmax() && s <= 256;
     if (zero_was_leafid) {
         leafid_proj(h, transpose, lmin, L.nl, s, L.T);
         zero = ZeroRows{};
