@@ -513,6 +513,21 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
         count_launch();
         return;
     }
+    if (f.all_llt && f.bmax() <= TS2_MAX) {  // 129..256-row leaves: 2 x 2 blocks
+        static bool attr2 = false;
+        if (!attr2) {
+            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc2), TS2_SMEM);
+            attr2 = true;
+        }
+        const int ct = cdiv(w, TS_NC);
+        const int groups = std::max(1, std::min(ct, cdiv(4 * current().num_sms, lv.nseg())));
+        const int cpt = cdiv(ct, groups);
+        LeafSolveTcArgs a{lv.dbounds(), f.bmax(), f.leaf_fac->get(), Y, ldy, w, ct, cpt};
+        k_leaf_solve_tc2<<<unsigned(lv.nseg()) * unsigned(cdiv(ct, cpt)), TS_THREADS, TS2_SMEM, current().stream>>>(a);
+        HG_LAUNCH();
+        count_launch();
+        return;
+    }
     set_smem(reinterpret_cast<const void*>(k_leaf_solve), smem);
     LeafSolveArgs g{lv.dbounds(), f.bmax(), f.leaf_fac->get(), f.leaf_kind->get(), f.leaf_piv->get(), Y, ldy, w};
     dim3 grid(unsigned(lv.nseg()), unsigned(cdiv(w, SOLVE_COLS)));
@@ -603,8 +618,9 @@ DFactor factorize(const DHodlr& h, int orient) {
         count_launch();
         const std::vector<int> kinds = f.leaf_kind->download();
         f.all_llt = std::all_of(kinds.begin(), kinds.end(), [](int k) { return k == 1; });
-        if (f.all_llt && bm <= TS_MAX) {  // tensor-core solve path: invert diagonal blocks once
-            k_leaf_diag_inv<<<unsigned(nl), 128, 0, current().stream>>>(lv.dbounds(), bm, f.leaf_fac->get());
+        if (f.all_llt && bm <= TS2_MAX) {  // tensor-core solve path: invert diagonal blocks once
+            k_leaf_diag_inv<<<unsigned(nl), 16 * ((bm + 15) / 16), 0, current().stream>>>(lv.dbounds(), bm,
+                                                                                          f.leaf_fac->get());
             HG_LAUNCH();
             count_launch();
         }

@@ -38,8 +38,8 @@ struct LeafSolveTcArgs {
 /// In place: every 16x16 diagonal block of each leaf's Cholesky factor ->
 /// its inverse (lower triangular, strict upper part zeroed). One CTA per
 /// leaf, thread (block jb, column c).
-__global__ void __launch_bounds__(128) k_leaf_diag_inv(const int* bounds, int bmax, double* fac) {
-    __shared__ double Ls[8][16][17];
+__global__ void __launch_bounds__(256) k_leaf_diag_inv(const int* bounds, int bmax, double* fac) {
+    __shared__ double Ls[16][16][17];  // up to 256-row leaves (blockDim = 16 per diagonal block)
     const int b = blockIdx.x, m = bounds[b + 1] - bounds[b];
     const int jb = threadIdx.x >> 4, c = threadIdx.x & 15;
     const int r0 = 16 * jb, mb = min(16, m - r0);
@@ -84,37 +84,17 @@ __device__ __forceinline__ void ts_load_factor(double* L, const double* F, int l
     }
 }
 
-__global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs g) {
-    extern __shared__ double sm[];
-    double* Ys = sm;
-    double* Ls = sm + TS_MAX * TS_YLD;
-    const int groups = (g.ctiles + g.cpt - 1) / g.cpt;
-    const int b = blockIdx.x / groups, grp = blockIdx.x % groups;
-    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, mp = (m + 15) & ~15, nb = mp / 16;
-    const double* F = g.fac + i64(b) * g.bmax * g.bmax;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+/// Forward substitution L x = b on rows [row0, row0 + mp) of the RHS tile
+/// (this warp's 8 columns) against the packed factor Ls of mp rows.
+__device__ __forceinline__ void ts_forward(const double* Ls, int mp, double* Ys, int row0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
-    ts_load_factor(Ls, F, g.bmax, m, mp);  // once for all of this CTA's column tiles
-    const int ct_end = min(g.ctiles, (grp + 1) * g.cpt);
-    for (int ct = grp * g.cpt; ct < ct_end; ++ct) {
-    const int c0 = ct * TS_NC, nc = min(TS_NC, g.w - c0);
-    for (int e = tid; e < mp * TS_NC; e += TS_THREADS) {
-        const int r = e % mp, c = e / mp;
-        double* d = Ys + r * TS_YLD + c;
-        if (r < m && c < nc)
-            tile::cp_async8(d, g.Y + (lo + r) + i64(c0 + c) * g.ldy, true);
-        else
-            *d = 0.0;
-    }
-    tile::cp_commit();
-    tile::cp_wait<0>();
-    __syncthreads();
-    // From here on every warp works on its own 8 columns: no block barriers.
+    const int nb = mp / 16;
     // ---- forward: L x = b
     for (int j = 0; j < nb; ++j) {
         const double* P = Ls + ts_poff(j, mp);
         const int ld = mp - 16 * j + 4;
-        double* Yj = Ys + 16 * j * TS_YLD + n0;
+        double* Yj = Ys + (row0 + 16 * j) * TS_YLD + n0;
         {  // x_j = L_jj^{-1} y_j
             double yb[4], x0[2] = {0.0, 0.0}, x1[2] = {0.0, 0.0};
 #pragma unroll
@@ -155,11 +135,18 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs
             }
         __syncwarp();
     }
+}
+
+/// Backward substitution L^T x = y on rows [row0, row0 + mp) (see ts_forward).
+__device__ __forceinline__ void ts_backward(const double* Ls, int mp, double* Ys, int row0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
+    const int nb = mp / 16;
     // ---- backward: L^T x = y
     for (int j = nb - 1; j >= 0; --j) {
         const double* P = Ls + ts_poff(j, mp);
         const int ld = mp - 16 * j + 4;
-        double* Yj = Ys + 16 * j * TS_YLD + n0;
+        double* Yj = Ys + (row0 + 16 * j) * TS_YLD + n0;
         // r_j = y_j - L[16(j+1):, 16j:16j+16]^T x_{>j}
         const int K = mp - 16 * (j + 1);
         double a0[2] = {0.0, 0.0}, a1[2] = {0.0, 0.0}, b0[2] = {0.0, 0.0}, b1[2] = {0.0, 0.0};
@@ -201,11 +188,173 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs
             __syncwarp();
         }
     }
+}
+
+__global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs g) {
+    extern __shared__ double sm[];
+    double* Ys = sm;
+    double* Ls = sm + TS_MAX * TS_YLD;
+    const int groups = (g.ctiles + g.cpt - 1) / g.cpt;
+    const int b = blockIdx.x / groups, grp = blockIdx.x % groups;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, mp = (m + 15) & ~15, nb = mp / 16;
+    const double* F = g.fac + i64(b) * g.bmax * g.bmax;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
+    ts_load_factor(Ls, F, g.bmax, m, mp);  // once for all of this CTA's column tiles
+    const int ct_end = min(g.ctiles, (grp + 1) * g.cpt);
+    for (int ct = grp * g.cpt; ct < ct_end; ++ct) {
+    const int c0 = ct * TS_NC, nc = min(TS_NC, g.w - c0);
+    for (int e = tid; e < mp * TS_NC; e += TS_THREADS) {
+        const int r = e % mp, c = e / mp;
+        double* d = Ys + r * TS_YLD + c;
+        if (r < m && c < nc)
+            tile::cp_async8(d, g.Y + (lo + r) + i64(c0 + c) * g.ldy, true);
+        else
+            *d = 0.0;
+    }
+    tile::cp_commit();
+    tile::cp_wait<0>();
+    __syncthreads();
+    // From here on every warp works on its own 8 columns: no block barriers.
+    ts_forward(Ls, mp, Ys, 0);
+    ts_backward(Ls, mp, Ys, 0);
     __syncthreads();
     for (int e = tid; e < m * nc; e += TS_THREADS) {
         const int r = e % m, c = e / m;
         g.Y[(lo + r) + i64(c0 + c) * g.ldy] = Ys[r * TS_YLD + c];
     }
     __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// Leaves of 129..256 rows: 2 x 2 blocks of at most 128 rows,
+//   L = [L11 0; L21 L22]:  forward  x1 = L11^-1 b1, b2 -= L21 x1, x2 = L22^-1 b2
+//                          backward x2 = L22^-T y2, y1 -= L21^T x2, x1 = L11^-T y1
+// with the packed 128-row machinery above for the diagonal blocks (one of
+// them resident at a time) and the couplings as DMMA products against L21
+// streamed through shared memory in 16-column panels (double-buffered).
+constexpr int TS2_MAX = 256, TS2_CLD = 128 + 4;
+constexpr size_t TS2_SMEM = (size_t(TS2_MAX) * TS_YLD + TS_LSIZE + 2 * 16 * TS2_CLD) * sizeof(double);
+
+/// Thread-cooperative cp.async of a 16 x 128 coupling panel into Cb (ld TS2_CLD):
+/// TRANS = false: Cb[k][r] = L21[r, 16 pk + k]  (forward, rows r < m2)
+/// TRANS = true:  Cb[k][i] = L21[16 pk + k, i]  (backward, k < m2 - 16 pk)
+template <bool TRANS>
+__device__ __forceinline__ void ts2_panel(double* Cb, const double* F, int ldf, int m2, int pk) {
+    for (int e = threadIdx.x; e < 16 * 128; e += TS_THREADS) {
+        const int k = TRANS ? (e & 15) : (e >> 7), r = TRANS ? (e >> 4) : (e & 127);
+        double* d = Cb + k * TS2_CLD + r;
+        const int gr = TRANS ? 128 + 16 * pk + k : 128 + r, gc = TRANS ? r : 16 * pk + k;
+        const bool v = TRANS ? (16 * pk + k < m2) : (r < m2);
+        if (v)
+            tile::cp_async8(d, F + gr + i64(gc) * ldf, true);
+        else
+            *d = 0.0;
+    }
+}
+
+/// acc[t] (rows 8t + g8 of the target half) += A_panel x (16 rows of the source half).
+__device__ __forceinline__ void ts2_couple(const double* Cb, const double* Xs, double (&acc)[16][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
+    double xb[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) xb[kk] = Xs[(4 * kk + t4) * TS_YLD + n0 + g8];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) tile::dmma(acc[t], Cb[(4 * kk + t4) * TS2_CLD + 8 * t + g8], xb[kk]);
+}
+
+/// Y[row0 + 8t + g8, n0 + 2t4 + e] -= acc (this warp's columns)
+__device__ __forceinline__ void ts2_sub(double* Ys, int row0, int rows, const double (&acc)[16][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+        if (8 * t + g8 < rows) {
+            double* y = Ys + (row0 + 8 * t + g8) * TS_YLD + n0 + 2 * t4;
+            y[0] -= acc[t][0];
+            y[1] -= acc[t][1];
+        }
+}
+
+template <bool TRANS>
+__device__ __forceinline__ void ts2_coupling(double* Cb, const double* F, int ldf, int m2, double* Ys, int src0,
+                                             int dst0, int dst_rows) {
+    double acc[16][2];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int npk = TRANS ? (m2 + 15) / 16 : 8;
+    ts2_panel<TRANS>(Cb, F, ldf, m2, 0);
+    tile::cp_commit();
+    for (int pk = 0; pk < npk; ++pk) {
+        double* cur = Cb + (pk & 1) * 16 * TS2_CLD;
+        if (pk + 1 < npk) ts2_panel<TRANS>(Cb + ((pk + 1) & 1) * 16 * TS2_CLD, F, ldf, m2, pk + 1);
+        tile::cp_commit();
+        tile::cp_wait<1>();
+        __syncthreads();
+        ts2_couple(cur, Ys + (src0 + 16 * pk) * TS_YLD, acc);
+        __syncthreads();
+    }
+    tile::cp_wait<0>();
+    ts2_sub(Ys, dst0, dst_rows, acc);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(TS_THREADS, 1) k_leaf_solve_tc2(LeafSolveTcArgs g) {
+    extern __shared__ double sm[];
+    double* Ys = sm;
+    double* Ls = Ys + TS2_MAX * TS_YLD;
+    double* Cb = Ls + TS_LSIZE;
+    const int groups = (g.ctiles + g.cpt - 1) / g.cpt;
+    const int b = blockIdx.x / groups, grp = blockIdx.x % groups;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo;
+    const int m1 = min(m, 128), m2 = max(m - 128, 0);
+    const int mp1 = (m1 + 15) & ~15, mp2 = (m2 + 15) & ~15;
+    const double* F = g.fac + i64(b) * g.bmax * g.bmax;
+    const double* F22 = F + 128 + i64(128) * g.bmax;
+    const int tid = threadIdx.x;
+    const int ct_end = min(g.ctiles, (grp + 1) * g.cpt);
+    for (int ct = grp * g.cpt; ct < ct_end; ++ct) {
+        const int c0 = ct * TS_NC, nc = min(TS_NC, g.w - c0);
+        for (int e = tid; e < (mp1 + mp2) * TS_NC; e += TS_THREADS) {
+            const int c = e / (mp1 + mp2), r = e - c * (mp1 + mp2);
+            const int gr = r < mp1 ? r : 128 + (r - mp1);  // tile rows: [0, mp1) top, then the bottom half at 128
+            double* d = Ys + (r < mp1 ? r : 128 + (r - mp1)) * TS_YLD + c;
+            if (gr < m && c < nc && (r < mp1 ? r < m1 : true))
+                tile::cp_async8(d, g.Y + (lo + gr) + i64(c0 + c) * g.ldy, true);
+            else
+                *d = 0.0;
+        }
+        ts_load_factor(Ls, F, g.bmax, m1, mp1);
+        tile::cp_commit();
+        tile::cp_wait<0>();
+        __syncthreads();
+        ts_forward(Ls, mp1, Ys, 0);
+        __syncthreads();
+        if (m2 > 0) {
+            ts2_coupling<false>(Cb, F, g.bmax, m2, Ys, 0, 128, m2);  // b2 -= L21 x1
+            ts_load_factor(Ls, F22, g.bmax, m2, mp2);
+            tile::cp_commit();
+            tile::cp_wait<0>();
+            __syncthreads();
+            ts_forward(Ls, mp2, Ys, 128);
+            ts_backward(Ls, mp2, Ys, 128);
+            __syncthreads();
+            ts2_coupling<true>(Cb, F, g.bmax, m2, Ys, 128, 0, 128);  // y1 -= L21^T x2
+            ts_load_factor(Ls, F, g.bmax, m1, mp1);
+            tile::cp_commit();
+            tile::cp_wait<0>();
+            __syncthreads();
+        }
+        ts_backward(Ls, mp1, Ys, 0);
+        __syncthreads();
+        for (int e = tid; e < m * nc; e += TS_THREADS) {
+            const int c = e / m, r = e - c * m;
+            g.Y[(lo + r) + i64(c0 + c) * g.ldy] = Ys[r * TS_YLD + c];
+        }
+        __syncthreads();
     }
 }
