@@ -107,27 +107,22 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
         }
         double part = 0.0;
         for (int i = k + 1 + tid; i < rows; i += blockDim.x) part += W[i + k * ldw] * W[i + k * ldw];
+        const double c0 = W[k + k * ldw];  // read before the sum's barriers (thread 0 rewrites it below)
         const double tail = qr_block_sum(part);
-        if (tid == 0) {
-            const double c0 = W[k + k * ldw];
-            if (tail <= DBL_MIN) {
-                s_tau = 0.0;
-                s_zero = 1;
-                s_div = 1.0;
-            } else {
-                double beta = sqrt(c0 * c0 + tail);
-                if (c0 >= 0.0) beta = -beta;
-                s_div = c0 - beta;
-                s_tau = (beta - c0) / beta;
-                s_zero = 0;
-                W[k + k * ldw] = beta;
-            }
-            d.tau[k] = s_tau;
+        // every thread derives the reflector from the same sum (no extra barrier)
+        const bool zero = tail <= DBL_MIN;
+        double tau = 0.0, div = 1.0, beta = c0;
+        if (!zero) {
+            beta = sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            div = c0 - beta;
+            tau = (beta - c0) / beta;
         }
-        __syncthreads();
-        const double tau = s_tau;
-        for (int i = k + 1 + tid; i < rows; i += blockDim.x)
-            W[i + k * ldw] = s_zero ? 0.0 : W[i + k * ldw] / s_div;
+        if (tid == 0) {
+            if (!zero) W[k + k * ldw] = beta;
+            d.tau[k] = tau;
+        }
+        for (int i = k + 1 + tid; i < rows; i += blockDim.x) W[i + k * ldw] = zero ? 0.0 : W[i + k * ldw] / div;
         __syncthreads();
         for (int j = k + 1 + warp; j < w; j += nwarps) {
             double* cj = W + j * ldw;

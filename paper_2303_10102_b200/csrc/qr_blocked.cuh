@@ -226,27 +226,23 @@ __global__ void __launch_bounds__(QB_THREADS, 3) k_qr_blocked(const QrDesc* desc
         for (int i = 0; i < jb; ++i) {
             double part = 0.0;
             for (int r = i + 1 + tid; r < nr; r += blockDim.x) part += S.P[r + i * ld] * S.P[r + i * ld];
+            const double c0 = S.P[i + i * ld];  // read before the sum's barriers (thread 0 rewrites it below)
             const double tail = qr_block_sum(part);
-            if (tid == 0) {
-                const double c0 = S.P[i + i * ld];
-                if (tail <= DBL_MIN) {
-                    s_tau = 0.0;
-                    s_zero = 1;
-                    s_div = 1.0;
-                } else {
-                    double beta = sqrt(c0 * c0 + tail);
-                    if (c0 >= 0.0) beta = -beta;
-                    s_div = c0 - beta;
-                    s_tau = (beta - c0) / beta;
-                    s_zero = 0;
-                    S.P[i + i * ld] = beta;
-                }
-                d.tau[p0 + i] = s_tau;
-                S.tau[i] = s_tau;
+            // every thread derives the reflector from the same sum (no extra barrier)
+            const bool zero = tail <= DBL_MIN;
+            double tau = 0.0, div = 1.0, beta = c0;
+            if (!zero) {
+                beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0.0) beta = -beta;
+                div = c0 - beta;
+                tau = (beta - c0) / beta;
             }
-            __syncthreads();
-            const double tau = s_tau;
-            for (int r = i + 1 + tid; r < nr; r += blockDim.x) S.P[r + i * ld] = s_zero ? 0.0 : S.P[r + i * ld] / s_div;
+            if (tid == 0) {
+                if (!zero) S.P[i + i * ld] = beta;
+                d.tau[p0 + i] = tau;
+                S.tau[i] = tau;
+            }
+            for (int r = i + 1 + tid; r < nr; r += blockDim.x) S.P[r + i * ld] = zero ? 0.0 : S.P[r + i * ld] / div;
             __syncthreads();
             for (int j = i + 1 + warp; j < jb; j += nwarps) {
                 double* cj = S.P + j * ld;
