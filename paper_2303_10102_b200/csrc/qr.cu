@@ -287,7 +287,11 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
         const size_t sb = qb_smem(max_rows, qcols);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q_blocked),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
-        k_form_q_blocked<<<unsigned(blocks.size()), QB_THREADS, sb, c.stream>>>(dd.get(), w, qcols);
+        // split the columns when the blocks alone leave SMs idle
+        int chunk = qcols;
+        while (chunk > 32 && int(blocks.size()) * cdiv(qcols, chunk) < 2 * c.num_sms) chunk = (chunk + 1) / 2;
+        k_form_q_blocked<<<dim3(unsigned(blocks.size()), unsigned(cdiv(qcols, chunk))), QB_THREADS, sb, c.stream>>>(
+            dd.get(), w, qcols, chunk);
     } else {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

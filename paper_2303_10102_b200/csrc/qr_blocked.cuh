@@ -291,19 +291,26 @@ __global__ void __launch_bounds__(QB_THREADS, 3) k_qr_blocked(const QrDesc* desc
         }
 }
 
-__global__ void __launch_bounds__(QB_THREADS, 3) k_form_q_blocked(const QfDesc* descs, int w, int qcols) {
+/// Columns of Q are independent given the reflectors: CTA (block, chunk)
+/// forms columns [cc0, cc0 + chunk) (few large blocks still fill the GPU).
+__global__ void __launch_bounds__(QB_THREADS, 3) k_form_q_blocked(const QfDesc* descs, int w, int qcols_all,
+                                                                  int chunk) {
     extern __shared__ double sm[];
     const QfDesc d = descs[blockIdx.x];
+    const int cc0 = blockIdx.y * chunk, qcols = min(qcols_all, cc0 + chunk) - cc0;
+    if (qcols <= 0) return;
     const int rows = d.rows, ld = qb_ld(rows);
-    const QbSmem S = qb_layout(sm, rows, qcols);
+    const QbSmem S = qb_layout(sm, rows, qcols_all);
     const int tid = threadIdx.x;
     const int nref = min(w, rows);
-    for (i64 e = tid; e < i64(rows) * qcols; e += blockDim.x) {
-        const int i = int(e % rows), c = int(e / rows);
-        double v = 0.0;
-        if (i < nref) v = d.Tin ? d.Tin[i + i64(c) * d.ldt] : (i == c ? 1.0 : 0.0);
-        d.Q[i + c * d.ldq] = v;
-    }
+    double* Q = d.Q + i64(cc0) * d.ldq;
+    for (int c = 0; c < qcols; ++c)
+        for (int i = tid; i < rows; i += blockDim.x) {
+            const int cg = cc0 + c;
+            double v = 0.0;
+            if (i < nref) v = d.Tin ? d.Tin[i + i64(cg) * d.ldt] : (i == cg ? 1.0 : 0.0);
+            Q[i + i64(c) * d.ldq] = v;
+        }
     __syncthreads();
     for (int p0 = ((nref - 1) / QB_NB) * QB_NB; p0 >= 0; p0 -= QB_NB) {
         const int jb = min(QB_NB, nref - p0), nr = rows - p0;
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(QB_THREADS, 3) k_form_q_blocked(const QfDesc* 
         qb_explicit_v(S.P, ld, nr, jb);
         __syncthreads();
         qb_build_t(S, ld, nr, jb);
-        double* Qp = d.Q + p0;
+        double* Qp = Q + p0;
         qb_vt_c(S, ld, nr, Qp, d.ldq, qcols);
         __syncthreads();
         for (int e = tid; e < QB_NB * qcols; e += blockDim.x) {  // W2 = T W1
