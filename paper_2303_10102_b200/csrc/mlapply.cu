@@ -664,7 +664,12 @@ void leafid_proj(const DHodlr& h, bool transpose, int l0, int nl, int s, double*
 int proj_chunk(const DTree& t, int nl, int tiles) {
     int chunk = ML_CHUNK;
     const i64 n = t.n();
-    while (chunk < t.part(1).max_seg() && (n / (2 * chunk)) * nl * tiles >= 8 * current().num_sms) chunk *= 2;
+    // beyond ~1024 rows an item's X chunk stops being L2-resident across the
+    // level items that share it (s = 64 matvec: 6.68 -> 6.31 ms at 1024)
+    const char* e = std::getenv("HG_PROJ_CHUNK_MAX");
+    const int cmax = e ? std::atoi(e) : 1024;
+    while (chunk < t.part(1).max_seg() && chunk < cmax && (n / (2 * chunk)) * nl * tiles >= 8 * current().num_sms)
+        chunk *= 2;
     return chunk;
 }
 
