@@ -109,7 +109,7 @@ def c1_points(n=4096):
 
 
 @pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4),
-                                                    (2048, 128, 40, 5, 0.05, 1e-6)])
+                                                    (2048, 128, 40, 5, 0.05, 1e-6), (1500, 64, 16, 3, 0.2, 1e-4)])
 def test_build_parity_vs_oracle(H, n, leaf, k, nu2, ell, nug):
     x = np.sort(np.random.default_rng(n).uniform(size=n))
     tau = O.tree_depth(n, leaf, 2 * leaf)

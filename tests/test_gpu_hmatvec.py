@@ -28,7 +28,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("n,tau,k", [(65536, 9, 8), (2000, 3, 12), (3001, 4, 70), (4096, 3, 300), (5, 2, 1),
-                                     (1 << 14, 7, 40)])
+                                     (1 << 14, 7, 40), (256, 1, 6), (512, 2, 10), (1000, 3, 9)])
 def test_narrow_matches_oracle_and_wide(H, n, tau, k):
     oh = O.Hodlr.random_spd(n, tau, k, 11)
     dh = H.HodlrMatrix.from_panels(oh.export_panels())
