@@ -500,7 +500,7 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
     if (f.all_llt && f.bmax() <= TS_MAX) {
         static bool attr = false;
         if (!attr) {
-            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc), TS_SMEM);
+            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc<TS_S>), TS_SMEM);
             attr = true;
         }
         // Column tiles per CTA: enough CTAs for ~4 waves, the factor loaded once per CTA.
@@ -508,7 +508,8 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
         const int groups = std::max(1, std::min(ct, cdiv(4 * 2 * current().num_sms, lv.nseg())));
         const int cpt = cdiv(ct, groups);
         LeafSolveTcArgs a{lv.dbounds(), f.bmax(), f.leaf_fac->get(), Y, ldy, w, ct, cpt};
-        k_leaf_solve_tc<<<unsigned(lv.nseg()) * unsigned(cdiv(ct, cpt)), TS_THREADS, TS_SMEM, current().stream>>>(a);
+        k_leaf_solve_tc<TS_S>
+            <<<unsigned(lv.nseg()) * unsigned(cdiv(ct, cpt)), TS_NC * 4 / TS_S, TS_SMEM, current().stream>>>(a);
         HG_LAUNCH();
         count_launch();
         return;

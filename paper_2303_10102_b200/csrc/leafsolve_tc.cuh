@@ -22,6 +22,10 @@
 // fragment loads below are bank-conflict free); 32 RHS columns per CTA,
 // 4 warps x 8 columns, two CTAs per SM (one loads while the other computes).
 constexpr int TS_NC = 32, TS_MAX = 128, TS_YLD = TS_NC + 4, TS_THREADS = 128;
+#ifndef HG_TS_S
+#define HG_TS_S 1
+#endif
+constexpr int TS_S = HG_TS_S;  // 8-column subtiles per warp in the 128-row kernel (2 measured 28% slower: fewer warps)
 constexpr int TS_LSIZE = 16 * (TS_MAX * (TS_MAX / 16 + 1) / 2 + 4 * (TS_MAX / 16));  // packed panels, mp = 128
 constexpr size_t TS_SMEM = (size_t(TS_MAX) * TS_YLD + TS_LSIZE) * sizeof(double);
 __device__ __forceinline__ int ts_poff(int j, int mp) { return 16 * j * (mp + 4) - 128 * j * (j - 1); }
@@ -72,7 +76,7 @@ __device__ __forceinline__ void ts_load_factor(double* L, const double* F, int l
     for (int j = 0; j < nb; ++j) {
         const int r0 = 16 * j, rows = mp - r0, ld = rows + 4;
         double* P = L + ts_poff(j, mp);
-        for (int e = threadIdx.x; e < rows * 16; e += TS_THREADS) {
+        for (int e = threadIdx.x; e < rows * 16; e += blockDim.x) {
             const int r = e % rows, c = e / rows;
             const int gr = r0 + r, gc = r0 + c;
             double* d = P + c * ld + r;
@@ -190,7 +194,160 @@ __device__ __forceinline__ void ts_backward(const double* Ls, int mp, double* Ys
     }
 }
 
-__global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs g) {
+/// ts_forward / ts_backward with S 8-column subtiles per warp: every factor
+/// fragment loaded from shared memory feeds S DMMAs (the single-subtile
+/// kernel is bound by those fragment loads, profiles/r1_ncu_qr_leafsolve.md).
+template <int S>
+__device__ __forceinline__ void ts_forward_s(const double* Ls, int mp, double* Ys, int row0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8 * S;
+    const int nb = mp / 16;
+    for (int j = 0; j < nb; ++j) {
+        const double* P = Ls + ts_poff(j, mp);
+        const int ld = mp - 16 * j + 4;
+        double* Yj = Ys + (row0 + 16 * j) * TS_YLD + n0;
+        {  // x_j = L_jj^{-1} y_j
+            double yb[S][4], x0[S][2], x1[S][2];
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                x0[u][0] = x0[u][1] = x1[u][0] = x1[u][1] = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) yb[u][kk] = Yj[(4 * kk + t4) * TS_YLD + 8 * u + g8];
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const double p0 = P[(4 * kk + t4) * ld + g8], p1 = P[(4 * kk + t4) * ld + 8 + g8];
+#pragma unroll
+                for (int u = 0; u < S; ++u) {
+                    tile::dmma(x0[u], p0, yb[u][kk]);
+                    tile::dmma(x1[u], p1, yb[u][kk]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                Yj[g8 * TS_YLD + 8 * u + 2 * t4] = x0[u][0];
+                Yj[g8 * TS_YLD + 8 * u + 2 * t4 + 1] = x0[u][1];
+                Yj[(8 + g8) * TS_YLD + 8 * u + 2 * t4] = x1[u][0];
+                Yj[(8 + g8) * TS_YLD + 8 * u + 2 * t4 + 1] = x1[u][1];
+            }
+            __syncwarp();
+        }
+        const int nrt = (mp - 16 * j) / 8;
+        double bf[S][4];
+#pragma unroll
+        for (int u = 0; u < S; ++u)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) bf[u][kk] = Yj[(4 * kk + t4) * TS_YLD + 8 * u + g8];
+        constexpr int MT = TS_MAX / 8 - 2;
+        double acc[MT][S][2];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+#pragma unroll
+            for (int u = 0; u < S; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+            if (t + 2 < nrt) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const double a = P[(4 * kk + t4) * ld + (t + 2) * 8 + g8];
+#pragma unroll
+                    for (int u = 0; u < S; ++u) tile::dmma(acc[t][u], a, bf[u][kk]);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+            if (t + 2 < nrt) {
+#pragma unroll
+                for (int u = 0; u < S; ++u) {
+                    double* yp = Yj + ((t + 2) * 8 + g8) * TS_YLD + 8 * u + 2 * t4;
+                    yp[0] -= acc[t][u][0];
+                    yp[1] -= acc[t][u][1];
+                }
+            }
+        __syncwarp();
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void ts_backward_s(const double* Ls, int mp, double* Ys, int row0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8 * S;
+    const int nb = mp / 16;
+    for (int j = nb - 1; j >= 0; --j) {
+        const double* P = Ls + ts_poff(j, mp);
+        const int ld = mp - 16 * j + 4;
+        double* Yj = Ys + (row0 + 16 * j) * TS_YLD + n0;
+        const int K = mp - 16 * (j + 1);
+        double a0[S][2], a1[S][2], b0[S][2], b1[S][2];
+#pragma unroll
+        for (int u = 0; u < S; ++u) a0[u][0] = a0[u][1] = a1[u][0] = a1[u][1] = b0[u][0] = b0[u][1] = b1[u][0] = b1[u][1] = 0.0;
+        const double* Xb = Yj + 16 * TS_YLD + g8;
+        int k4 = 0;
+        for (; k4 + 8 <= K; k4 += 8) {
+            const double p00 = P[g8 * ld + 16 + k4 + t4], p10 = P[(8 + g8) * ld + 16 + k4 + t4];
+            const double p01 = P[g8 * ld + 16 + k4 + 4 + t4], p11 = P[(8 + g8) * ld + 16 + k4 + 4 + t4];
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                const double x0 = Xb[(k4 + t4) * TS_YLD + 8 * u], x1 = Xb[(k4 + 4 + t4) * TS_YLD + 8 * u];
+                tile::dmma(a0[u], p00, x0);
+                tile::dmma(a1[u], p10, x0);
+                tile::dmma(b0[u], p01, x1);
+                tile::dmma(b1[u], p11, x1);
+            }
+        }
+        if (k4 < K) {
+            const double p00 = P[g8 * ld + 16 + k4 + t4], p10 = P[(8 + g8) * ld + 16 + k4 + t4];
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                const double x0 = Xb[(k4 + t4) * TS_YLD + 8 * u];
+                tile::dmma(a0[u], p00, x0);
+                tile::dmma(a1[u], p10, x0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            double* y0 = Yj + g8 * TS_YLD + 8 * u + 2 * t4;
+            double* y1 = y0 + 8 * TS_YLD;
+            y0[0] -= a0[u][0] + b0[u][0];
+            y0[1] -= a0[u][1] + b0[u][1];
+            y1[0] -= a1[u][0] + b1[u][0];
+            y1[1] -= a1[u][1] + b1[u][1];
+        }
+        __syncwarp();
+        {  // x_j = L_jj^{-T} r_j
+            double rb[S][4], x0[S][2], x1[S][2];
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                x0[u][0] = x0[u][1] = x1[u][0] = x1[u][1] = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) rb[u][kk] = Yj[(4 * kk + t4) * TS_YLD + 8 * u + g8];
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const double p0 = P[g8 * ld + 4 * kk + t4], p1 = P[(8 + g8) * ld + 4 * kk + t4];
+#pragma unroll
+                for (int u = 0; u < S; ++u) {
+                    tile::dmma(x0[u], p0, rb[u][kk]);
+                    tile::dmma(x1[u], p1, rb[u][kk]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                double* y0 = Yj + g8 * TS_YLD + 8 * u + 2 * t4;
+                double* y1 = y0 + 8 * TS_YLD;
+                y0[0] = x0[u][0];
+                y0[1] = x0[u][1];
+                y1[0] = x1[u][0];
+                y1[1] = x1[u][1];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(TS_NC * 4 / S, 2) k_leaf_solve_tc(LeafSolveTcArgs g) {
     extern __shared__ double sm[];
     double* Ys = sm;
     double* Ls = sm + TS_MAX * TS_YLD;
@@ -204,7 +361,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs
     const int ct_end = min(g.ctiles, (grp + 1) * g.cpt);
     for (int ct = grp * g.cpt; ct < ct_end; ++ct) {
     const int c0 = ct * TS_NC, nc = min(TS_NC, g.w - c0);
-    for (int e = tid; e < mp * TS_NC; e += TS_THREADS) {
+    for (int e = tid; e < mp * TS_NC; e += int(blockDim.x)) {
         const int r = e % mp, c = e / mp;
         double* d = Ys + r * TS_YLD + c;
         if (r < m && c < nc)
@@ -216,10 +373,10 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_leaf_solve_tc(LeafSolveTcArgs
     tile::cp_wait<0>();
     __syncthreads();
     // From here on every warp works on its own 8 columns: no block barriers.
-    ts_forward(Ls, mp, Ys, 0);
-    ts_backward(Ls, mp, Ys, 0);
+    ts_forward_s<S>(Ls, mp, Ys, 0);
+    ts_backward_s<S>(Ls, mp, Ys, 0);
     __syncthreads();
-    for (int e = tid; e < m * nc; e += TS_THREADS) {
+    for (int e = tid; e < m * nc; e += int(blockDim.x)) {
         const int r = e % m, c = e / m;
         g.Y[(lo + r) + i64(c0 + c) * g.ldy] = Ys[r * TS_YLD + c];
     }
