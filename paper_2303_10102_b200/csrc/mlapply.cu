@@ -175,6 +175,10 @@ struct LoadUpdB {
 };
 
 constexpr int PACK_MAX = 2048;  // packed update K held as a (level, column) table in shared memory
+#ifndef HG_UPD_NS
+#define HG_UPD_NS 2
+#endif
+constexpr int UPD_NS = HG_UPD_NS;  // cp.async stages of the packed update (3 measured slower: occupancy)
 
 /// Packed A operand: K runs over the levels' columns back to back (no
 /// per-level padding to BK); tab[c] = level << 16 | column for c < coff[nl].
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(THREADS) k_ml_update_packed(UpdArgs g) {
             const int c = n0 + ni;
             if (c < g.s && m < it.rows) y = g.Y[i64(it.row0 + m) + i64(c) * g.ldy];
         });
-    tile::run_t<2, BM, TBN>(la, lb, (ktot + BK - 1) / BK, smem, acc);
+    tile::run_t<UPD_NS, BM, TBN>(la, lb, (ktot + BK - 1) / BK, smem, acc);
     tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int m, int ni) {
         const int c = n0 + ni;
         if (c >= g.s || m >= it.rows) return;
@@ -821,12 +825,13 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         constexpr int N = decltype(TN)::value;
         constexpr int bytes = tile::smem_bytes_t(2, BM, N);
         if (packed) {
+            constexpr int pbytes = tile::smem_bytes_t(UPD_NS, BM, N);
             static bool once = [] {  // static table + dynamic stages exceed the default 48 KB
-                HG_CUDA(cudaFuncSetAttribute(k_ml_update_packed<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+                HG_CUDA(cudaFuncSetAttribute(k_ml_update_packed<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, pbytes));
                 return true;
             }();
             (void)once;
-            k_ml_update_packed<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
+            k_ml_update_packed<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, pbytes, c.stream>>>(ua);
         } else {
             attr_once<k_ml_update<N>>(bytes);
             k_ml_update<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, bytes, c.stream>>>(ua);
