@@ -63,21 +63,6 @@ __global__ void k_range_post(int k, const int* qmap, const double* qR, const int
         if (e % k >= s_nr) Rj[e] = 0.0;
 }
 
-/// S[cl] = Q * diag(sign) (or the identity for full-width nodes).
-__global__ void k_q_sign(const int* bounds, int k, const int* qmap, const double* sign, double* S, i64 lds) {
-    const int j = blockIdx.x;
-    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
-    const bool full = qmap[j] < 0;
-    for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
-        const int r = e % m, c = e / m;
-        double* p = S + i64(lo + r) + i64(c) * lds;
-        if (full)
-            *p = r == c ? 1.0 : 0.0;
-        else
-            *p *= sign[j * k + c];
-    }
-}
-
 __device__ double cta_sum(double v) {
     __shared__ double sh[32];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -222,24 +207,6 @@ __global__ void k_place_completion(const WorkItem* items, const int* cj, const i
     }
 }
 
-/// presc (sketch.cpp:203-206): max over params of ||dY_param[cl]||_F.
-__global__ void k_presc(const int* bounds, int k, int p, const double* dY, i64 ld, double* presc) {
-    const int j = blockIdx.x;
-    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
-    double best = 0.0;
-    for (int q = 0; q < p; ++q) {
-        double part = 0.0;
-        for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
-            const int r = e % m, c = e / m;
-            const double v = dY[i64(lo + r) + i64(q * k + c) * ld];
-            part += v * v;
-        }
-        best = fmax(best, sqrt(cta_sum(part)));
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) presc[j] = best;
-}
-
 /// q2 width (sketch.cpp:214-221).
 __global__ void k_w2_nodes(int nodes, const int* bounds, int k, int kp, const int* qmap, const double* R2,
                            const double* presc, int* w2out) {
@@ -318,19 +285,6 @@ __global__ void k_diffqr(int k, const double* G, const double* R, const int* per
 
 // ------------------------------------------------------------ recompression
 /// M_j = T_L T_R^T (W x W, zero outside wl x wr) from the per-child R factors.
-__global__ void k_core(int W, const double* Rc, double* M) {
-    const int j = blockIdx.x;
-    const double* L = Rc + i64(2 * j) * W * W;
-    const double* Rr = Rc + i64(2 * j + 1) * W * W;
-    double* Mj = M + i64(j) * W * W;
-    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
-        const int a = e % W, b = e / W;
-        double s = 0.0;
-        for (int c = max(a, b); c < W; ++c) s += L[a + c * W] * Rr[b + c * W];
-        Mj[e] = s;
-    }
-}
-
 /// Truncation rank at rtol relative to the leading pivoted diagonal.
 __global__ void k_trunc_rank(int nodes, int W, const double* RM, const int* wmin, double rtol, int* r_out) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -350,8 +304,7 @@ __global__ void k_tins(int W, int rmax, const int* r, const double* RM, const in
     double* TR = Tin + i64(2 * j + 1) * W * rmax;
     const double* R = RM + i64(j) * W * W;
     for (int e = threadIdx.x; e < W * rmax; e += blockDim.x) {
-        const int i = e % W, a = e / W;
-        if (a >= rj) TL[e] = 0.0;
+        if (e / W >= rj) TL[e] = 0.0;
         TR[e] = 0.0;
     }
     __syncthreads();
@@ -362,73 +315,6 @@ __global__ void k_tins(int W, int rmax, const int* r, const double* RM, const in
 }
 
 std::vector<int> dl_int(const DBuf<int>& d) { return d.download(); }
-
-/// Recompress the derivative level panel D (n x W, symmetric storage) in
-/// place of `out` (hodlr_matrix.cpp:42-66 via sketch.cpp:331-341).
-void compress_level(DHodlr& D, int l, double rtol) {
-    const int W = D.Rl(l);
-    if (W == 0) return;
-    const DTree& t = *D.tree;
-    const i64 n = t.n();
-    const Partition& pc = t.part(l);
-    const int nodes = 1 << (l - 1);
-    const auto& hb = pc.hbounds();
-    double* P = D.Ul(l);
-    // Unpivoted QR of every child block (both factors of every node).
-    std::vector<BatchedQR::Block> blocks;
-    for (int c = 0; c < 2 * nodes; ++c) blocks.push_back({P + hb[static_cast<size_t>(c)], n, hb[static_cast<size_t>(c + 1)] - hb[static_cast<size_t>(c)]});
-    BatchedQR qr(blocks, W, false);
-    // Core M = T_L T_R^T and its rank-revealing pivoted QR.
-    DVec M(static_cast<size_t>(nodes) * W * W);
-    k_core<<<nodes, 256, 0, current().stream>>>(W, qr.R(), M.get());
-    HG_LAUNCH();
-    count_launch();
-    std::vector<BatchedQR::Block> mb;
-    for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * W * W, W, W});
-    BatchedQR mq(mb, W, true);
-    std::vector<int> wmin(static_cast<size_t>(nodes));
-    for (int j = 0; j < nodes; ++j) {
-        const int cl = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)], cr = hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)];
-        wmin[static_cast<size_t>(j)] = std::min({cl, cr, W});
-    }
-    DBuf<int> dwmin, dr(static_cast<size_t>(nodes));
-    dwmin.upload(wmin);
-    k_trunc_rank<<<cdiv(nodes, 128), 128, 0, current().stream>>>(nodes, W, mq.R(), dwmin.get(), rtol, dr.get());
-    HG_LAUNCH();
-    count_launch();
-    std::vector<int> r = dl_int(dr);
-    int rmax = 0;
-    for (int x : r) rmax = std::max(rmax, x);
-    auto Pn = rmax ? make_dvec(static_cast<size_t>(n) * static_cast<size_t>(rmax), true) : nullptr;
-    if (rmax) {
-        // Per child c: Tin_c = Q_M[:, :r] (left child) or P R_M[:r, :]^T (right child).
-        DVec Tin(static_cast<size_t>(2 * nodes) * W * rmax);
-        std::vector<double*> qo;
-        std::vector<i64> ql;
-        for (int j = 0; j < nodes; ++j) {
-            qo.push_back(Tin.get() + i64(2 * j) * W * rmax);
-            ql.push_back(W);
-        }
-        mq.form_q(rmax, nullptr, 0, 0, qo, ql);
-        k_tins<<<nodes, 256, 0, current().stream>>>(W, rmax, dr.get(), mq.R(), mq.perm(), Tin.get());
-        HG_LAUNCH();
-        count_launch();
-        std::vector<double*> out;
-        std::vector<i64> ld;
-        for (int c = 0; c < 2 * nodes; ++c) {
-            out.push_back(Pn->get() + hb[static_cast<size_t>(c)]);
-            ld.push_back(n);
-        }
-        qr.form_q(rmax, Tin.get(), i64(W) * rmax, W, out, ld);
-    }
-    D.R[static_cast<size_t>(l - 1)] = rmax;
-    D.U[static_cast<size_t>(l - 1)] = Pn;
-    D.V[static_cast<size_t>(l - 1)] = Pn;
-    for (int j = 0; j < nodes; ++j) {
-        D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
-        D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
-    }
-}
 
 __global__ void k_transpose_blocks(int w, const double* A, double* B) {
     const int j = blockIdx.x;

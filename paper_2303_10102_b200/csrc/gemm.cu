@@ -326,31 +326,6 @@ __device__ double block_sum(double v) {
     return v;  // valid in thread 0
 }
 
-/// Partial sums of sum(A .* B) over n x w: block b owns a fixed row range for
-/// every column (deterministic), one partial per block.
-__global__ void k_dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* partial) {
-    const i64 per = (n + gridDim.x - 1) / gridDim.x;
-    const i64 r0 = i64(blockIdx.x) * per, r1 = min(n, r0 + per);
-    double v = 0.0;
-    for (int j = 0; j < w; ++j) {
-        const double* a = A + j * lda;
-        const double* b = B + j * ldb;
-        for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) v = fma(a[i], b[i], v);
-    }
-    v = block_sum(v);
-    if (threadIdx.x == 0) partial[blockIdx.x] = v;
-}
-
-struct DotPanels {
-    i64 n;
-    const double *A, *B;
-    i64 lda, ldb;
-    __device__ double operator()(i64 e) const {
-        const i64 i = e % n, j = e / n;
-        return A[i + j * lda] * B[i + j * ldb];
-    }
-};
-
 struct PairDot {
     int ra, rb, xr, ldg, ldh;
     i64 gs, hs;

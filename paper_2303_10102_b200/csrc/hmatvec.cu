@@ -38,7 +38,6 @@ namespace hg {
 namespace {
 
 constexpr int MV_T = 128;     // threads per CTA
-constexpr int MV_W = MV_T / 32;
 constexpr int MV_MAXL = 24;
 constexpr int MV_RMAX = 256;  // widest level the path takes
 constexpr int MV_G = 32;      // tier-1 fan-in (chunks folded per group)

@@ -79,7 +79,6 @@ struct Json {
         if (it == o.end()) throw IoError(where + ": missing key '" + key + "'");
         return it->second;
     }
-    bool has(const std::string& key) const { return kind == Obj && o.count(key) != 0; }
     long long as_int(const std::string& where) const {
         if (kind == Int) return i;
         if (kind == Num && d == double(static_cast<long long>(d))) return static_cast<long long>(d);

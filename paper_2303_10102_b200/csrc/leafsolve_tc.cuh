@@ -353,10 +353,9 @@ __global__ void __launch_bounds__(TS_NC * 4 / S, 2) k_leaf_solve_tc(LeafSolveTcA
     double* Ls = sm + TS_MAX * TS_YLD;
     const int groups = (g.ctiles + g.cpt - 1) / g.cpt;
     const int b = blockIdx.x / groups, grp = blockIdx.x % groups;
-    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, mp = (m + 15) & ~15, nb = mp / 16;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, mp = (m + 15) & ~15;
     const double* F = g.fac + i64(b) * g.bmax * g.bmax;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g8 = lane >> 2, t4 = lane & 3, n0 = warp * 8;
+    const int tid = threadIdx.x;
     ts_load_factor(Ls, F, g.bmax, m, mp);  // once for all of this CTA's column tiles
     const int ct_end = min(g.ctiles, (grp + 1) * g.cpt);
     for (int ct = grp * g.cpt; ct < ct_end; ++ct) {

@@ -37,8 +37,6 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
     __shared__ double nu[MAXW], nd[MAXW];
     __shared__ int s_best;
     __shared__ int trans[MAXW];
-    __shared__ double s_tau, s_div;
-    __shared__ int s_zero;
     const QrDesc d = descs[blockIdx.x];
     const int rows = d.rows;
     const bool use_smem = i64(rows) * w <= smem_elems;

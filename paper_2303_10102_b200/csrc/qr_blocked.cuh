@@ -207,8 +207,6 @@ __device__ __forceinline__ void qb_c_minus_vw(const QbSmem& S, int ld, int nr, d
 
 __global__ void __launch_bounds__(QB_THREADS, 3) k_qr_blocked(const QrDesc* descs, int w) {
     extern __shared__ double sm[];
-    __shared__ double s_tau, s_div;
-    __shared__ int s_zero;
     const QrDesc d = descs[blockIdx.x];
     const int rows = d.rows, ld = qb_ld(rows);
     const QbSmem S = qb_layout(sm, rows, w);
