@@ -689,20 +689,39 @@ void factor_solve(const DFactor& f, double* Y, i64 ldy, int w) {
 }
 
 double factor_logdet(const DFactor& f) {
-    std::vector<double> lld = f.leaf_ld->download();
-    std::vector<int> lsg = f.leaf_sign->download();
+    // every (log|det|, sign) array copied back asynchronously, one stream sync
+    auto& c = current();
+    const int tau = f.tau();
+    std::vector<double> lld(f.leaf_ld->size());
+    std::vector<int> lsg(f.leaf_sign->size());
+    std::vector<std::vector<double>> cl(static_cast<size_t>(tau));
+    std::vector<std::vector<int>> cs(static_cast<size_t>(tau));
+    auto get = [&](auto& h, const auto& d) {
+        if (!h.empty())
+            HG_CUDA(cudaMemcpyAsync(h.data(), d.get(), h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, c.stream));
+    };
+    get(lld, *f.leaf_ld);
+    get(lsg, *f.leaf_sign);
+    for (int i = 1; i <= tau; ++i) {
+        const size_t li = static_cast<size_t>(i - 1);
+        if (!f.cap[li]) continue;
+        cl[li].resize(f.cap_ld[li]->size());
+        cs[li].resize(f.cap_sign[li]->size());
+        get(cl[li], *f.cap_ld[li]);
+        get(cs[li], *f.cap_sign[li]);
+    }
+    HG_CUDA(cudaStreamSynchronize(c.stream));
     double ld = 0.0;
     for (size_t b = 0; b < lld.size(); ++b) {
         if (lsg[b] <= 0) throw NotPositiveDefinite("leaf block has non-positive determinant");
         ld += lld[b];
     }
-    for (int i = 1; i <= f.tau(); ++i) {
-        if (!f.cap[static_cast<size_t>(i - 1)]) continue;
-        std::vector<double> cl = f.cap_ld[static_cast<size_t>(i - 1)]->download();
-        std::vector<int> cs = f.cap_sign[static_cast<size_t>(i - 1)]->download();
-        for (size_t j = 0; j < cl.size(); ++j) {
-            if (cs[j] <= 0) throw NotPositiveDefinite("capacitance has non-positive determinant");
-            ld += cl[j];
+    for (int i = 1; i <= tau; ++i) {
+        const size_t li = static_cast<size_t>(i - 1);
+        if (!f.cap[li]) continue;
+        for (size_t j = 0; j < cl[li].size(); ++j) {
+            if (cs[li][j] <= 0) throw NotPositiveDefinite("capacitance has non-positive determinant");
+            ld += cl[li][j];
         }
     }
     return ld;
