@@ -41,11 +41,11 @@ int guard(F&& f) {
 
 Mat from_ptr(const double* p, Index r, Index c) {
     Mat m(r, c);
-    if (r * c) std::memcpy(m.data(), p, static_cast<size_t>(r * c) * sizeof(double));
+    if (r > 0 && c > 0) std::memcpy(m.data(), p, static_cast<size_t>(r * c) * sizeof(double));
     return m;
 }
 void to_ptr(const Mat& m, double* p) {
-    if (m.r * m.c) std::memcpy(p, m.data(), static_cast<size_t>(m.r * m.c) * sizeof(double));
+    if (m.r > 0 && m.c > 0) std::memcpy(p, m.data(), static_cast<size_t>(m.r * m.c) * sizeof(double));
 }
 
 struct OHodlr {
