@@ -87,6 +87,40 @@ __device__ bool dev_llt(double* W, int ldw, int m) {
     return true;
 }
 
+/// dev_llt on the packed lower triangle: column j holds rows [j, m) at
+/// Wp[i + cb(j)], cb(j) = j m - j (j + 1) / 2 (half the shared memory of the
+/// square layout, so three factorizations share an SM instead of one).
+__device__ __forceinline__ int ll_cb(int j, int m) { return j * m - j * (j + 1) / 2; }
+
+__device__ bool dev_llt_packed(double* Wp, int m) {
+    __shared__ int s_ok;
+    for (int k = 0; k < m; ++k) {
+        const int ck = ll_cb(k, m);
+        if (threadIdx.x == 0) {
+            const double x = Wp[k + ck];
+            if (x <= 0.0) {
+                s_ok = 0;
+            } else {
+                Wp[k + ck] = sqrt(x);
+                s_ok = 1;
+            }
+        }
+        __syncthreads();
+        if (!s_ok) return false;
+        const double d = Wp[k + ck];
+        for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) Wp[i + ck] /= d;
+        __syncthreads();
+        const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int j = k + 1 + int(threadIdx.x >> 5); j < m; j += nw) {
+            const double wjk = Wp[j + ck];
+            double* cj = Wp + ll_cb(j, m);
+            for (int i = j + lane; i < m; i += 32) cj[i] -= Wp[i + ck] * wjk;
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
 /// In-place LU with partial pivoting (Eigen PartialPivLU: first max-abs
 /// pivot; zero pivots leave the column unscaled). Row swaps -> piv[k].
 __device__ int dev_lu(double* W, int ldw, int m, int* piv) {
@@ -149,6 +183,43 @@ __global__ void __launch_bounds__(FNT) k_leaf_factor(LeafFacArgs g) {
     const int m = g.bounds[b + 1] - g.bounds[b];
     const i64 ls = i64(g.bmax) * g.bmax;
     const double* A = g.orig + b * ls;
+    if (g.use_smem == 2) {  // packed lower-triangle Cholesky in shared memory
+        for (int j = 0; j < m; ++j)
+            for (int i = j + threadIdx.x; i < m; i += blockDim.x) sm[i + ll_cb(j, m)] = A[i + i64(j) * g.bmax];
+        __syncthreads();
+        if (dev_llt_packed(sm, m)) {
+            double* F = g.fac + b * ls;
+            for (int j = 0; j < m; ++j)
+                for (int i = j + threadIdx.x; i < m; i += blockDim.x) F[i + i64(j) * g.bmax] = sm[i + ll_cb(j, m)];
+            if (threadIdx.x == 0) {
+                double ld = 0.0;
+                for (int i = 0; i < m; ++i) ld += log(sm[i + ll_cb(i, m)]);
+                g.kind[b] = 1;
+                g.ld[b] = 2.0 * ld;
+                g.sign[b] = 1;
+            }
+            return;
+        }
+        // not SPD: PartialPivLU in global memory (factorization.cpp:10-17 fallback)
+        double* W = g.fac + b * ls;
+        for (int j = 0; j < m; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) W[i + i64(j) * g.bmax] = A[i + i64(j) * g.bmax];
+        __syncthreads();
+        const int nswap = dev_lu(W, g.bmax, m, g.piv + i64(b) * g.bmax);
+        if (threadIdx.x == 0) {
+            double ld = 0.0;
+            int sign = (nswap & 1) ? -1 : 1;
+            for (int i = 0; i < m; ++i) {
+                const double d = W[i + i64(i) * g.bmax];
+                if (d < 0) sign = -sign;
+                ld += log(fabs(d));
+            }
+            g.kind[b] = 0;
+            g.ld[b] = ld;
+            g.sign[b] = sign;
+        }
+        return;
+    }
     double* W = g.use_smem ? sm : g.fac + b * ls;
     const int ldw = g.use_smem ? m : g.bmax;
     int* piv = g.piv + i64(b) * g.bmax;
@@ -609,8 +680,9 @@ DFactor factorize(const DHodlr& h, int orient) {
     f.leaf_ld = make_dvec(static_cast<size_t>(nl), false);
     f.leaf_sign = std::make_shared<DBuf<int>>(static_cast<size_t>(nl));
     {
-        const size_t smem = static_cast<size_t>(bm) * bm * sizeof(double);
-        const int use = smem <= SMEM_CAP ? 1 : 0;
+        const size_t psmem = static_cast<size_t>(bm) * (bm + 1) / 2 * sizeof(double);
+        const size_t smem = h.sym && psmem <= SMEM_CAP ? psmem : static_cast<size_t>(bm) * bm * sizeof(double);
+        const int use = h.sym && psmem <= SMEM_CAP ? 2 : (smem <= SMEM_CAP ? 1 : 0);
         if (use) set_smem(reinterpret_cast<const void*>(k_leaf_factor), smem);
         LeafFacArgs g{lv.dbounds(), bm, h.leaves->get(), f.leaf_fac->get(), h.sym ? 1 : 0, use,
                       f.leaf_kind->get(), f.leaf_piv->get(), f.leaf_ld->get(), f.leaf_sign->get()};
