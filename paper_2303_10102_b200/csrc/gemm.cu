@@ -169,18 +169,20 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int grou
             v = (n < g.w && m < it.rows) ? g.Y[i64(it.row0 + m) + i64(n) * g.ldy] : 0.0;
         });
     };
-    Acc ycur, ynext;
-    if (ld_y) load_y(j0, ycur);
+    // Y two tiles ahead in registers (more of the HBM stream in flight per SM)
+    Acc ycur, ynext, ynext2;
+    if (ld_y) {
+        load_y(j0, ycur);
+        if (j0 + 1 < j1) load_y(j0 + 1, ynext);
+    }
     issue_t(j0, 0);
     tile::cp_commit();
     for (int j = j0; j < j1; ++j) {
         const int buf = (j - j0) & 1;
         tile::cp_wait<0>();
         __syncthreads();  // tile j (and X) landed; every warp is done with the other buffer
-        if (j + 1 < j1) {
-            issue_t(j + 1, buf ^ 1);
-            if (ld_y) load_y(j + 1, ynext);
-        }
+        if (j + 1 < j1) issue_t(j + 1, buf ^ 1);
+        if (ld_y && j + 2 < j1) load_y(j + 2, ynext2);
         tile::cp_commit();
         Acc acc;
         acc.zero();
@@ -194,7 +196,10 @@ __global__ void __launch_bounds__(THREADS) k_seg_nn_stream(SegNnArgs g, int grou
             if (n >= g.w || m >= it.rows) return;
             g.Y[i64(it.row0 + m) + i64(n) * g.ldy] = g.alpha * v + (ld_y ? g.beta * y : 0.0);
         });
-        if (ld_y) ycur = ynext;
+        if (ld_y) {
+            ycur = ynext;
+            ynext = ynext2;
+        }
     }
     tile::cp_wait<0>();
 }
