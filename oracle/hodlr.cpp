@@ -11,6 +11,7 @@
 #include <random>
 
 #include "oracle.hpp"
+#include "matern1d.hpp"
 
 namespace oracle {
 
@@ -404,113 +405,25 @@ Matern1dOracle::Matern1dOracle(std::vector<double> x, int nu2, double sigma2, do
         if (x_[i] < x_[i - 1]) throw std::invalid_argument("Matern1d: points must be sorted");
 }
 
-namespace {
-double matern_c(int nu2) { return nu2 == 1 ? 1.0 : (nu2 == 3 ? std::sqrt(3.0) : std::sqrt(5.0)); }
-
-/// exp(-lambda d) * sum_m coef[m] d^m representation of each kernel.
-int matern_poly(int nu2, int which, double sigma2, double ell, double coef[4], double& lambda) {
-    lambda = matern_c(nu2) / ell;
-    const double L = lambda;
-    for (int m = 0; m < 4; ++m) coef[m] = 0;
-    double s = which == 0 ? 1.0 : sigma2;  // d/dsigma2 drops the sigma2 factor
-    if (which <= 0) {
-        coef[0] = s;
-        if (nu2 >= 3) coef[1] = s * L;
-        if (nu2 == 5) coef[2] = s * L * L / 3.0;
-        return nu2 == 1 ? 1 : (nu2 == 3 ? 2 : 3);
-    }
-    // which == 1: d/dell
-    if (nu2 == 1) {
-        coef[1] = s * L / ell;
-        return 2;
-    }
-    if (nu2 == 3) {
-        coef[2] = s * L * L / ell;
-        return 3;
-    }
-    coef[2] = s * L * L / (3.0 * ell);
-    coef[3] = s * L * L * L / (3.0 * ell);
-    return 4;
-}
-}  // namespace
-
 double Matern1dOracle::kernel(double d, int which) const {
-    double coef[4], lambda;
-    int nt = matern_poly(nu2_, which, sigma2_, ell_, coef, lambda);
-    double p = 0, dm = 1;
-    for (int m = 0; m < nt; ++m) {
-        p += coef[m] * dm;
-        dm *= d;
-    }
-    return p * std::exp(-lambda * d);
+    return matern1d::kernel(nu2_, which, sigma2_, ell_, d);
 }
 
 Mat Matern1dOracle::apply_impl(int which, const Mat& v) const {
     const Index n = dim();
     if (v.r != n) throw std::invalid_argument("Matern1d: dimension mismatch");
     Mat y(n, v.c);
-    double coef[4], lambda;
-    const int nt = matern_poly(nu2_, which, sigma2_, ell_, coef, lambda);
-    if (!scan_) {
+    if (!scan_) {  // dense kernel matrix times V through the GEMM
         Mat kd(n, n);
         for (Index j = 0; j < n; ++j)
-            for (Index i = 0; i < n; ++i) kd(i, j) = kernel(std::abs(x_[static_cast<size_t>(i)] - x_[static_cast<size_t>(j)]), which);
+            for (Index i = 0; i < n; ++i) kd(i, j) = kernel(std::abs(x_[size_t(i)] - x_[size_t(j)]), which);
         y = matmul(kd, v);
-    } else {
-        // Two-sided exponential-polynomial recurrence:
-        // F_m(i) = rho sum_{q<=m} C(m,q) d^{m-q} F_q(i-1) + [m=0] v_i.
-        static const double binom[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
-#pragma omp parallel for schedule(static)
-        for (Index c = 0; c < v.c; ++c) {
-            const double* vc = v.col(c);
-            double* yc = y.col(c);
-            double st[4] = {0, 0, 0, 0};
-            for (Index i = 0; i < n; ++i) {
-                if (i > 0) {
-                    double d = x_[static_cast<size_t>(i)] - x_[static_cast<size_t>(i - 1)];
-                    double rho = std::exp(-lambda * d);
-                    double ns[4];
-                    for (int m = nt - 1; m >= 0; --m) {
-                        double s = 0, dp = 1;
-                        for (int q = m; q >= 0; --q) {
-                            s += binom[m][q] * dp * st[q];
-                            dp *= d;
-                        }
-                        ns[m] = rho * s;
-                    }
-                    for (int m = 0; m < nt; ++m) st[m] = ns[m];
-                }
-                st[0] += vc[i];
-                double acc = 0;
-                for (int m = 0; m < nt; ++m) acc += coef[m] * st[m];
-                yc[i] = acc;
-            }
-            for (int m = 0; m < 4; ++m) st[m] = 0;
-            for (Index i = n - 1; i >= 0; --i) {
-                if (i < n - 1) {
-                    double d = x_[static_cast<size_t>(i + 1)] - x_[static_cast<size_t>(i)];
-                    double rho = std::exp(-lambda * d);
-                    double ns[4];
-                    for (int m = nt - 1; m >= 0; --m) {
-                        double s = 0, dp = 1;
-                        for (int q = m; q >= 0; --q) {
-                            s += binom[m][q] * dp * st[q];
-                            dp *= d;
-                        }
-                        ns[m] = rho * s;
-                    }
-                    for (int m = 0; m < nt; ++m) st[m] = ns[m];
-                }
-                st[0] += vc[i];
-                double acc = 0;
-                for (int m = 0; m < nt; ++m) acc += coef[m] * st[m];
-                yc[i] += acc - coef[0] * vc[i];
-            }
-        }
+        if (which < 0 && nugget_ != 0.0)
+            for (Index c = 0; c < v.c; ++c)
+                for (Index i = 0; i < n; ++i) y(i, c) += nugget_ * v(i, c);
+        return y;
     }
-    if (which < 0 && nugget_ != 0.0)
-        for (Index c = 0; c < v.c; ++c)
-            for (Index i = 0; i < n; ++i) y(i, c) += nugget_ * v(i, c);
+    matern1d::apply(x_.data(), n, nu2_, sigma2_, ell_, nugget_, which, true, v.data(), v.r, v.c, y.data(), n);
     return y;
 }
 

@@ -13,7 +13,13 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+# Loaded as oracle.pyref_impl (oracle/pyref.py) this module binds the REFERENCE
+# itself (oracle/_ref/libhodlrgp_ref.so: /root/reference/proj/src compiled
+# unmodified against oracle/eigen_shim, same or_* ABI); otherwise the restated
+# oracle (oracle/_build/liboracle.so).
+IS_REFERENCE = __name__.endswith("pyref_impl")
+LIB_PATH = os.path.join(_HERE, "_ref", "libhodlrgp_ref.so") if IS_REFERENCE else os.path.join(
+    _HERE, "_build", "liboracle.so")
 
 i64 = C.c_int64
 u64 = C.c_uint64
@@ -27,7 +33,7 @@ _lib = None
 
 
 def build():
-    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    subprocess.run(["make", "-s", "-C", _HERE] + (["-f", "ref.mk"] if IS_REFERENCE else []), check=True)
 
 
 def lib():
