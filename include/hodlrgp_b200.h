@@ -51,6 +51,21 @@ hg_status hg_ctx_synchronize(hg_ctx_t ctx);
 /* Number of kernels this context has launched so far. */
 uint64_t hg_ctx_launches(hg_ctx_t ctx);
 void* hg_ctx_stream(hg_ctx_t ctx);
+/* Numerical options of a context (defaults 0):
+ *  HG_OPT_PRODUCT_ASSOCIATION — how solve_multiply applies each Woodbury factor
+ *    to the running factors. HG_ASSOC_SOLVE (default): rows -= v cap^{-T}(u^T rows),
+ *    stable at the condition numbers of BASELINE's configs. HG_ASSOC_REFERENCE:
+ *    p = -(cap^{-1} v^T)^T formed first, rows += p (q^T rows), exactly the
+ *    association of product_rep.cpp:32-45,74-78 (parity mode).
+ *  HG_OPT_COMPRESSION — truncation of the derivative blocks' cores
+ *    (LowRankBlock::compressed, hodlr_matrix.cpp:42-66): HG_COMPRESS_PIVOTED_QR
+ *    (default, rank-revealing pivoted QR at the same 1e-13 threshold) or
+ *    HG_COMPRESS_JACOBI_SVD (singular values, as the reference). */
+enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2 };
+enum { HG_ASSOC_SOLVE = 0, HG_ASSOC_REFERENCE = 1 };
+enum { HG_COMPRESS_PIVOTED_QR = 0, HG_COMPRESS_JACOBI_SVD = 1 };
+hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value);
+int hg_ctx_get_option(hg_ctx_t ctx, int option);
 
 /* ----------------------------------------------------- cluster tree (host) */
 /* tree_depth — cluster_tree.cpp:34-38 */

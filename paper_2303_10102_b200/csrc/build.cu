@@ -326,6 +326,125 @@ __global__ void k_transpose_blocks(int w, const double* A, double* B) {
     }
 }
 
+/// Batched one-sided (Hestenes) Jacobi SVD of the w x w cores M_j, one CTA
+/// per node: columns of A = M_j are rotated pairwise (round-robin tournament,
+/// one warp per pair) until every pair is orthogonal to eps, V accumulates the
+/// rotations, so A = U Sigma and M_j = (U Sigma) V^T. Columns are then sorted
+/// by norm (the singular values, non-increasing) and the truncation rank is
+/// the reference's rule: r = #{sigma_i > rtol sigma_0}, i < wmin
+/// (hodlr_matrix.cpp:56-60). Outputs, per node: US (w x w, sorted A columns)
+/// and V (w x w, sorted), both in the workspace, and r. This is the
+/// HG_COMPRESS_JACOBI_SVD mode of the recompression (parity with JacobiSVD).
+__global__ void __launch_bounds__(256) k_jacobi_svd(int w, const double* M, const int* wmin, double rtol,
+                                                    double* A_ws, double* V_ws, double* US, double* Vs,
+                                                    int* r_out) {
+    const int j = blockIdx.x;
+    const i64 ww = i64(w) * w;
+    double* A = A_ws + j * ww;
+    double* V = V_ws + j * ww;
+    for (i64 e = threadIdx.x; e < ww; e += blockDim.x) {
+        A[e] = M[j * ww + e];
+        V[e] = (e % w) == (e / w) ? 1.0 : 0.0;
+    }
+    __shared__ int s_rot;
+    __shared__ double s_norm[320];
+    __shared__ int s_perm[320];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int wp = (w + 1) & ~1;  // players (one dummy when w is odd)
+    const double eps = 2.220446049250313e-16;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (threadIdx.x == 0) s_rot = 0;
+        __syncthreads();
+        for (int step = 0; step < wp - 1; ++step) {
+            for (int t = warp; t < wp / 2; t += nwarps) {
+                auto pos = [&](int k) { return k == 0 ? 0 : 1 + (k - 1 + step) % (wp - 1); };
+                int p = pos(t), q = pos(wp - 1 - t);
+                if (p >= w || q >= w) continue;
+                if (p > q) { const int x = p; p = q; q = x; }
+                double* ap = A + i64(p) * w;
+                double* aq = A + i64(q) * w;
+                double al = 0, be = 0, ga = 0;
+                for (int i = lane; i < w; i += 32) {
+                    const double x = ap[i], y = aq[i];
+                    al += x * x;
+                    be += y * y;
+                    ga += x * y;
+                }
+                for (int o = 16; o; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (ga == 0.0 || fabs(ga) <= eps * sqrt(al * be)) continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                for (int i = lane; i < w; i += 32) {
+                    const double x = ap[i], y = aq[i];
+                    ap[i] = c * x - sn * y;
+                    aq[i] = sn * x + c * y;
+                }
+                double* vp = V + i64(p) * w;
+                double* vq = V + i64(q) * w;
+                for (int i = lane; i < w; i += 32) {
+                    const double x = vp[i], y = vq[i];
+                    vp[i] = c * x - sn * y;
+                    vq[i] = sn * x + c * y;
+                }
+                if (lane == 0) s_rot = 1;
+            }
+            __syncthreads();
+        }
+        if (!s_rot) break;
+        __syncthreads();
+    }
+    // singular values = column norms; stable sort non-increasing
+    for (int c = warp; c < w; c += nwarps) {
+        double s2 = 0;
+        for (int i = lane; i < w; i += 32) s2 += A[i64(c) * w + i] * A[i64(c) * w + i];
+        for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0) s_norm[c] = sqrt(s2);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < w; ++c) s_perm[c] = c;
+        for (int a = 1; a < w; ++a) {  // insertion sort, stable
+            const int x = s_perm[a];
+            int b = a - 1;
+            while (b >= 0 && s_norm[s_perm[b]] < s_norm[x]) {
+                s_perm[b + 1] = s_perm[b];
+                --b;
+            }
+            s_perm[b + 1] = x;
+        }
+        const double s0 = s_norm[s_perm[0]];
+        int r = 0;
+        while (r < wmin[j] && s_norm[s_perm[r]] > rtol * s0) ++r;
+        r_out[j] = r;
+    }
+    __syncthreads();
+    for (i64 e = threadIdx.x; e < ww; e += blockDim.x) {
+        const int i = int(e % w), c = int(e / w);
+        US[j * ww + e] = A[i64(s_perm[c]) * w + i];
+        Vs[j * ww + e] = V[i64(s_perm[c]) * w + i];
+    }
+}
+
+/// Tin[2j] = US[:, :r_j], Tin[2j+1] = V[:, :r_j] (w x rmax, zero past r_j).
+__global__ void k_svd_tins(int w, int rmax, const int* r, const double* US, const double* Vs, double* Tin) {
+    const int j = blockIdx.x;
+    const int rj = r[j];
+    const i64 ww = i64(w) * w;
+    double* TL = Tin + i64(2 * j) * w * rmax;
+    double* TR = Tin + i64(2 * j + 1) * w * rmax;
+    for (int e = threadIdx.x; e < w * rmax; e += blockDim.x) {
+        const bool keep = e / w < rj;
+        TL[e] = keep ? US[j * ww + e] : 0.0;
+        TR[e] = keep ? Vs[j * ww + e] : 0.0;
+    }
+}
+
 /// Structured recompression of a derivative level built by the sketch
 /// (sketch.cpp:297-311 then :331-341). Its left factor is
 /// [dqc | Q | q2] = [Q | q2] [[Omega, I, 0], [0, 0, I]] with [Q | q2]
@@ -358,9 +477,6 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
     k_transpose_blocks<<<nodes, 256, 0, ctx.stream>>>(w, qz.R(), M.get());
     HG_LAUNCH();
     count_launch();
-    std::vector<BatchedQR::Block> mb;
-    for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * w * w, w, w});
-    BatchedQR mq(mb, w, true);
     std::vector<int> wmin(static_cast<size_t>(nodes));
     for (int j = 0; j < nodes; ++j) {
         const int cl = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
@@ -369,24 +485,47 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
     }
     DBuf<int> dwmin, dr(static_cast<size_t>(nodes));
     dwmin.upload(wmin);
-    k_trunc_rank<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, w, mq.R(), dwmin.get(), rtol, dr.get());
-    HG_LAUNCH();
-    count_launch();
+    const bool svd = ctx.compression == HG_COMPRESS_JACOBI_SVD;
+    std::unique_ptr<BatchedQR> mq;
+    std::unique_ptr<DVec> US, VS;
+    if (svd) {
+        if (w > 320) throw std::length_error("compress: Jacobi SVD core wider than 320");
+        const size_t ws = static_cast<size_t>(nodes) * w * w;
+        DVec Aw(ws), Vw(ws);
+        US = std::make_unique<DVec>(ws);
+        VS = std::make_unique<DVec>(ws);
+        k_jacobi_svd<<<nodes, 256, 0, ctx.stream>>>(w, M.get(), dwmin.get(), rtol, Aw.get(), Vw.get(), US->get(),
+                                                    VS->get(), dr.get());
+        HG_LAUNCH();
+        count_launch();
+    } else {
+        std::vector<BatchedQR::Block> mb;
+        for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * w * w, w, w});
+        mq = std::make_unique<BatchedQR>(mb, w, true);
+        k_trunc_rank<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, w, mq->R(), dwmin.get(), rtol, dr.get());
+        HG_LAUNCH();
+        count_launch();
+    }
     std::vector<int> r = dl_int(dr);
     int rmax = 0;
     for (int x : r) rmax = std::max(rmax, x);
     auto Pn = rmax ? make_dvec(static_cast<size_t>(n) * static_cast<size_t>(rmax), true) : nullptr;
     if (rmax) {
-        // Tin[2j] = Q_M[:, :r_j]; Tin[2j+1] = P_M R_M[:r_j, :]^T (w x rmax each)
+        // QR mode:  Tin[2j] = Q_M[:, :r_j]; Tin[2j+1] = P_M R_M[:r_j, :]^T
+        // SVD mode: Tin[2j] = U_r Sigma_r;  Tin[2j+1] = V_r           (w x rmax each)
         DVec Tin(static_cast<size_t>(2 * nodes) * w * rmax);
-        std::vector<double*> qo;
-        std::vector<i64> ql;
-        for (int j = 0; j < nodes; ++j) {
-            qo.push_back(Tin.get() + i64(2 * j) * w * rmax);
-            ql.push_back(w);
+        if (svd) {
+            k_svd_tins<<<nodes, 256, 0, ctx.stream>>>(w, rmax, dr.get(), US->get(), VS->get(), Tin.get());
+        } else {
+            std::vector<double*> qo;
+            std::vector<i64> ql;
+            for (int j = 0; j < nodes; ++j) {
+                qo.push_back(Tin.get() + i64(2 * j) * w * rmax);
+                ql.push_back(w);
+            }
+            mq->form_q(rmax, nullptr, 0, 0, qo, ql);
+            k_tins<<<nodes, 256, 0, ctx.stream>>>(w, rmax, dr.get(), mq->R(), mq->perm(), Tin.get());
         }
-        mq.form_q(rmax, nullptr, 0, 0, qo, ql);
-        k_tins<<<nodes, 256, 0, ctx.stream>>>(w, rmax, dr.get(), mq.R(), mq.perm(), Tin.get());
         HG_LAUNCH();
         count_launch();
         // left' = [Q | q2] Q_M[:, :r] on left-child rows (odd rows are overwritten next)

@@ -186,6 +186,25 @@ hg_status hg_ctx_synchronize(hg_ctx_t ctx) { return guard(ctx, [&] { sync(); });
 uint64_t hg_ctx_launches(hg_ctx_t ctx) { return ctx->c.launches; }
 void* hg_ctx_stream(hg_ctx_t ctx) { return ctx->c.stream; }
 
+hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value) {
+    return guard(nullptr, [&] {
+        if (!ctx) throw std::invalid_argument("hg_ctx_set_option: null context");
+        if (option == HG_OPT_PRODUCT_ASSOCIATION && (value == HG_ASSOC_SOLVE || value == HG_ASSOC_REFERENCE))
+            ctx->c.product_assoc = value;
+        else if (option == HG_OPT_COMPRESSION && (value == HG_COMPRESS_PIVOTED_QR || value == HG_COMPRESS_JACOBI_SVD))
+            ctx->c.compression = value;
+        else
+            throw std::invalid_argument("hg_ctx_set_option: unknown option or value");
+    });
+}
+
+int hg_ctx_get_option(hg_ctx_t ctx, int option) {
+    if (!ctx) return -1;
+    if (option == HG_OPT_PRODUCT_ASSOCIATION) return ctx->c.product_assoc;
+    if (option == HG_OPT_COMPRESSION) return ctx->c.compression;
+    return -1;
+}
+
 // ------------------------------------------------------------------- tree
 int hg_tree_depth(int64_t n, int64_t leaf_min, int64_t leaf_max) { return tree_depth(n, leaf_min, leaf_max); }
 

@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/hodlrgp_b200.h"  // HG_OPT_* / HG_ASSOC_* / HG_COMPRESS_* values
+
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -48,7 +50,10 @@ struct Ctx {
     bool own_stream = false;
     int num_sms = 148;
     std::uint64_t launches = 0;  // kernels launched through this context
+    int product_assoc = 0;       // HG_OPT_PRODUCT_ASSOCIATION (HG_ASSOC_*)
+    int compression = 0;         // HG_OPT_COMPRESSION (HG_COMPRESS_*)
 };
+
 
 Ctx& current();           // thread's active context (set by the C ABI)
 void set_current(Ctx* c);

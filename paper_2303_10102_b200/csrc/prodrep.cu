@@ -31,6 +31,20 @@ void level_op(const DFactor& f, int i, bool inverse, double* Y, int w) {
 
 }  // namespace
 
+/// rows += p (q^T rows) per level-(i-1) node with q = u = [wbar 0; 0 xbar]
+/// and p the node's m x 2R panel (product_rep.cpp:32-45): the reference's
+/// association of the Woodbury update, used when HG_OPT_PRODUCT_ASSOCIATION
+/// is HG_ASSOC_REFERENCE.
+void level_update_pq(const DFactor& f, int i, const double* P, double* Y, int w) {
+    const int R = f.Rl(i);
+    if (R == 0 || w <= 0) return;
+    const Partition& p = f.tree->part(i);
+    const i64 n = f.n(), L = i64(p.nseg()) * R;
+    DVec Q(static_cast<size_t>(L) * static_cast<size_t>(w));
+    seg_tn(p, f.Wl(i), n, R, Y, n, w, Q.get(), R, int(L));
+    seg_nn(p, P, n, 2 * R, Q.get(), 2 * R, int(L), TMap::parent(0, 0), Y, n, w, 1.0, 1.0);
+}
+
 void level_multiply(const DFactor& f, int i, double* Y, i64 ldy, int w) {
     const int R = f.Rl(i);
     if (R == 0 || w <= 0) return;
@@ -82,22 +96,34 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
     rep.Cu = make_view(store, S + i64(cuo) * n, static_cast<size_t>(n) * static_cast<size_t>(cw));
     rep.Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(cw), true);
 
+    const bool ref_assoc = inverse && current().product_assoc == HG_ASSOC_REFERENCE;
     for (int i = 1; i <= tau; ++i) {
         const int R = f.Rl(i);
         if (R == 0) continue;
-        // product_rep.cpp:84-104: older corrections' left factors and the
-        // running base's coarser left factors, in one call.
-        const int us = ucum[static_cast<size_t>(i - 1)];
-        level_op(f, i, inverse, S + i64(cuo - us) * n, us + rep.coff[static_cast<size_t>(i - 1)]);
-        // product_rep.cpp:106-119: spawn c.u = p, c.v = B_sub^T q.
         const Partition& p = f.tree->part(i);
         const int C2 = 2 * R;
         double* cu = rep.Cul(i);
-        DVec Q(static_cast<size_t>(n) * static_cast<size_t>(C2));
-        if (inverse) {
-            // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
+        // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
+        auto form_p = [&] {
             seg_nn(p, f.Fl(i), n, R, f.capinvT[static_cast<size_t>(i - 1)]->get(), C2, p.nseg() * R,
                    TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
+        };
+        // product_rep.cpp:84-104: older corrections' left factors and the
+        // running base's coarser left factors, in one call.
+        const int us = ucum[static_cast<size_t>(i - 1)];
+        const int wu = us + rep.coff[static_cast<size_t>(i - 1)];
+        if (ref_assoc) {
+            // The reference's association (product_rep.cpp:32-45,74-78): p is
+            // formed first, then rows += p (q^T rows) with q = u.
+            form_p();
+            level_update_pq(f, i, cu, S + i64(cuo - us) * n, wu);
+        } else {
+            level_op(f, i, inverse, S + i64(cuo - us) * n, wu);
+        }
+        // product_rep.cpp:106-119: spawn c.u = p, c.v = B_sub^T q.
+        DVec Q(static_cast<size_t>(n) * static_cast<size_t>(C2));
+        if (inverse) {
+            if (!ref_assoc) form_p();
             // q = u = [wbar 0; 0 xbar]
             panel_parity_scale(p, n, R, f.Wl(i), n, 1.0, 0.0, Q.get(), n, 0.0);
             panel_parity_scale(p, n, R, f.Wl(i), n, 0.0, 1.0, Q.get() + i64(R) * n, n, 0.0);

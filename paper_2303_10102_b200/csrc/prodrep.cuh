@@ -37,5 +37,7 @@ std::vector<double> prodrep_densify(const DProductRep& p);
 
 /// Y <- (I + u v^T) Y for level i of a Right factorization (multiply path).
 void level_multiply(const DFactor& f, int i, double* Y, i64 ldy, int w);
+/// rows += p (q^T rows) with q = u (the reference association, product_rep.cpp:32-45).
+void level_update_pq(const DFactor& f, int i, const double* P, double* Y, int w);
 
 }  // namespace hg

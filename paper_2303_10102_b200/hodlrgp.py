@@ -22,6 +22,10 @@ lp = C.POINTER(C.c_int64)
 
 HOST, DEVICE = 0, 1
 RIGHT, LEFT = 0, 1
+# Context options (include/hodlrgp_b200.h)
+OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION = 1, 2
+ASSOC_SOLVE, ASSOC_REFERENCE = 0, 1
+COMPRESS_PIVOTED_QR, COMPRESS_JACOBI_SVD = 0, 1
 
 _SIGS = {
     "hg_last_error": (C.c_char_p, []),
@@ -30,6 +34,8 @@ _SIGS = {
     "hg_ctx_synchronize": (C.c_int, [vp]),
     "hg_ctx_launches": (u64, [vp]),
     "hg_ctx_stream": (vp, [vp]),
+    "hg_ctx_set_option": (C.c_int, [vp, C.c_int, C.c_int]),
+    "hg_ctx_get_option": (C.c_int, [vp, C.c_int]),
     "hg_tree_depth": (C.c_int, [i64, i64, i64]),
     "hg_tree_ranges": (C.c_int, [i64, C.c_int, lp]),
     "hg_kd_ordering": (C.c_int, [i64, C.c_int, dp, i64, i64, lp, lp, ip]),
@@ -201,6 +207,14 @@ class Context:
     @property
     def launches(self):
         return int(lib().hg_ctx_launches(self.ptr))
+
+    def set_option(self, option, value):
+        """hg_ctx_set_option: OPT_PRODUCT_ASSOCIATION (ASSOC_SOLVE | ASSOC_REFERENCE),
+        OPT_COMPRESSION (COMPRESS_PIVOTED_QR | COMPRESS_JACOBI_SVD)."""
+        _check(lib().hg_ctx_set_option(self.ptr, option, value))
+
+    def get_option(self, option):
+        return int(lib().hg_ctx_get_option(self.ptr, option))
 
     @property
     def stream(self):
