@@ -13,9 +13,10 @@ Synthetic data: x ~ U[0,1] (numpy seed 0, sorted), y ~ N(0, I) (seed 1; a
 dense N(0,K) draw is infeasible at 2^20), B ~ N(0, I) n x 4 (seed 2). Inputs
 (GBs of factors) exceed L2, so no explicit flush is needed.
 
---impl reference runs the CPU restatement of the reference (oracle/, the
-reference itself cannot be built here: Eigen is absent) on a bounded sample
-and extrapolates with the reference's O(n log^2 n) cost model.
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+/root/reference/proj/src compiled unmodified against the Eigen-API shim) on
+bounded C4-setting samples at three sizes and reports their n log^2 n fit at
+n = 2^20, labelled as extrapolated, with the sizes and times it ran.
 """
 import argparse
 import json
@@ -46,6 +47,7 @@ def parse():
     ap.add_argument("--impl", default="hodlr", choices=["hodlr", "reference"])
     ap.add_argument("--log2n", type=int, default=N_LOG2)
     ap.add_argument("--cpu-sample-log2", type=int, default=13)
+    ap.add_argument("--traffic-json", default=os.path.join(ROOT, "profiles", "r2_traffic.json"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -69,30 +71,67 @@ def config(log2n, tau):
     }
 
 
-def extrapolate(t_sample, n_sample, n):
-    """Reference cost model O(n log^2 n)."""
+def fit_nlog2n(ns, ts):
+    """Least-squares c in t = c n log2(n)^2 (the reference's per-iteration cost
+    model) over the measured (n, t) samples; also the
+    free log-log slope for the record."""
     import math
 
-    return t_sample * (n / n_sample) * (math.log2(n) / math.log2(n_sample)) ** 2
+    f = [n * math.log2(n) ** 2 for n in ns]
+    c = sum(a * b for a, b in zip(f, ts)) / sum(a * a for a in f)
+    slope = None
+    if len(set(ns)) > 1:
+        lx = [math.log(n) for n in ns]
+        ly = [math.log(t) for t in ts]
+        mx, my = sum(lx) / len(lx), sum(ly) / len(ly)
+        slope = sum((a - mx) * (b - my) for a, b in zip(lx, ly)) / sum((a - mx) ** 2 for a in lx)
+    return c, slope
 
 
-def cpu_sample(log2s, steps=1):
-    """Oracle (CPU restatement) MLE iteration on a 2^log2s sample, all host threads."""
+def host_description():
+    d = {"nproc": os.cpu_count()}
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                d["lscpu_model"] = line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal:"):
+                d["MemTotal"] = line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return d
+
+
+def reference_module():
+    """The reference itself (oracle/_ref: /root/reference/proj/src compiled
+    unmodified against the Eigen-API shim); the restated oracle only if that
+    library was not built."""
+    from oracle import pyref as R
+
+    if R.available():
+        return R, "reference"
     from oracle import pyoracle as O
 
-    threads = os.cpu_count() or 1
+    return O, "port"
+
+
+def enable_openblas(M):
     blas = "/opt/prime-rl/.venv/lib/python3.12/site-packages/scipy.libs"
     so = [f for f in os.listdir(blas) if f.startswith("libscipy_openblas")] if os.path.isdir(blas) else []
-    used_blas = bool(so) and O.lib().or_enable_blas(os.path.join(blas, so[0]).encode(), 1) == 1
+    return bool(so) and M.lib().or_enable_blas(os.path.join(blas, so[0]).encode(), 1) == 1
+
+
+def cpu_iteration(M, log2s, cache):
+    """One MLE iteration (acceptance.cpp:297-308) at the C4 settings on n = 2^log2s."""
     n, x, y, _ = workload(log2s)
-    tau = O.tree_depth(n, LEAF, 2 * LEAF)
-    o = O.CovOracle.matern(x, NU2, SIGMA2, ELL, NUGGET, True)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        O.mle_iteration(o, tau, K_RANK, SEED, y, 2, cache=True)
-        times.append(time.perf_counter() - t0)
-    return times, n, threads, used_blas
+    tau = M.tree_depth(n, LEAF, 2 * LEAF)
+    o = M.CovOracle.matern(x, NU2, SIGMA2, ELL, NUGGET, True)
+    t0 = time.perf_counter()
+    _, _, _, stages = M.mle_iteration(o, tau, K_RANK, SEED, y, 2, cache=cache)
+    return time.perf_counter() - t0, n, stages
 
 
 class Clocks:
@@ -137,22 +176,49 @@ class Clocks:
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref),
+    all host threads (OpenMP at its 10 sites, OpenBLAS dgemm inside), as coded
+    (fisher_information recomputes solve_multiply per pair, mle.cpp:43-54).
+    A C4 iteration at n = 2^20 needs ~120 GB and hours on the host, so each
+    step is one iteration at the C4 settings on a bounded n, cycling through
+    2^(s-1), 2^s, 2^(s+1) (s = --cpu-sample-log2); the value is the
+    n log^2 n fit of the timed steps evaluated at n = 2^20 (extrapolated; the
+    sizes, times and fit are in the line)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    M, kind = reference_module()
+    used_blas = enable_openblas(M)
     W, K = args.warmup, args.steps
-    _, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=max(W, 0))
-    times, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=K)
+    sizes = [args.cpu_sample_log2 - 1, args.cpu_sample_log2, args.cpu_sample_log2 + 1]
+    for i in range(max(min(W, 1), 0)):  # a CPU has no warm-up effect beyond page faults; one is enough
+        cpu_iteration(M, sizes[i % 3], cache=False)
+    ns, ts, stages = [], [], {}
+    for i in range(K):
+        t, n_s, st = cpu_iteration(M, sizes[i % 3], cache=False)
+        ns.append(n_s)
+        ts.append(t)
+        stages[n_s] = [float(v) for v in st]
     n = 1 << args.log2n
-    t = extrapolate(statistics.mean(times), n_s, n)
+    c, slope = fit_nlog2n(ns, ts)
+    import math
+
+    t = c * n * math.log2(n) ** 2
     tau = int(np.floor(np.log2(n / LEAF)))
-    sample = (f"oracle/ CPU restatement of the reference, one MLE iteration at n=2^{args.cpu_sample_log2} "
-              f"(same C4 settings), mean {statistics.mean(times):.2f}s, extrapolated to n=2^{args.log2n} "
-              f"by n log^2 n; OpenMP at the reference's sites{', OpenBLAS dgemm' if used_blas else ''}")
+    threads = os.cpu_count() or 1
+    sample = {"what": (f"{'the reference itself (oracle/_ref)' if kind == 'reference' else 'oracle/ restatement'}: "
+                       f"one MLE iteration per step at the C4 settings, as coded (no ProductRep cache)"
+                       f"{', OpenBLAS dgemm' if used_blas else ''}"),
+              "n_run": ns, "seconds": ts, "stage_seconds_by_n": stages,
+              "fit": "t = c n log2(n)^2 (least squares)", "c": c, "loglog_slope": slope,
+              "extrapolated_to_n": n, "host": host_description()}
+    cfg = config(args.log2n, tau)
+    cfg["n_run"] = sorted(set(ns))
+    cfg["extrapolated"] = True
     line = {"impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": args.gpus, "steps": K,
-            "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config(args.log2n, tau),
-            "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+            "warmup": min(W, 1), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -282,17 +348,24 @@ def main():
     dom = max(prof, key=lambda c: prof[c]["ms"])
     d = prof[dom]
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
-    traffic = None
-    try:  # DRAM bytes of the class from the committed ncu capture (profiles/r1_traffic_seg_tn_class.json)
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic_seg_tn_class.json")))
-        if dom == "seg_tn":
-            traffic = sum(v["dram_bytes"] for v in tj.values()) / max(d["launches"], 1)
-    except (OSError, ValueError):
+    # DRAM traffic of the dominant class: only from an ncu capture of THIS
+    # build (scripts/traffic_capture.py writes the .so's sha256 next to the
+    # per-launch dram__bytes); anything else -> null.
+    traffic, traffic_src = None, "no ncu capture of this build"
+    try:
+        import hashlib
+
+        tj = json.load(open(args.traffic_json))
+        sha = hashlib.sha256(open(H.LIB_PATH, "rb").read()).hexdigest()
+        if tj.get("lib_sha256") == sha and tj.get("class") == dom and tj.get("launches"):
+            traffic = tj["dram_bytes"] / tj["launches"]
+            traffic_src = f"{os.path.relpath(args.traffic_json, ROOT)} (ncu, same .so sha256)"
+    except (OSError, ValueError, KeyError):
         pass
     roofline = {"bound": "tensor", "kernel": f"k_{dom}", "achieved": achieved, "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": traffic,
-                "traffic_unit": "DRAM bytes per call (ncu dram__bytes_read+write over one step's k_seg_tn/k_ml_proj/"
-                                "k_ml_update launches / calls)",
+                "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                "traffic_source": traffic_src,
                 "algorithmic_bytes_per_call": d["bytes"] / max(d["launches"], 1),
                 "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                 "launches": d["launches"], "share_of_step": d["ms"] / sum(v["ms"] for v in prof.values())}
@@ -335,12 +408,23 @@ def main():
         v["hbm_frac"] = v["GB/s"] / hbm
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, n_s, threads, used_blas = cpu_sample(args.cpu_sample_log2, steps=1)
-        t_ext = extrapolate(times[0], n_s, n)
-        cpu = {"value": t_ext, "unit": "s", "cores": threads, "kind": "port",
-               "sample": (f"oracle/ restatement, one MLE iteration at n=2^{args.cpu_sample_log2} in {times[0]:.2f}s, "
-                          f"extrapolated to n=2^{args.log2n} by n log^2 n"
-                          f"{' (OpenBLAS dgemm)' if used_blas else ''}")}
+        # bounded sample (~20-30 s of host time): the reference at the C4
+        # settings on n = 2^(s-1) and 2^s, cached and as coded, fitted n log^2 n
+        import math
+
+        M, kind = reference_module()
+        used_blas = enable_openblas(M)
+        runs = {}
+        for cache in (False, True):
+            pts = [cpu_iteration(M, args.cpu_sample_log2 + d, cache)[:2] for d in (-1, 0)]
+            cc, slope = fit_nlog2n([p[1] for p in pts], [p[0] for p in pts])
+            runs["cached" if cache else "as_coded"] = {"n_run": [p[1] for p in pts], "seconds": [p[0] for p in pts],
+                                                       "extrapolated_s": cc * n * math.log2(n) ** 2}
+        cpu = {"value": runs["as_coded"]["extrapolated_s"], "unit": "s", "cores": os.cpu_count() or 1, "kind": kind,
+               "sample": {"what": (f"{'the reference itself (oracle/_ref)' if kind == 'reference' else 'restated oracle'}"
+                                   f", one MLE iteration at the C4 settings per n{', OpenBLAS dgemm' if used_blas else ''}"
+                                   f"; value = as coded, n log^2 n fit at n = 2^{args.log2n} (extrapolated)"),
+                          **runs, "host": host_description()}}
     if rank == 0:
         line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",

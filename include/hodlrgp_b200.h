@@ -173,6 +173,10 @@ hg_status hg_oracle_cokriging(hg_ctx_t ctx, int64_t m, double sigma2, double ell
                               hg_oracle_t* out);
 hg_status hg_oracle_spde2d(hg_ctx_t ctx, int nside, double sigma2, double ell, double kappa, double nugget,
                            const int64_t* order, hg_oracle_t* out);
+/* PermutedOracle (oracle.hpp:58-111): the view K'(i,j) = K(p_i, p_j) of any
+ * oracle under to_base[reordered position] = base index (host array, copied).
+ * The base must outlive the view; applies advance both oracles' counters. */
+hg_status hg_oracle_permuted(hg_ctx_t ctx, hg_oracle_t base, const int64_t* to_base, hg_oracle_t* out);
 hg_status hg_oracle_set_parameters(hg_oracle_t o, const double* theta, int p);
 hg_status hg_oracle_free(hg_oracle_t o);
 /* apply (j = -1) / apply_derivative (j >= 0) — oracle.hpp:25-35 */

@@ -454,6 +454,13 @@ hg_status hg_oracle_callback(hg_ctx_t ctx, int64_t n, int p, hg_apply_fn fn, voi
     return guard(ctx, [&] { *out = new hg_oracle_s{make_callback_oracle(n, p, reinterpret_cast<ApplyFn>(fn), user)}; });
 }
 
+hg_status hg_oracle_permuted(hg_ctx_t ctx, hg_oracle_t base, const int64_t* to_base, hg_oracle_t* out) {
+    return guard(ctx, [&] {
+        if (!base) throw std::invalid_argument("hg_oracle_permuted: null base oracle");
+        *out = new hg_oracle_s{make_permuted_oracle(base->o.get(), to_base)};
+    });
+}
+
 hg_status hg_oracle_set_parameters(hg_oracle_t o, const double* theta, int p) {
     return guard(nullptr, [&] { o->o->set_parameters(theta, p); });
 }

@@ -126,7 +126,8 @@ public:
     MaternOracle(i64 n, const double* x, int nu2, double sigma2, double ell, double nugget, bool scan)
         : DOracle(n, 2), nu2_(nu2), sigma2_(sigma2), ell_(ell), nugget_(nugget), scan_(scan) {
         if (nu2 != 1 && nu2 != 3 && nu2 != 5) throw std::invalid_argument("Matern: nu in {1/2, 3/2, 5/2}");
-        for (i64 i = 1; i < n; ++i)
+        // the scan recurrence needs sorted points; the dense kernel takes any order
+        for (i64 i = 1; scan && i < n; ++i)
             if (x[i] < x[i - 1]) throw std::invalid_argument("Matern: points must be sorted");
         x_.upload(x, static_cast<size_t>(n));
     }
@@ -211,7 +212,59 @@ private:
     void* user_;
 };
 
+/// Row gather/scatter of a column-major panel: dst[perm? ...] (see PermutedOracle).
+__global__ void k_permute_rows(i64 n, int s, const i64* p, const double* src, i64 lds, double* dst, i64 ldd,
+                               int scatter) {
+    const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (i >= n || c >= s) return;
+    if (scatter)
+        dst[p[i] + c * ldd] = src[i + c * lds];  // reordered layout -> base layout
+    else
+        dst[i + c * ldd] = src[p[i] + c * lds];  // base layout -> reordered layout
+}
+
+/// PermutedOracle (oracle.hpp:58-111): K'(i, j) = K(p_i, p_j) with p mapping
+/// reordered positions to base indices; V is scattered into the base layout,
+/// the base oracle applied (its counters advance too, like base_.apply), and
+/// the result gathered back. The base must outlive this view.
+class PermutedOracle : public DOracle {
+public:
+    PermutedOracle(DOracle* base, const std::int64_t* to_base) : DOracle(base->dim(), base->num_params()), base_(base) {
+        std::vector<i64> p(to_base, to_base + n_);  // int64_t -> i64
+        std::vector<char> seen(static_cast<size_t>(n_), 0);
+        for (i64 v : p) {
+            if (v < 0 || v >= n_ || seen[static_cast<size_t>(v)])
+                throw std::invalid_argument("PermutedOracle: permutation size mismatch");
+            seen[static_cast<size_t>(v)] = 1;
+        }
+        p_.upload(p);
+    }
+    void set_parameters(const double* theta, int p) override { base_->set_parameters(theta, p); }
+
+protected:
+    void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {
+        DVec W(static_cast<size_t>(n_) * s), Z(static_cast<size_t>(n_) * s);
+        dim3 grid(unsigned(cdiv(n_, 256)), unsigned(s));
+        k_permute_rows<<<grid, 256, 0, current().stream>>>(n_, s, p_.get(), V, ldv, W.get(), n_, 1);
+        HG_LAUNCH();
+        count_launch();
+        base_->apply(j, W.get(), n_, s, Z.get(), n_);
+        k_permute_rows<<<grid, 256, 0, current().stream>>>(n_, s, p_.get(), Z.get(), n_, Y, ldy, 0);
+        HG_LAUNCH();
+        count_launch();
+    }
+
+private:
+    DOracle* base_;
+    DBuf<i64> p_;
+};
+
 }  // namespace
+
+std::unique_ptr<DOracle> make_permuted_oracle(DOracle* base, const std::int64_t* to_base) {
+    return std::make_unique<PermutedOracle>(base, to_base);
+}
 
 std::unique_ptr<DOracle> make_dense_oracle(i64 n, const double* K, int p, const double* dK) {
     return std::make_unique<DenseOracle>(n, K, p, dK);

@@ -73,6 +73,10 @@ using ApplyFn = int (*)(void* user, int j, const double* V, std::int64_t ldv, st
                         std::int64_t ldy, void* stream);
 std::unique_ptr<DOracle> make_callback_oracle(i64 n, int p, ApplyFn fn, void* user);
 
+/// PermutedOracle (oracle.hpp:58-111) over any device oracle; to_base (host,
+/// n entries) maps reordered positions to base indices. base must outlive it.
+std::unique_ptr<DOracle> make_permuted_oracle(DOracle* base, const std::int64_t* to_base);
+
 /// Plain C = alpha A B + beta C (A m x k, B k x n), via the segmented engine.
 void gemm_nn(i64 m, int n, int k, const double* A, i64 lda, const double* B, i64 ldb, double* C, i64 ldc,
              double alpha, double beta);

@@ -81,6 +81,7 @@ _SIGS = {
     "hg_oracle_spde2d": (C.c_int, [vp, C.c_int, dbl, dbl, dbl, dbl, C.c_void_p, C.POINTER(vp)]),
     "hg_oracle_callback": (C.c_int, [vp, i64, C.c_int, vp, vp, C.POINTER(vp)]),
     "hg_oracle_set_parameters": (C.c_int, [vp, dp, C.c_int]),
+    "hg_oracle_permuted": (C.c_int, [vp, vp, lp, C.POINTER(vp)]),
     "hg_oracle_free": (C.c_int, [vp]),
     "hg_oracle_apply": (C.c_int, [vp, vp, C.c_int, vp, i64, i64, vp, i64, C.c_int]),
     "hg_oracle_counters": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.c_int]),
@@ -623,6 +624,18 @@ def DenseMatrixOracle(k, dks=(), ctx=None):
     o = vp()
     _check(lib().hg_oracle_dense(ctx.ptr, n, _d(k), len(dks), _d(buf), C.byref(o)))
     return CovarianceOracle(o, ctx, n, len(dks))
+
+
+def PermutedOracle(base, to_base):
+    """oracle.hpp:58-111: the view K'(i, j) = K(p_i, p_j) of any device oracle,
+    to_base[reordered position] = base index. Keeps `base` alive."""
+    p = np.ascontiguousarray(to_base, dtype=np.int64)
+    o = vp()
+    _check(lib().hg_oracle_permuted(base.ctx.ptr, base.ptr, p.ctypes.data_as(lp), C.byref(o)))
+    view = CovarianceOracle(o, base.ctx, base.n, base.p)
+    view.base = base
+    view.to_base = p
+    return view
 
 
 def MaternOracle(x, nu2, sigma2, ell, nugget, scan=True, ctx=None):
