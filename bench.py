@@ -350,16 +350,19 @@ def main():
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
     # DRAM traffic of the dominant class: only from an ncu capture of THIS
     # build (scripts/traffic_capture.py writes the .so's sha256 next to the
-    # per-launch dram__bytes); anything else -> null.
+    # class's DRAM bytes over one step); per ledger call = step bytes / this
+    # step's ledger call count for the class. Anything else -> null.
     traffic, traffic_src = None, "no ncu capture of this build"
     try:
         import hashlib
 
         tj = json.load(open(args.traffic_json))
         sha = hashlib.sha256(open(H.LIB_PATH, "rb").read()).hexdigest()
-        if tj.get("lib_sha256") == sha and tj.get("class") == dom and tj.get("launches"):
-            traffic = tj["dram_bytes"] / tj["launches"]
-            traffic_src = f"{os.path.relpath(args.traffic_json, ROOT)} (ncu, same .so sha256)"
+        tc = tj.get("classes", {}).get(dom)
+        if tj.get("lib_sha256") == sha and tc and d["launches"]:
+            traffic = tc["dram_bytes"] / d["launches"]
+            traffic_src = (f"{os.path.relpath(args.traffic_json, ROOT)} (ncu, same .so sha256): "
+                           f"{tc['dram_bytes']:.4g} B over one step's {tc['kernels']} kernels / {d['launches']} ledger calls")
     except (OSError, ValueError, KeyError):
         pass
     roofline = {"bound": "tensor", "kernel": f"k_{dom}", "achieved": achieved, "peak": fp64_peak,

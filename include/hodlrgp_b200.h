@@ -60,10 +60,17 @@ void* hg_ctx_stream(hg_ctx_t ctx);
  *  HG_OPT_COMPRESSION — truncation of the derivative blocks' cores
  *    (LowRankBlock::compressed, hodlr_matrix.cpp:42-66): HG_COMPRESS_PIVOTED_QR
  *    (default, rank-revealing pivoted QR at the same 1e-13 threshold) or
- *    HG_COMPRESS_JACOBI_SVD (singular values, as the reference). */
-enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2 };
+ *    HG_COMPRESS_JACOBI_SVD (singular values, as the reference).
+ *  HG_OPT_Q2_BASIS — the derivative build's second basis q2 (sketch.cpp:194-233).
+ *    HG_Q2_REORTHOGONALIZED (default): q2 is projected against q once more and
+ *    renormalised, so [q | q2] is orthonormal to roundoff; columns kept near
+ *    the w2 floor otherwise overlap q and double-count dK q in the committed
+ *    derivative block (the error that dominates dK/dtheta at n = 2^20).
+ *    HG_Q2_REFERENCE: q2 exactly as the reference forms it (parity mode). */
+enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2, HG_OPT_Q2_BASIS = 3 };
 enum { HG_ASSOC_SOLVE = 0, HG_ASSOC_REFERENCE = 1 };
 enum { HG_COMPRESS_PIVOTED_QR = 0, HG_COMPRESS_JACOBI_SVD = 1 };
+enum { HG_Q2_REORTHOGONALIZED = 0, HG_Q2_REFERENCE = 1 };
 hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value);
 int hg_ctx_get_option(hg_ctx_t ctx, int option);
 

@@ -88,6 +88,7 @@ const char* or_last_error() { return g_err.c_str(); }
 int or_enable_blas(const char* path, int threads) { return enable_external_blas(path, threads) ? 1 : 0; }
 const char* or_blas_backend() { return blas_backend(); }
 void or_set_solve_association(int on) { set_solve_association(on != 0); }
+void or_set_q2_reorthogonalize(int on) { set_q2_reorthogonalize(on != 0); }
 
 // ------------------------------------------------------------------ tree
 int or_tree_depth(std::int64_t n, std::int64_t lmin, std::int64_t lmax) { return tree_depth(n, lmin, lmax); }

@@ -109,6 +109,11 @@ const char* g_backend = "builtin";
 }  // namespace
 
 bool enable_external_blas(const char* path, int threads) {
+    if (!path || !*path) {  // back to the built-in loops
+        g_dgemm = nullptr;
+        g_backend = "builtin";
+        return true;
+    }
     void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
     if (!h) return false;
     auto f = reinterpret_cast<dgemm_fn>(dlsym(h, "scipy_dgemm_"));

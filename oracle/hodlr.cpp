@@ -13,7 +13,11 @@
 #include "oracle.hpp"
 #include "matern1d.hpp"
 
+
 namespace oracle {
+
+bool g_q2_reorthogonalize = false;
+void set_q2_reorthogonalize(bool on) { g_q2_reorthogonalize = on; }
 
 // ============================================================ cluster tree
 // cluster_tree.cpp:10-22
@@ -642,6 +646,16 @@ BuildResult build_impl(const CovarianceOracle& oracle, const ClusterTree& tree, 
                 while (w2 < w2cap && std::abs(qr2.qr(w2, w2)) > floor_) ++w2;
                 w2s[static_cast<size_t>(j)] = w2;
                 if (w2 > 0) q2[static_cast<size_t>(j)] = qr2.householder_q_thin(w2);
+                if (w2 > 0 && g_q2_reorthogonalize) {  // device HG_Q2_REORTHOGONALIZED
+                    Mat& b = q2[static_cast<size_t>(j)];
+                    b = b - matmul(q, matmul_t(q, true, b, false));
+                    for (Index c = 0; c < b.c; ++c) {
+                        double nn = 0;
+                        for (Index r = 0; r < b.r; ++r) nn += b(r, c) * b(r, c);
+                        const double inv = nn > 0 ? 1.0 / std::sqrt(nn) : 0.0;
+                        for (Index r = 0; r < b.r; ++r) b(r, c) *= inv;
+                    }
+                }
             }
             for (Index j = 0; j < nodes; ++j) {
                 const Mat& b = q2[static_cast<size_t>(j)];

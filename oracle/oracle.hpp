@@ -417,6 +417,10 @@ struct ProductRep {
 /// the association the device path uses; identical in exact arithmetic but
 /// it avoids forming p when the capacitance is ill-conditioned.
 void set_solve_association(bool on);
+/// Diagnostic switch (default off = the reference, sketch.cpp:194-233). On:
+/// each q2 is projected against q once more and its columns renormalised,
+/// the device's default HG_Q2_REORTHOGONALIZED.
+void set_q2_reorthogonalize(bool on);
 ProductRep multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 ProductRep solve_multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 double trace_product_rep(const ProductRep& p);

@@ -47,6 +47,7 @@ def lib():
             "or_enable_blas": (C.c_int, [C.c_char_p, C.c_int]),
             "or_blas_backend": (C.c_char_p, []),
             "or_set_solve_association": (None, [C.c_int]),
+            "or_set_q2_reorthogonalize": (None, [C.c_int]),
             "or_tree_depth": (C.c_int, [i64, i64, i64]),
             "or_tree_ranges": (C.c_int, [i64, C.c_int, lp]),
             "or_kd_ordering": (C.c_int, [i64, C.c_int, dp, i64, i64, lp, lp, ip]),
@@ -140,6 +141,11 @@ def _f(a):
 def set_solve_association(on):
     """Diagnostic: product association of the device path (see oracle.hpp)."""
     lib().or_set_solve_association(int(on))
+
+
+def set_q2_reorthogonalize(on):
+    """Diagnostic: the device's default q2 basis (HG_Q2_REORTHOGONALIZED, see oracle.hpp)."""
+    lib().or_set_q2_reorthogonalize(int(on))
 
 
 def randn(r, c, seed):

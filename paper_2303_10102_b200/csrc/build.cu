@@ -227,6 +227,20 @@ __global__ void k_w2_nodes(int nodes, const int* bounds, int k, int kp, const in
     w2out[j] = w2;
 }
 
+/// Column c < w_j of node j's left-child rows scaled to unit norm (after the
+/// re-orthogonalisation of q2 against q, HG_Q2_REORTHOGONALIZED).
+__global__ void k_col_normalize(const int* bounds, const int* wj, double* P, i64 ldp) {
+    const int j = blockIdx.x, c = blockIdx.y;
+    if (c >= wj[j]) return;
+    const int lo = bounds[2 * j], m = bounds[2 * j + 1] - lo;
+    double* col = P + i64(lo) + i64(c) * ldp;
+    double s = 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) s += col[r] * col[r];
+    s = cta_sum(s);
+    const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) col[r] *= inv;
+}
+
 /// Zero columns [w_j, wtot) of the rows of one child (odd = right) of node j.
 __global__ void k_mask_cols(const int* bounds, int odd, const int* wj, int wtot, double* P, i64 ldp) {
     const int j = blockIdx.x;
@@ -961,6 +975,22 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dw2.get(), w2max, S2.get(), n);
                 HG_LAUNCH();
                 ++ctx.launches;
+                if (ctx.q2_basis == HG_Q2_REORTHOGONALIZED) {
+                    // q2 columns kept near the w2 floor are the normalised
+                    // projection roundoff of the derivative sketch and overlap q
+                    // by up to roundoff / floor; that overlap double-counts
+                    // dK q in the committed block [dqc | q | q2][t | dt | dt2]^T.
+                    // One more projection against q (CGS2) and a
+                    // renormalisation make [q | q2] orthonormal to roundoff.
+                    DVec G2(static_cast<size_t>(2 * nodes) * k * w2max);
+                    seg_tn(pc, S.get(), n, k, S2.get(), n, w2max, G2.get(), i64(k) * w2max, k);
+                    seg_nn(pc, S.get(), n, k, G2.get(), i64(k) * w2max, k, TMap::same(), S2.get(), n, w2max, -1.0,
+                           1.0);
+                    k_col_normalize<<<dim3(unsigned(nodes), unsigned(w2max)), 256, 0, ctx.stream>>>(
+                        pc.dbounds(), dw2.get(), S2.get(), n);
+                    HG_LAUNCH();
+                    ++ctx.launches;
+                }
             }
         }
 

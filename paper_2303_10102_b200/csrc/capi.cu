@@ -193,6 +193,8 @@ hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value) {
             ctx->c.product_assoc = value;
         else if (option == HG_OPT_COMPRESSION && (value == HG_COMPRESS_PIVOTED_QR || value == HG_COMPRESS_JACOBI_SVD))
             ctx->c.compression = value;
+        else if (option == HG_OPT_Q2_BASIS && (value == HG_Q2_REORTHOGONALIZED || value == HG_Q2_REFERENCE))
+            ctx->c.q2_basis = value;
         else
             throw std::invalid_argument("hg_ctx_set_option: unknown option or value");
     });
@@ -202,6 +204,7 @@ int hg_ctx_get_option(hg_ctx_t ctx, int option) {
     if (!ctx) return -1;
     if (option == HG_OPT_PRODUCT_ASSOCIATION) return ctx->c.product_assoc;
     if (option == HG_OPT_COMPRESSION) return ctx->c.compression;
+    if (option == HG_OPT_Q2_BASIS) return ctx->c.q2_basis;
     return -1;
 }
 

@@ -52,6 +52,7 @@ struct Ctx {
     std::uint64_t launches = 0;  // kernels launched through this context
     int product_assoc = 0;       // HG_OPT_PRODUCT_ASSOCIATION (HG_ASSOC_*)
     int compression = 0;         // HG_OPT_COMPRESSION (HG_COMPRESS_*)
+    int q2_basis = 0;            // HG_OPT_Q2_BASIS (HG_Q2_*)
 };
 
 

@@ -530,6 +530,65 @@ void cap_solve(const DFactor& f, int i, const double* Q, bool top_odd, bool tran
     count_launch();
 }
 
+/// p = -v cap^{-T} of every level-i node by LU substitution per row of v
+/// (product_rep.cpp:74-78: p = -(cap.solve(v^T))^T), the reference's own
+/// association; v = [0 w; x 0] from the source panel F. One thread per row.
+__global__ void k_cap_p_rows(int R, const int* bounds, const double* lu, const int* piv_all, const double* F, i64 n,
+                             double* P) {
+    extern __shared__ double sm[];
+    const int j = blockIdx.x, m = 2 * R, nthr = blockDim.x, c = threadIdx.x;
+    const int lo = bounds[2 * j], mid = bounds[2 * j + 1], hi = bounds[2 * j + 2];
+    const int row = lo + blockIdx.y * nthr + c;
+    if (row >= hi) return;
+    const double* A = lu + i64(j) * m * m;
+    const int* piv = piv_all + i64(j) * m;
+    double* x = sm;  // x[r * nthr + c]
+    const bool left = row < mid;
+    for (int r = 0; r < m; ++r) {
+        const bool src = left ? r >= R : r < R;
+        x[r * nthr + c] = src ? F[row + i64(left ? r - R : r) * n] : 0.0;
+    }
+    for (int k = 0; k < m; ++k) {
+        const int p = piv[k];
+        if (p != k) {
+            const double t = x[k * nthr + c];
+            x[k * nthr + c] = x[p * nthr + c];
+            x[p * nthr + c] = t;
+        }
+    }
+    for (int i = 0; i < m; ++i) {  // unit lower
+        double s = x[i * nthr + c];
+        for (int p = 0; p < i; ++p) s -= A[i + i64(p) * m] * x[p * nthr + c];
+        x[i * nthr + c] = s;
+    }
+    for (int i = m - 1; i >= 0; --i) {  // upper
+        double s = x[i * nthr + c];
+        for (int p = i + 1; p < m; ++p) s -= A[i + i64(p) * m] * x[p * nthr + c];
+        x[i * nthr + c] = s / A[i + i64(i) * m];
+    }
+    for (int r = 0; r < m; ++r) P[row + i64(r) * n] = -x[r * nthr + c];
+}
+
+void form_p_reference_impl(const DFactor& f, int i, double* P) {
+    const int R = f.Rl(i), m = 2 * R;
+    if (R == 0) return;
+    const Partition& p = f.tree->part(i);
+    const int nodes = p.nseg() / 2;
+    int maxrows = 0;
+    for (int j = 0; j < nodes; ++j) maxrows = std::max(maxrows, p.hbounds()[2 * j + 2] - p.hbounds()[2 * j]);
+    int thr = 64;
+    while (thr > 8 && static_cast<size_t>(m) * thr * sizeof(double) > SMEM_CAP) thr >>= 1;
+    const size_t smem = static_cast<size_t>(m) * thr * sizeof(double);
+    if (smem > SMEM_CAP) throw std::length_error("form_p_reference: capacitance too large for shared memory");
+    ProfScope prof(PROF_CAP_SOLVE, 2.0 * double(f.n()) * m * m, 8.0 * nodes * double(m) * m + 16.0 * f.n() * m);
+    set_smem(reinterpret_cast<const void*>(k_cap_p_rows), smem);
+    dim3 grid(unsigned(nodes), unsigned(cdiv(maxrows, thr)));
+    k_cap_p_rows<<<grid, thr, smem, current().stream>>>(R, p.dbounds(), f.cap[static_cast<size_t>(i - 1)]->get(),
+                                                       f.cap_piv[static_cast<size_t>(i - 1)]->get(), f.Fl(i), f.n(), P);
+    HG_LAUNCH();
+    count_launch();
+}
+
 /// Node panels (nodes*m rows, ld L = nodes*m) of the capacitance operators,
 /// with Pi the half swap so that node j's right-hand side is the contiguous
 /// block [Q_{2j}; Q_{2j+1}]:
@@ -611,6 +670,8 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
 }  // namespace
 
 void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w) { leaf_solve_subst(f, Y, ldy, w); }
+
+void form_p_reference(const DFactor& f, int i, double* P) { form_p_reference_impl(f, i, P); }
 
 void level_inverse(const DFactor& f, int i, bool transposed, double* Y, i64 ldy, int w) {
     const int R = f.Rl(i);

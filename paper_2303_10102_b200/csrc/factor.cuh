@@ -57,6 +57,9 @@ void leaf_solve(const DFactor& f, double* Y, i64 ldy, int w);
 ///   transposed = false: Y -= u cap^{-1} v^T Y   (Right solve, factorize)
 ///   transposed = true : Y -= v cap^{-T} u^T Y   (Left solve, pipeline)
 void level_inverse(const DFactor& f, int i, bool transposed, double* Y, i64 ldy, int w);
+/// p = -v cap^{-T} (n x 2R, ld n) of level i by LU substitution per row, the
+/// reference's association (HG_ASSOC_REFERENCE; product_rep.cpp:74-78).
+void form_p_reference(const DFactor& f, int i, double* P);
 
 /// HodlrFactorization::solve (factorization.cpp:170-212), in place.
 void factor_solve(const DFactor& f, double* Y, i64 ldy, int w);

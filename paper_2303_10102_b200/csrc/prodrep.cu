@@ -105,8 +105,11 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         double* cu = rep.Cul(i);
         // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
         auto form_p = [&] {
-            seg_nn(p, f.Fl(i), n, R, f.capinvT[static_cast<size_t>(i - 1)]->get(), C2, p.nseg() * R,
-                   TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
+            if (ref_assoc)  // the reference's LU substitution on v^T (no explicit inverse)
+                form_p_reference(f, i, cu);
+            else
+                seg_nn(p, f.Fl(i), n, R, f.capinvT[static_cast<size_t>(i - 1)]->get(), C2, p.nseg() * R,
+                       TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
         };
         // product_rep.cpp:84-104: older corrections' left factors and the
         // running base's coarser left factors, in one call.

@@ -23,7 +23,8 @@ lp = C.POINTER(C.c_int64)
 HOST, DEVICE = 0, 1
 RIGHT, LEFT = 0, 1
 # Context options (include/hodlrgp_b200.h)
-OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION = 1, 2
+OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION, OPT_Q2_BASIS = 1, 2, 3
+Q2_REORTHOGONALIZED, Q2_REFERENCE = 0, 1
 ASSOC_SOLVE, ASSOC_REFERENCE = 0, 1
 COMPRESS_PIVOTED_QR, COMPRESS_JACOBI_SVD = 0, 1
 

@@ -17,6 +17,7 @@ from oracle import pyoracle as O
 from paper_2303_10102_b200 import hodlrgp as H
 
 O.set_solve_association(True)
+O.set_q2_reorthogonalize(True)  # the device defaults
 SIG2, ELL, NUG, K, SEED = 1.0, 0.05, 1e-6, 40, 7
 args = [int(a) for a in sys.argv[1:] if not a.startswith("--")]
 cpu_max = 0

@@ -1,6 +1,8 @@
 """Which GPU build stage costs derivative accuracy at large n (C4 settings)?
 Per-level errors of D0/D1 and the GPU Fisher for build variants:
-  default  — scan oracle with masked peel applies, pivoted-QR recompression
+  default  — scan oracle with masked peel applies, pivoted-QR recompression,
+             q2 re-orthogonalised against q
+  q2ref    — q2 as the reference forms it (HG_Q2_REFERENCE)
   svd      — HG_COMPRESS_JACOBI_SVD recompression
   unmasked — the same scan oracle behind a callback (no masked applies)
   cpu      — the restated CPU oracle's build (n <= --cpu)
@@ -55,8 +57,9 @@ for lg in args:
     print(f"===== n = 2^{lg} tau = {tau}", flush=True)
     g = H.MaternOracle(x, 5, SIG2, ELL, NUG, True)
     ctx = H.context()
-    for name in ("default", "svd", "unmasked"):
+    for name in ("default", "q2ref", "svd", "unmasked"):
         ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_JACOBI_SVD if name == "svd" else H.COMPRESS_PIVOTED_QR)
+        ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REFERENCE if name == "q2ref" else H.Q2_REORTHOGONALIZED)
         orc = unmasked(g) if name == "unmasked" else g
         br = H.build_hodlr_with_derivatives(orc, H.ClusterTree(n, tau), K, SEED)
         gp = [br.h.export_panels()] + [d.export_panels() for d in br.deriv]
@@ -64,6 +67,7 @@ for lg in args:
         s, f = fisher(br.h, br.deriv, y)
         print(f"{name} score {s} F {f.ravel()}  F_ss/(n/2) {f[0, 0] / (n / 2):.5f}", flush=True)
     ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_PIVOTED_QR)
+    ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REORTHOGONALIZED)
     if lg <= cpu_max:
         o = O.CovOracle.matern(x, 5, SIG2, ELL, NUG, True)
         bo = O.Build(o, tau, K, SEED, True, 2)

@@ -36,10 +36,12 @@ for a in (H.ASSOC_SOLVE, H.ASSOC_REFERENCE):
     for c in (H.COMPRESS_PIVOTED_QR, H.COMPRESS_JACOBI_SVD):
         ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, a)
         ctx.set_option(H.OPT_COMPRESSION, c)
+        ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REFERENCE if a == H.ASSOC_REFERENCE else H.Q2_REORTHOGONALIZED)
         res[f"device/{'solve' if a == 0 else 'ref'}/{'qr' if c == 0 else 'svd'}"] = H.mle_iteration(
             H.MaternOracle(x, *args, True), tau, 24, 0, y)[:3]
 ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, H.ASSOC_SOLVE)
 ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_PIVOTED_QR)
+ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REORTHOGONALIZED)
 ll, s, f = H.dense_exact(H.MaternOracle(x, *args, False), y)[:3] if n <= 8192 else (None, None, None)
 if ll is not None:
     res["dense"] = (ll, s, f)

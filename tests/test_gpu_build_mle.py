@@ -108,9 +108,46 @@ def c1_points(n=4096):
     return np.sort(np.random.default_rng(0).uniform(size=n))
 
 
-@pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4),
-                                                    (2048, 128, 40, 5, 0.05, 1e-6), (1500, 64, 16, 3, 0.2, 1e-4)])
-def test_build_parity_vs_oracle(H, n, leaf, k, nu2, ell, nug):
+@pytest.fixture
+def reference_modes(H):
+    """Device in the reference-faithful parity modes (product association of
+    product_rep.cpp:32-45,74-78, Jacobi-SVD truncation of hodlr_matrix.cpp:42-66,
+    q2 exactly as sketch.cpp:194-233) for the duration of one test."""
+    ctx = H.context()
+    ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, H.ASSOC_REFERENCE)
+    ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_JACOBI_SVD)
+    ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REFERENCE)
+    yield ctx
+    ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, H.ASSOC_SOLVE)
+    ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_PIVOTED_QR)
+    ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REORTHOGONALIZED)
+
+
+@pytest.fixture
+def oracle_q2_reorth():
+    """The oracle switched to the device's default q2 basis (oracle.hpp)."""
+    O.set_q2_reorthogonalize(True)
+    yield
+    O.set_q2_reorthogonalize(False)
+
+
+BUILD_CASES = [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4), (2048, 128, 40, 5, 0.05, 1e-6),
+               (1500, 64, 16, 3, 0.2, 1e-4)]
+
+
+@pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", BUILD_CASES)
+def test_build_parity_vs_oracle(H, oracle_q2_reorth, n, leaf, k, nu2, ell, nug):
+    """Device defaults against the oracle with the same q2 basis switch."""
+    _build_parity(H, n, leaf, k, nu2, ell, nug)
+
+
+@pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", BUILD_CASES)
+def test_build_parity_reference_modes(H, reference_modes, n, leaf, k, nu2, ell, nug):
+    """Device in the reference-faithful modes against the unmodified oracle."""
+    _build_parity(H, n, leaf, k, nu2, ell, nug)
+
+
+def _build_parity(H, n, leaf, k, nu2, ell, nug):
     x = np.sort(np.random.default_rng(n).uniform(size=n))
     tau = O.tree_depth(n, leaf, 2 * leaf)
     oo = O.CovOracle.matern(x, nu2, 1.0, ell, nug, True)
@@ -119,7 +156,7 @@ def test_build_parity_vs_oracle(H, n, leaf, k, nu2, ell, nug):
     db = H.build_hodlr_with_derivatives(do, H.ClusterTree(n, tau), k, 0)
     dec_o, dec_d = ob.decisions(), db.decisions()
     mism = int((dec_o != dec_d).any(axis=1).sum())
-    assert mism <= max(1, len(dec_o) // 100), (mism, len(dec_o))
+    assert mism == 0, (mism, len(dec_o), np.nonzero((dec_o != dec_d).any(axis=1))[0][:10])
     if n <= 4096:
         a0, a1 = ob.h().densify(), db.h.densify()
         assert np.linalg.norm(a1 - a0) <= 1e-10 * np.linalg.norm(a0)
@@ -255,3 +292,77 @@ def test_build_long_deficient_blocks(H):
             a, b = lv[l][2 * j]
             Q = U[a:b]
             assert np.abs(Q.T @ Q - np.eye(Rl)).max() <= 1e-12
+
+
+def _openblas():
+    import os
+
+    d = os.path.join(os.path.dirname(np.__file__), "..", "scipy.libs")
+    so = [f for f in os.listdir(d) if f.startswith("libscipy_openblas")] if os.path.isdir(d) else []
+    return os.path.join(d, so[0]).encode() if so else None
+
+
+def _spread(runs, base):
+    """Largest relative deviation of any run from `base`, per output."""
+    return [max(_rel(r[i], base[i]) for r in runs) for i in range(len(base))]
+
+
+def test_mle_glue_c1_reference_association(H, reference_modes):
+    """mle.cpp:25-54 on identical H, dK/dtheta_j with the device in the
+    reference's product association (HG_ASSOC_REFERENCE, p formed by LU
+    substitution as product_rep.cpp:74-78) against the reference itself
+    (oracle/_ref).
+
+    That association is ill-conditioned at C1 (cond(cap) ~ 1e7): the
+    reference's own score/Fisher move by ~3e-7 / ~3e-5 when only the
+    summation order of its dgemm changes (built-in loops vs OpenBLAS), and
+    the restated oracle sits inside that spread. Stated tolerance: the
+    device within 2x the reference's own spread; loglik (no p involved)
+    1e-12. The solve association (default) is held to 1e-9 / 1e-7 above."""
+    from oracle import pyref as R
+
+    n, tau, k, x, oo, K, y = _c1_setup()
+    ob = O.Build(oo, tau, k, 0, True, p=2)
+    oh, od = ob.h(), [ob.deriv(0), ob.deriv(1)]
+    dh, dd = dev(H, oh), [dev(H, d) for d in od]
+    df = H.factorize(dh, H.LEFT)
+    dev_out = (H.score(df, dd, y), H.fisher_information(df, dd))
+    runs = []
+    for M in ([R] if R.available() else []) + [O]:
+        mh, md = M.Hodlr.import_panels(oh.export_panels()), [M.Hodlr.import_panels(d.export_panels()) for d in od]
+        for blas in (None, _openblas()):
+            M.lib().or_enable_blas(blas or b"", 1)
+            mf = M.factorize(mh, 1)
+            if M is O:
+                assert H.log_likelihood(df, y) == pytest.approx(O.log_likelihood(mf, y), rel=1e-12)
+            runs.append((M.score(mf, md, y), M.fisher_information(mf, md, cache=False)))
+        M.lib().or_enable_blas(b"", 1)
+    base = runs[0]
+    spread = _spread(runs[1:], base)
+    got = [_rel(dev_out[i], base[i]) for i in range(2)]
+    assert all(g <= max(2 * sp, 1e-9) for g, sp in zip(got, spread)), (got, spread)
+
+
+def test_mle_iteration_c1_reference_modes(H, reference_modes):
+    """Config C1 end to end (build from the same SketchPlan bytes + pipeline)
+    with the device in all reference-faithful modes against the reference
+    itself (oracle/_ref). Stated tolerances: loglik 1e-10; score and Fisher
+    within 2x the reference's own spread across dgemm summation orders and
+    the restated oracle (see the test above)."""
+    from oracle import pyref as R
+
+    n, tau, k, x, oo, K, y = _c1_setup()
+    do = H.MaternOracle(x, 3, 1.0, 0.2, 1e-4, False)
+    ll1, s1, f1, t = H.mle_iteration(do, tau, k, 0, y)
+    runs = []
+    for M in ([R] if R.available() else []) + [O]:
+        for blas in (None, _openblas()):
+            M.lib().or_enable_blas(blas or b"", 1)
+            runs.append(M.mle_iteration(M.CovOracle.matern(x, 3, 1.0, 0.2, 1e-4, False), tau, k, 0, y, 2,
+                                        cache=False)[:3])
+        M.lib().or_enable_blas(b"", 1)
+    base = runs[0]
+    assert ll1 == pytest.approx(base[0], rel=1e-10)
+    spread = _spread(runs[1:], base)
+    got = [_rel(v, base[i]) for i, v in enumerate((ll1, s1, f1))]
+    assert all(g <= max(2 * sp, 1e-9) for g, sp in zip(got[1:], spread[1:])), (got, spread)
