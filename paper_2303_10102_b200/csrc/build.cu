@@ -207,6 +207,59 @@ __global__ void k_place_completion(const WorkItem* items, const int* cj, const i
     }
 }
 
+/// Completion basis of one long deficient node by CholeskyQR: the projected
+/// canonical candidates W (left-child rows, c_j columns) have Gram matrix
+/// G = W^T W = I - S_c S_c^T-like and every accepted column has norm >= 0.5
+/// after projection, so cond(W) <= 2 and W R^-1 (R = chol(G)^T, positive
+/// diagonal) is orthonormal to O(eps cond^2). R_tt is exactly the
+/// sequential loop's projected norm (sketch.cpp:60-74), so R_tt < 0.5 sends
+/// the node back to that loop. One warp per node: writes R^-1 (upper,
+/// cmax x cmax per even segment, zero-padded), diag(R) for the placement
+/// and a fail flag.
+__global__ void k_completion_cholqr(const int* cj, int cmax, const double* Gw, double* Rinv, double* Rdiag, int* fail) {
+    const int j = blockIdx.x, lane = threadIdx.x;
+    const int c = cj[j];
+    const double* G = Gw + i64(2 * j) * cmax * cmax;
+    double* Ri = Rinv + i64(2 * j) * cmax * cmax;
+    double* Rd = Rdiag + i64(j) * cmax * cmax;
+    __shared__ double L[64 * 65];
+    for (int e = lane; e < cmax * cmax; e += 32) {
+        Ri[e] = 0.0;
+        Rinv[i64(2 * j + 1) * cmax * cmax + e] = 0.0;
+        Rd[e] = 0.0;
+    }
+    if (c <= 0) {
+        if (lane == 0) fail[j] = 0;
+        return;
+    }
+    for (int e = lane; e < c * c; e += 32) L[(e % c) * 65 + e / c] = G[(e % c) + i64(e / c) * cmax];
+    __syncwarp();
+    int bad = 0;
+    for (int t = 0; t < c; ++t) {  // right-looking Cholesky, lower L (row r, col t at L[r * 65 + t])
+        const double d = L[t * 65 + t];
+        const double ltt = d > 0.0 ? sqrt(d) : 0.0;
+        bad |= !(ltt >= 0.5);
+        __syncwarp();
+        for (int r = t + 1 + lane; r < c; r += 32) L[r * 65 + t] = ltt > 0.0 ? L[r * 65 + t] / ltt : 0.0;
+        __syncwarp();
+        if (lane == 0) L[t * 65 + t] = ltt;
+        for (int r = t + 1 + lane; r < c; r += 32)
+            for (int q = t + 1; q <= r; ++q) L[r * 65 + q] -= L[r * 65 + t] * L[q * 65 + t];
+        __syncwarp();
+    }
+    if (lane == 0) fail[j] = bad;
+    if (bad) return;
+    // R = L^T (upper); R^-1 column by column (lane = column), back substitution
+    for (int col = lane; col < c; col += 32) {
+        for (int i = col; i >= 0; --i) {
+            double s = (i == col) ? 1.0 : 0.0;
+            for (int q = i + 1; q <= col; ++q) s -= L[q * 65 + i] * Ri[q + i64(col) * cmax];
+            Ri[i + i64(col) * cmax] = s / L[i * 65 + i];
+        }
+        Rd[col + i64(col) * cmax] = L[col * 65 + col];
+    }
+}
+
 /// q2 width (sketch.cpp:214-221).
 __global__ void k_w2_nodes(int nodes, const int* bounds, int k, int kp, const int* qmap, const double* R2,
                            const double* presc, int* w2out) {
@@ -514,7 +567,13 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
         count_launch();
     } else {
         std::vector<BatchedQR::Block> mb;
-        for (int j = 0; j < nodes; ++j) mb.push_back({M.get() + i64(j) * w * w, w, w});
+        for (int j = 0; j < nodes; ++j) {  // k_trunc_rank stops at rtol |r00| or wmin
+            QrStop st;
+            st.rel = rtol;
+            st.max_steps = std::max(wmin[static_cast<size_t>(j)], 1);
+            st.active = true;
+            mb.push_back({M.get() + i64(j) * w * w, w, w, st});
+        }
         mq = std::make_unique<BatchedQR>(mb, w, true);
         k_trunc_rank<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, w, mq->R(), dwmin.get(), rtol, dr.get());
         HG_LAUNCH();
@@ -618,41 +677,31 @@ void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double*
     k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dcj.get(), cmax, W.get(), n);
     HG_LAUNCH();
     ctx.launches += 4;
-    std::vector<BatchedQR::Block> blocks;
+    if (cmax > 64) throw std::length_error("complete_deficient: more than 64 completion columns");
     std::vector<int> rmap(static_cast<size_t>(nodes), -1);
-    for (int j : big) {
-        rmap[static_cast<size_t>(j)] = int(blocks.size());
-        blocks.push_back({W.get() + hb[static_cast<size_t>(2 * j)], n,
-                          hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)]});
-    }
-    BatchedQR qr(blocks, cmax, false);
-    std::vector<double> Rh(blocks.size() * static_cast<size_t>(cmax) * cmax);
-    HG_CUDA(cudaMemcpyAsync(Rh.data(), qr.R(), Rh.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    sync();
+    for (int j : big) rmap[static_cast<size_t>(j)] = j;
+    DVec Gw(static_cast<size_t>(2 * nodes) * cmax * cmax), Rinv(static_cast<size_t>(2 * nodes) * cmax * cmax),
+        Rd(static_cast<size_t>(nodes) * cmax * cmax);
+    DBuf<int> dfail(static_cast<size_t>(nodes));
+    seg_tn(pc, W.get(), n, cmax, W.get(), n, cmax, Gw.get(), i64(cmax) * cmax, cmax);
+    k_completion_cholqr<<<nodes, 32, 0, ctx.stream>>>(dcj.get(), cmax, Gw.get(), Rinv.get(), Rd.get(), dfail.get());
+    HG_LAUNCH();
+    count_launch();
+    const std::vector<int> failh = dfail.download();
     std::vector<int> fallback_nr(static_cast<size_t>(nodes), k);
     bool any_fallback = false;
-    for (int j : big) {
-        const double* R = Rh.data() + static_cast<size_t>(rmap[static_cast<size_t>(j)]) * cmax * cmax;
-        for (int t = 0; t < cj[static_cast<size_t>(j)]; ++t)
-            if (std::abs(R[t + t * cmax]) < 0.5) {
-                rmap[static_cast<size_t>(j)] = -1;
-                fallback_nr[static_cast<size_t>(j)] = nrh[static_cast<size_t>(j)];
-                any_fallback = true;
-                break;
-            }
-    }
+    for (int j : big)
+        if (failh[static_cast<size_t>(j)]) {
+            rmap[static_cast<size_t>(j)] = -1;
+            fallback_nr[static_cast<size_t>(j)] = nrh[static_cast<size_t>(j)];
+            any_fallback = true;
+        }
     DVec Qw(static_cast<size_t>(n) * cmax);
-    std::vector<double*> qo;
-    std::vector<i64> ql;
-    for (int j : big) {
-        qo.push_back(Qw.get() + hb[static_cast<size_t>(2 * j)]);
-        ql.push_back(n);
-    }
-    qr.form_q(cmax, nullptr, 0, 0, qo, ql);
+    seg_nn(pc, W.get(), n, cmax, Rinv.get(), i64(cmax) * cmax, cmax, TMap::same(), Qw.get(), n, cmax, 1.0, 0.0);
     DBuf<int> drmap;
     drmap.upload(rmap);
     const TileList& tl = pc.tiles(256);
-    k_place_completion<<<tl.count, 256, 0, ctx.stream>>>(tl.items.get(), dcj.get(), nr.get(), qr.R(), cmax,
+    k_place_completion<<<tl.count, 256, 0, ctx.stream>>>(tl.items.get(), dcj.get(), nr.get(), Rd.get(), cmax,
                                                          drmap.get(), Qw.get(), n, S, n);
     HG_LAUNCH();
     count_launch();
@@ -886,7 +935,13 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             const int m = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
             if (m == k) continue;
             qmap[static_cast<size_t>(j)] = int(blocks.size());
-            blocks.push_back({Y.get() + hb[static_cast<size_t>(2 * j)], n, m});
+            // only R's diagonal up to the numeric rank (64 eps |r00|, k_range_post)
+            // and Q's first nr columns are read: stop the pivoted QR there
+            QrStop st;
+            st.rel = 64 * DBL_EPSILON;
+            st.max_steps = k;
+            st.active = true;
+            blocks.push_back({Y.get() + hb[static_cast<size_t>(2 * j)], n, m, st});
         }
         DBuf<int> dqmap;
         dqmap.upload(qmap);
@@ -896,23 +951,28 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         S.zero();
         {
             std::unique_ptr<BatchedQR> qr;
-            if (!blocks.empty()) {
-                qr = std::make_unique<BatchedQR>(blocks, k, true);
-                std::vector<double*> qo;
-                std::vector<i64> ql;
-                for (int j = 0; j < nodes; ++j)
-                    if (qmap[static_cast<size_t>(j)] >= 0) {
-                        qo.push_back(S.get() + hb[static_cast<size_t>(2 * j)]);
-                        ql.push_back(n);
-                    }
-                qr->form_q(k, nullptr, 0, 0, qo, ql);
-            }
+            if (!blocks.empty()) qr = std::make_unique<BatchedQR>(blocks, k, true);
             DVec dummyR(1);
             DBuf<int> dummyP(1);
             k_range_post<<<nodes, 128, 0, ctx.stream>>>(k, dqmap.get(), qr ? qr->R() : dummyR.get(),
                                                         qr ? qr->perm() : dummyP.get(), Rn.get(), perm.get(),
                                                         sign.get(), nr.get());
             HG_LAUNCH();
+            if (qr) {
+                // Q columns past a node's numeric rank are replaced by the
+                // completion below: form only the widest numeric rank
+                const std::vector<int> nrh = nr.download();
+                int nrmax = 1;
+                std::vector<double*> qo;
+                std::vector<i64> ql;
+                for (int j = 0; j < nodes; ++j)
+                    if (qmap[static_cast<size_t>(j)] >= 0) {
+                        nrmax = std::max(nrmax, nrh[static_cast<size_t>(j)]);
+                        qo.push_back(S.get() + hb[static_cast<size_t>(2 * j)]);
+                        ql.push_back(n);
+                    }
+                qr->form_q(nrmax, nullptr, 0, 0, qo, ql);
+            }
             const TileList& tl256 = pc.tiles(256);
             k_q_sign_rows<<<tl256.count, 256, 0, ctx.stream>>>(tl256.items.get(), pc.dbounds(), k, dqmap.get(),
                                                                sign.get(), S.get(), n);
@@ -949,8 +1009,18 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             }
             std::vector<BatchedQR::Block> b2;
             for (int j = 0; j < nodes; ++j)
-                if (qmap[static_cast<size_t>(j)] >= 0)
-                    b2.push_back({resid.get() + hb[static_cast<size_t>(2 * j)], n, hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)]});
+                if (qmap[static_cast<size_t>(j)] >= 0) {
+                    // k_w2_nodes reads the diagonal up to the first entry at the
+                    // floor max(1e-10 |r00|, 1e-12 presc_j) or the cap: stop there
+                    const int m = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
+                    QrStop st;
+                    st.rel = 1e-10;
+                    st.abs_scale = 1e-12;
+                    st.abs_ptr = presc.get() + j;
+                    st.max_steps = std::max(std::min(kp, m - k), 1);
+                    st.active = true;
+                    b2.push_back({resid.get() + hb[static_cast<size_t>(2 * j)], n, m, st});
+                }
             std::unique_ptr<BatchedQR> qr2;
             if (!b2.empty()) {
                 qr2 = std::make_unique<BatchedQR>(b2, kp, true);

@@ -1,5 +1,6 @@
 // Batched (column-pivoted) Householder QR and Q formation — see qr.cuh.
 #include <cfloat>
+#include <cstdlib>
 
 #include "prof.cuh"
 #include "qr.cuh"
@@ -60,6 +61,9 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
         __syncthreads();
     }
     const double downdate_thr = sqrt(DBL_EPSILON);
+    int steps = nsz;
+    double beta0 = 0.0, stop_abs = -1.0;
+    if (PIVOT && d.stop.active && d.stop.abs_ptr) stop_abs = d.stop.abs_scale * *d.stop.abs_ptr;
     for (int k = 0; k < nsz; ++k) {
         if (PIVOT) {
             if (warp == 0) {  // first index of the largest norm (Eigen's maxCoeff), warp argmax
@@ -120,6 +124,16 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
             if (!zero) W[k + k * ldw] = beta;
             d.tau[k] = tau;
         }
+        if (PIVOT && d.stop.active) {  // uniform: every thread holds the same beta
+            if (k == 0) beta0 = fabs(beta);
+            if (fabs(beta) <= fmax(d.stop.rel * beta0, stop_abs) || k + 1 >= d.stop.max_steps) {
+                for (int i = k + 1 + tid; i < rows; i += blockDim.x) W[i + k * ldw] = zero ? 0.0 : W[i + k * ldw] / div;
+                for (int t = k + 1 + tid; t < nsz; t += blockDim.x) d.tau[t] = 0.0;
+                steps = k + 1;
+                __syncthreads();
+                break;
+            }
+        }
         for (int i = k + 1 + tid; i < rows; i += blockDim.x) W[i + k * ldw] = zero ? 0.0 : W[i + k * ldw] / div;
         __syncthreads();
         for (int j = k + 1 + warp; j < w; j += nwarps) {
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
         }
     if (PIVOT && tid == 0) {
         for (int j = 0; j < w; ++j) d.perm[j] = j;
-        for (int k = 0; k < nsz; ++k) {
+        for (int k = 0; k < steps; ++k) {
             const int t = d.perm[k];
             d.perm[k] = d.perm[trans[k]];
             d.perm[trans[k]] = t;
@@ -305,7 +319,12 @@ namespace hg {
 
 namespace {
 int chunk_rows(int w) {
-    int fit = int(QR_SMEM / (sizeof(double) * static_cast<size_t>(std::max(w, 1))));
+    static const size_t budget = [] {  // HG_QR_CHUNK_KB: TSQR chunk budget (tuning knob)
+        const char* e = std::getenv("HG_QR_CHUNK_KB");
+        const long v = e ? std::atol(e) : 0;
+        return v > 0 ? static_cast<size_t>(v) * 1024 : QR_SMEM;
+    }();
+    int fit = int(std::min(budget, QR_SMEM) / (sizeof(double) * static_cast<size_t>(std::max(w, 1))));
     fit = (fit / 32) * 32;
     return std::max(fit, 4 * w);
 }
@@ -387,7 +406,8 @@ BatchedQR::BatchedQR(const std::vector<Block>& blocks, int w, bool pivot) : w_(w
         top_node_[static_cast<size_t>(b)] = int(i);
         top_level_[static_cast<size_t>(b)] = L;
         descs.push_back(QrDesc{cur[i].A, cur[i].lda, cur[i].rows, top_tau_.get() + static_cast<size_t>(b) * w,
-                               R_.get() + static_cast<size_t>(b) * w * w, w, perm_.get() + static_cast<size_t>(b) * w});
+                               R_.get() + static_cast<size_t>(b) * w * w, w, perm_.get() + static_cast<size_t>(b) * w,
+                               pivot ? blocks[static_cast<size_t>(b)].stop : QrStop{}});
     }
     batched_qr(descs, w, pivot);
 }

@@ -10,6 +10,19 @@
 
 namespace hg {
 
+/// Early termination of a pivoted QR whose caller only reads the leading
+/// diagonal up to the first |R(s,s)| <= max(rel |R(0,0)|, abs_scale *abs_ptr)
+/// (or up to max_steps): the factorization stops after that step; later
+/// taus are 0 (identity reflectors), later R rows and pivots are unspecified.
+/// The columns the caller reads are bitwise those of the full factorization.
+struct QrStop {
+    double rel = 0.0;
+    double abs_scale = 0.0;
+    const double* abs_ptr = nullptr;  // device scalar, may be null
+    int max_steps = 1 << 30;
+    bool active = false;
+};
+
 struct QrDesc {
     double* A;    // block (rows x w), ld lda; overwritten by R (upper) + essentials
     i64 lda;
@@ -18,6 +31,7 @@ struct QrDesc {
     double* R;    // w x w (ld ldr), may be null
     int ldr;
     int* perm;    // w (pivoted only)
+    QrStop stop = {};
 };
 
 /// QR of every block (all blocks have w columns). Pivoting follows Eigen:
@@ -53,6 +67,7 @@ public:
         double* A;
         i64 lda;
         int rows;
+        QrStop stop = {};  // pivoted top-level QR only
     };
     BatchedQR(const std::vector<Block>& blocks, int w, bool pivot);
     int w() const { return w_; }
