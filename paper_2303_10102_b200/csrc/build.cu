@@ -7,6 +7,7 @@
 // recompression) runs one CTA per node.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <random>
@@ -381,6 +382,25 @@ __global__ void k_tins(int W, int rmax, const int* r, const double* RM, const in
     }
 }
 
+/// Direct truncation (Z P = Q_Z R_Z pivoted, stopped at rank r):
+/// TinL[perm[i], a] = R_Z[a, i] (a < r), TinR = [I_r; 0] (w x rmax each).
+__global__ void k_tins_direct(int W, int rmax, const int* r, const double* RZ, const int* permZ, double* Tin) {
+    const int j = blockIdx.x;
+    const int rj = r[j];
+    double* TL = Tin + i64(2 * j) * W * rmax;
+    double* TR = Tin + i64(2 * j + 1) * W * rmax;
+    const double* R = RZ + i64(j) * W * W;
+    for (int e = threadIdx.x; e < W * rmax; e += blockDim.x) {
+        TL[e] = 0.0;
+        TR[e] = (e % W == e / W && e / W < rj) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < W * rmax; e += blockDim.x) {
+        const int i = e % W, a = e / W;
+        if (a < rj) TL[permZ[j * W + i] + i64(a) * W] = R[a + i64(i) * W];
+    }
+}
+
 std::vector<int> dl_int(const DBuf<int>& d) { return d.download(); }
 
 __global__ void k_transpose_blocks(int w, const double* A, double* B) {
@@ -535,24 +555,76 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
     panel_axpby(n, k, 1.0, P + i64(k) * n, n, 0.0, Z.get(), n);
     seg_nn(pc, P, n, k, Om, i64(k) * k, k, TMap::parent(0, 0), Z.get(), n, k, -1.0, 1.0);
     if (w > k) panel_axpby(n, w - k, 1.0, P + i64(2 * k) * n, n, 0.0, Z.get() + i64(k) * n, n);
-    std::vector<BatchedQR::Block> blocks;
-    for (int j = 0; j < nodes; ++j)
-        blocks.push_back({Z.get() + hb[static_cast<size_t>(2 * j + 1)], n,
-                          hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)]});
-    BatchedQR qz(blocks, w, false);
-    DVec M(static_cast<size_t>(nodes) * w * w);
-    k_transpose_blocks<<<nodes, 256, 0, ctx.stream>>>(w, qz.R(), M.get());
-    HG_LAUNCH();
-    count_launch();
     std::vector<int> wmin(static_cast<size_t>(nodes));
+    int zrows = 0;
     for (int j = 0; j < nodes; ++j) {
         const int cl = hb[static_cast<size_t>(2 * j + 1)] - hb[static_cast<size_t>(2 * j)];
         const int cr = hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)];
         wmin[static_cast<size_t>(j)] = std::min({cl, cr, w});
+        zrows = std::max(zrows, cr);
     }
+    const bool svd = ctx.compression == HG_COMPRESS_JACOBI_SVD;
+    // Blocks one CTA factors directly: a column-pivoted QR of Z itself,
+    // stopped at the truncation rank, is the rank-revealing factorization
+    // (Z P = Q_Z R_Z; block = [Q|q2] P R_Z[:r]^T Q_Z[:, :r]^T), ~r/w of the
+    // work of a full QR of Z plus the pivoted QR of its core.
+    static const bool direct_ok = [] {  // HG_Z_DIRECT=0: always the two-stage path (A/B knob)
+        const char* e = std::getenv("HG_Z_DIRECT");
+        return !(e && e[0] == '0');
+    }();
+    const bool direct = direct_ok && !svd && zrows <= qr_chunk_rows(w);
+    std::vector<BatchedQR::Block> blocks;
+    for (int j = 0; j < nodes; ++j) {
+        QrStop st;
+        if (direct) {
+            st.rel = rtol;
+            st.max_steps = std::max(wmin[static_cast<size_t>(j)], 1);
+            st.active = true;
+        }
+        blocks.push_back({Z.get() + hb[static_cast<size_t>(2 * j + 1)], n,
+                          hb[static_cast<size_t>(2 * j + 2)] - hb[static_cast<size_t>(2 * j + 1)], st});
+    }
+    BatchedQR qz(blocks, w, direct);
     DBuf<int> dwmin, dr(static_cast<size_t>(nodes));
     dwmin.upload(wmin);
-    const bool svd = ctx.compression == HG_COMPRESS_JACOBI_SVD;
+    if (direct) {
+        k_trunc_rank<<<cdiv(nodes, 128), 128, 0, ctx.stream>>>(nodes, w, qz.R(), dwmin.get(), rtol, dr.get());
+        HG_LAUNCH();
+        count_launch();
+        std::vector<int> r = dl_int(dr);
+        int rmax = 0;
+        for (int x : r) rmax = std::max(rmax, x);
+        auto Pn = rmax ? make_dvec(static_cast<size_t>(n) * static_cast<size_t>(rmax), true) : nullptr;
+        if (rmax) {
+            DVec Tin(static_cast<size_t>(2 * nodes) * w * rmax);
+            k_tins_direct<<<nodes, 256, 0, ctx.stream>>>(w, rmax, dr.get(), qz.R(), qz.perm(), Tin.get());
+            HG_LAUNCH();
+            count_launch();
+            // left' = [Q | q2] P R_Z[:r]^T on left-child rows
+            seg_nn(pc, P + i64(k) * n, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n,
+                   rmax, 1.0, 0.0);
+            // right' = Q_Z[:, :r] on right-child rows
+            std::vector<double*> out;
+            std::vector<i64> ld;
+            for (int j = 0; j < nodes; ++j) {
+                out.push_back(Pn->get() + hb[static_cast<size_t>(2 * j + 1)]);
+                ld.push_back(n);
+            }
+            qz.form_q(rmax, Tin.get() + i64(w) * rmax, i64(2) * w * rmax, w, out, ld);
+        }
+        D.R[static_cast<size_t>(l - 1)] = rmax;
+        D.U[static_cast<size_t>(l - 1)] = Pn;
+        D.V[static_cast<size_t>(l - 1)] = Pn;
+        for (int j = 0; j < nodes; ++j) {
+            D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+            D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = r[static_cast<size_t>(j)];
+        }
+        return;
+    }
+    DVec M(static_cast<size_t>(nodes) * w * w);
+    k_transpose_blocks<<<nodes, 256, 0, ctx.stream>>>(w, qz.R(), M.get());
+    HG_LAUNCH();
+    count_launch();
     std::unique_ptr<BatchedQR> mq;
     std::unique_ptr<DVec> US, VS;
     if (svd) {

@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int
     extern __shared__ double sm[];
     const QfDesc d = descs[blockIdx.x];
     const int rows = d.rows;
-    const int nref = min(w, rows);
+    // identity Tin: H_i (i >= c) leaves e_c unchanged (only the first qcols reflectors act)
+    const int nref = d.Tin ? min(w, rows) : min(min(w, rows), qcols);
     const bool use_smem = i64(rows) * qcols <= smem_elems;
     double* Q = use_smem ? sm : d.Q;
     const i64 ldq = use_smem ? rows : d.ldq;
@@ -329,6 +330,8 @@ int chunk_rows(int w) {
     return std::max(fit, 4 * w);
 }
 }  // namespace
+
+int qr_chunk_rows(int w) { return chunk_rows(w); }
 
 BatchedQR::BatchedQR(const std::vector<Block>& blocks, int w, bool pivot) : w_(w), pivot_(pivot), blocks_(blocks) {
     const int CH = chunk_rows(w);

@@ -61,6 +61,10 @@ namespace hg {
 /// final per-block matrix gets the (optionally pivoted) QR. Equivalent to a
 /// direct (pivoted) Householder QR of each block: the pivot choice reads the
 /// same column norms, and Q is recovered by applying the tree top-down.
+/// Blocks of at most this many rows (w columns) are factored by one CTA
+/// directly; taller ones go through the TSQR tree.
+int qr_chunk_rows(int w);
+
 class BatchedQR {
 public:
     struct Block {

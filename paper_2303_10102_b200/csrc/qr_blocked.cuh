@@ -71,16 +71,18 @@ __device__ __forceinline__ void qb_build_t(const QbSmem& S, int ld, int nr, int 
         if (lane == 0) S.G[a + QB_NB * b] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < QB_NB * QB_NB; ++i) S.T[i] = 0.0;
+    if (warp == 0) {  // column i of T depends on columns < i; its rows a < i are independent (lane a)
+        for (int i = lane; i < QB_NB * QB_NB; i += 32) S.T[i] = 0.0;
+        __syncwarp();
         for (int i = 0; i < jb; ++i) {
             const double ti = S.tau[i];
-            S.T[i + QB_NB * i] = ti;
-            for (int a = 0; a < i; ++a) {
-                double s = 0.0;
-                for (int b = a; b < i; ++b) s += S.T[a + QB_NB * b] * S.G[b + QB_NB * i];
-                S.T[a + QB_NB * i] = -ti * s;
-            }
+            double s = 0.0;
+            if (lane < i)
+                for (int b = lane; b < i; ++b) s += S.T[lane + QB_NB * b] * S.G[b + QB_NB * i];
+            __syncwarp();
+            if (lane < i) S.T[lane + QB_NB * i] = -ti * s;
+            if (lane == 0) S.T[i + QB_NB * i] = ti;
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -300,7 +302,9 @@ __global__ void __launch_bounds__(QB_THREADS, 3) k_form_q_blocked(const QfDesc* 
     const int rows = d.rows, ld = qb_ld(rows);
     const QbSmem S = qb_layout(sm, rows, qcols_all);
     const int tid = threadIdx.x;
-    const int nref = min(w, rows);
+    // identity Tin: H_i (i >= c) leaves e_c unchanged, so columns < cc0 + qcols
+    // only see the first cc0 + qcols reflectors
+    const int nref = d.Tin ? min(w, rows) : min(min(w, rows), cc0 + qcols);
     double* Q = d.Q + i64(cc0) * d.ldq;
     for (int c = 0; c < qcols; ++c)
         for (int i = tid; i < rows; i += blockDim.x) {
