@@ -141,6 +141,16 @@ struct LoadUpdA {
         while (kt >= L->ktoff[l + 1]) ++l;
         const int kb = (kt - L->ktoff[l]) * BK, R = L->R[l];
         const double* base = L->Q[l] + row0;
+        if (tile::pairs_aligned(base, n)) {  // row pairs as 16-byte copies
+            const int m2 = 2 * (threadIdx.x & 31);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = (threadIdx.x >> 5) + 4 * q, kk = kb + k;
+                const int bytes = kk < R ? (m2 + 1 < rows ? 16 : (m2 < rows ? 8 : 0)) : 0;
+                tile::cp_async16(S + k * tile::LD_MC + m2, bytes ? base + m2 + kk * n : base, bytes);
+            }
+            return;
+        }
         const int m = threadIdx.x & 63;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -190,7 +200,25 @@ struct LoadUpdAPacked {
     int row0, rows;
     i64 n;
     __device__ __forceinline__ void issue(double* S, int kt) const {
-        const int m = threadIdx.x & 63, ktot = L->coff[L->nl];
+        const int ktot = L->coff[L->nl];
+        if (((row0 | n) & 1) == 0) {  // row pairs as 16-byte copies (panels are 16-byte aligned)
+            const int m2 = 2 * (threadIdx.x & 31);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = (threadIdx.x >> 5) + 4 * q, cc = kt * BK + k;
+                const int bytes = cc < ktot ? (m2 + 1 < rows ? 16 : (m2 < rows ? 8 : 0)) : 0;
+                const int e = cc < ktot ? tab[cc] : 0, l = e >> 16, j = e & 0xffff;
+                const double* src = L->Q[l] + row0 + m2 + i64(j) * n;
+                if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    tile::cp_async16(S + k * tile::LD_MC + m2, bytes ? src : L->Q[0], bytes);
+                } else {  // a panel view at an odd offset
+                    tile::cp_async8(S + k * tile::LD_MC + m2, bytes >= 8 ? src : L->Q[0], bytes >= 8);
+                    tile::cp_async8(S + k * tile::LD_MC + m2 + 1, bytes == 16 ? src + 1 : L->Q[0], bytes == 16);
+                }
+            }
+            return;
+        }
+        const int m = threadIdx.x & 63;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int k = (threadIdx.x >> 6) + 2 * q, cc = kt * BK + k;

@@ -78,6 +78,18 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
     const int bytes = valid ? 8 : 0;  // 0 => zero-fill
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+/// 16-byte copy that bypasses L1 (streamed operands); `bytes` in {0, 8, 16}
+/// valid source bytes, the rest of the 16 zero-filled. Both addresses must be
+/// 16-byte aligned.
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+/// An operand whose column starts are all 16-byte aligned (pairs of
+/// consecutive elements of a column can move as one 16-byte copy).
+__device__ __forceinline__ bool pairs_aligned(const double* base, long long ld) {
+    return (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (ld & 1) == 0;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -199,6 +211,18 @@ struct LoadKCT {
     long long ld;
     int kmax, mmax;
     __device__ __forceinline__ void issue(double* S, int kt) const {
+        if (pairs_aligned(base, ld)) {  // k pairs as 16-byte copies (half the copy instructions)
+#pragma unroll
+            for (int q = 0; q < (R * BK / 2 + THREADS - 1) / THREADS; ++q) {
+                const int e = threadIdx.x + THREADS * q;
+                if (R * BK / 2 % THREADS != 0 && e >= R * BK / 2) break;
+                const int k2 = (e & (BK / 2 - 1)) * 2, m = e / (BK / 2);
+                const int kk = kt * BK + k2;
+                const int bytes = m < mmax ? (kk + 1 < kmax ? 16 : (kk < kmax ? 8 : 0)) : 0;
+                cp_async16(S + m * LD_KC + k2, bytes ? base + kk + m * ld : base, bytes);
+            }
+            return;
+        }
         const int k = threadIdx.x & 15;
         const int kk = kt * BK + k;
 #pragma unroll
@@ -221,6 +245,18 @@ struct LoadMCT {
     long long ld;
     int mmax, kmax;
     __device__ __forceinline__ void issue(double* S, int kt) const {
+        if (pairs_aligned(base, ld)) {  // m pairs as 16-byte copies
+#pragma unroll
+            for (int q = 0; q < (R * BK / 2 + THREADS - 1) / THREADS; ++q) {
+                const int e = threadIdx.x + THREADS * q;
+                if (R * BK / 2 % THREADS != 0 && e >= R * BK / 2) break;
+                const int m2 = (e % (R / 2)) * 2, k = e / (R / 2);
+                const int kk = kt * BK + k;
+                const int bytes = kk < kmax ? (m2 + 1 < mmax ? 16 : (m2 < mmax ? 8 : 0)) : 0;
+                cp_async16(S + k * (R + 4) + m2, bytes ? base + m2 + kk * ld : base, bytes);
+            }
+            return;
+        }
 #pragma unroll
         for (int q = 0; q < R / 8; ++q) {
             const int e = threadIdx.x + THREADS * q;
