@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
     if (r0 >= m) return;
     const int n0 = blockIdx.y * TBN;
     const double* Lb = g.L + i64(b) * g.lstride;
-    tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
+    tile::LoadKCT<TBN, false> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
     typename tile::Shape<BM, TBN>::Acc acc;
     acc.zero();
     typename tile::Shape<BM, TBN>::Acc yv;
@@ -240,10 +240,10 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm(LeafMmArgs g) {
             if (n < g.w && mi < m) y = g.Y[i64(lo + mi) + i64(n) * g.ldy];
         });
     if (!TRANS) {
-        tile::LoadMCT<BM> la{Lb + r0, g.ldl, m - r0, m};
+        tile::LoadMCT<BM, false> la{Lb + r0, g.ldl, m - r0, m};
         tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
     } else {
-        tile::LoadKCT<BM> la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
+        tile::LoadKCT<BM, false> la{Lb + i64(r0) * g.ldl, g.ldl, m, m - r0};
         tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
     }
     tile::for_each_slot2<BM, TBN>(acc, yv, [&](double v, double y, int mi0, int ni) {
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, const dou
         const int t1 = min(ntiles, int(blockIdx.y + 1) * tiles_per);
         for (int tn = int(blockIdx.y) * tiles_per; tn < t1; ++tn) {
             const int n0 = tn * TBN;
-            tile::LoadKCT<TBN> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
-            tile::LoadMCT<BM> la{Lb + r0, g.ldl, m - r0, m};
+            tile::LoadKCT<TBN, false> lb{g.X + lo + i64(n0) * g.ldx, g.ldx, m, g.w - n0};
+            tile::LoadMCT<BM, false> la{Lb + r0, g.ldl, m - r0, m};
             typename tile::Shape<BM, TBN>::Acc acc;
             acc.zero();
             tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);

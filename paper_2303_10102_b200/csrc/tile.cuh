@@ -203,7 +203,7 @@ constexpr int SMEM_BYTES = smem_bytes(STAGES);
 
 /// Column-major operand whose rows are the reduction index k (k-contiguous):
 /// element (k, m) at base[k + m * ld], valid for k < kmax, m < mmax.
-template <int R>
+template <int R, bool VEC = true>
 struct LoadKCT {
     static constexpr bool KC = true;
     static constexpr int ROWS = R;
@@ -211,7 +211,7 @@ struct LoadKCT {
     long long ld;
     int kmax, mmax;
     __device__ __forceinline__ void issue(double* S, int kt) const {
-        if (pairs_aligned(base, ld)) {  // k pairs as 16-byte copies (half the copy instructions)
+        if (VEC && pairs_aligned(base, ld)) {  // k pairs as 16-byte copies (half the copy instructions)
 #pragma unroll
             for (int q = 0; q < (R * BK / 2 + THREADS - 1) / THREADS; ++q) {
                 const int e = threadIdx.x + THREADS * q;
@@ -237,7 +237,7 @@ using LoadKC = LoadKCT<64>;
 
 /// Column-major operand whose rows are the output index m (m-contiguous):
 /// element (m, k) at base[m + k * ld], valid for m < mmax, k < kmax.
-template <int R>
+template <int R, bool VEC = true>
 struct LoadMCT {
     static constexpr bool KC = false;
     static constexpr int ROWS = R;
@@ -245,7 +245,7 @@ struct LoadMCT {
     long long ld;
     int mmax, kmax;
     __device__ __forceinline__ void issue(double* S, int kt) const {
-        if (pairs_aligned(base, ld)) {  // m pairs as 16-byte copies
+        if (VEC && pairs_aligned(base, ld)) {  // m pairs as 16-byte copies
 #pragma unroll
             for (int q = 0; q < (R * BK / 2 + THREADS - 1) / THREADS; ++q) {
                 const int e = threadIdx.x + THREADS * q;
