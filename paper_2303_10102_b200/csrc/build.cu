@@ -1052,9 +1052,34 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             ctx.launches += 2;
             complete_deficient(pc, k, nr, S.get(), n);
         }
-        // Pass 2: Z = K S - H S (sketch.cpp:177-183).
-        DVec Z(static_cast<size_t>(n) * k);
-        peel(o, -1, out.h, l - 1, S.get(), k, Z.get(), 1);
+        // Pass 2, Z = K S - H S (sketch.cpp:177-183), and the value half of
+        // every differentiated pass, K ds_q - H ds_q (:270-271), in ONE peel
+        // over [S | ds_0 | .. | ds_{p-1}]: the coarser levels' panels are
+        // streamed once instead of 1 + p times. ds_q = S Omega_q needs only
+        // S and dY (diff_qr, :245-268), not Z.
+        std::vector<DVecP> oms(static_cast<size_t>(p));
+        std::vector<std::vector<int>> rws(static_cast<size_t>(p));
+        DVec SX(static_cast<size_t>(n) * k * (1 + p)), ZX(static_cast<size_t>(n) * k * (1 + p));
+        panel_axpby(n, k, 1.0, S.get(), n, 0.0, SX.get(), n);
+        for (int q = 0; q < p; ++q) {
+            DVec G(static_cast<size_t>(2 * nodes) * k * k);
+            DVecP OmP = make_dvec(static_cast<size_t>(nodes) * k * k, false);
+            omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)] = OmP;
+            DBuf<int> rw(static_cast<size_t>(nodes)), ill(static_cast<size_t>(nodes));
+            const double* dYq = dY.get() + i64(q) * k * n;
+            seg_tn(pc, S.get(), n, k, dYq, n, k, G.get(), i64(k) * k, k);
+            k_diffqr<<<nodes, 64, 0, ctx.stream>>>(k, G.get(), Rn.get(), perm.get(), nr.get(), dqmap.get(),
+                                                   OmP->get(), rw.get(), ill.get());
+            HG_LAUNCH();
+            ++ctx.launches;
+            seg_nn(pc, S.get(), n, k, OmP->get(), i64(k) * k, k, TMap::parent(0, 0), SX.get() + i64(1 + q) * k * n, n,
+                   k, 1.0, 0.0);
+            rws[static_cast<size_t>(q)] = rw.download();
+            std::vector<int> ic = ill.download();
+            for (int x : ic) out.warnings += x;
+        }
+        peel(o, -1, out.h, l - 1, SX.get(), k * (1 + p), ZX.get(), 1);
+        const double* Z = ZX.get();
 
         // q2 residual bases (sketch.cpp:194-233).
         std::vector<int> w2(static_cast<size_t>(nodes), 0);
@@ -1136,31 +1161,21 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             }
         }
 
-        // Differentiated passes (sketch.cpp:236-295) and the commit (:297-311).
-        std::vector<std::vector<int>> rws(static_cast<size_t>(p));
+        // Differentiated passes (sketch.cpp:236-295) and the commit (:297-311):
+        // dZ_q = K_q S - D_q S + (K ds_q - H ds_q), dZ2_q = K_q q2 - D_q q2,
+        // the D_q applies to [S | q2] in one peel.
         for (int q = 0; q < p; ++q) {
-            DVec G(static_cast<size_t>(2 * nodes) * k * k), ds(static_cast<size_t>(n) * k);
-            DVecP OmP = make_dvec(static_cast<size_t>(nodes) * k * k, false);
-            omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)] = OmP;
-            DVec& Om = *OmP;
-            DBuf<int> rw(static_cast<size_t>(nodes)), ill(static_cast<size_t>(nodes));
-            const double* dYq = dY.get() + i64(q) * k * n;
-            seg_tn(pc, S.get(), n, k, dYq, n, k, G.get(), i64(k) * k, k);
-            k_diffqr<<<nodes, 64, 0, ctx.stream>>>(k, G.get(), Rn.get(), perm.get(), nr.get(), dqmap.get(), Om.get(),
-                                                   rw.get(), ill.get());
-            HG_LAUNCH();
-            ++ctx.launches;
-            seg_nn(pc, S.get(), n, k, Om.get(), i64(k) * k, k, TMap::parent(0, 0), ds.get(), n, k, 1.0, 0.0);
-            // dZ = K_q S - D_q S + K ds - H ds
-            DVec dZ(static_cast<size_t>(n) * k), tmp(static_cast<size_t>(n) * k);
-            peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S.get(), k, dZ.get(), 1);
-            peel(o, -1, out.h, l - 1, ds.get(), k, tmp.get(), 1);
-            panel_axpby(n, k, 1.0, tmp.get(), n, 1.0, dZ.get(), n);
-            DVec dZ2;
+            const double* ds = SX.get() + i64(1 + q) * k * n;
+            const int wq = k + w2max;
+            DVec X2(static_cast<size_t>(n) * wq), O2(static_cast<size_t>(n) * wq);
+            panel_axpby(n, k, 1.0, S.get(), n, 0.0, X2.get(), n);
+            if (w2max > 0) panel_axpby(n, w2max, 1.0, S2.get(), n, 0.0, X2.get() + i64(k) * n, n);
+            peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, X2.get(), wq, O2.get(), 1);
+            double* dZ = O2.get();
+            panel_axpby(n, k, 1.0, ZX.get() + i64(1 + q) * k * n, n, 1.0, dZ, n);
+            double* dZ2 = O2.get() + i64(k) * n;
             if (w2max > 0) {
-                dZ2.alloc(static_cast<size_t>(n) * w2max);
-                peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, S2.get(), w2max, dZ2.get(), 1);
-                k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 1, dw2.get(), w2max, dZ2.get(), n);
+                k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 1, dw2.get(), w2max, dZ2, n);
                 HG_LAUNCH();
                 ++ctx.launches;
             }
@@ -1169,26 +1184,23 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             DHodlr& D = out.deriv[static_cast<size_t>(q)];
             D.set_level(l, Wd, true);
             double* Pd = D.Ul(l);
-            panel_parity_scale(pc, n, k, ds.get(), n, 1.0, 0.0, Pd, n, 0.0);
-            panel_parity_scale(pc, n, k, Z.get(), n, 0.0, 1.0, Pd, n, 1.0);
+            panel_parity_scale(pc, n, k, ds, n, 1.0, 0.0, Pd, n, 0.0);
+            panel_parity_scale(pc, n, k, Z, n, 0.0, 1.0, Pd, n, 1.0);
             panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, Pd + i64(k) * n, n, 0.0);
-            panel_parity_scale(pc, n, k, dZ.get(), n, 0.0, 1.0, Pd + i64(k) * n, n, 1.0);
+            panel_parity_scale(pc, n, k, dZ, n, 0.0, 1.0, Pd + i64(k) * n, n, 1.0);
             if (w2max > 0) {
                 panel_parity_scale(pc, n, w2max, S2.get(), n, 1.0, 0.0, Pd + i64(2 * k) * n, n, 0.0);
-                panel_parity_scale(pc, n, w2max, dZ2.get(), n, 0.0, 1.0, Pd + i64(2 * k) * n, n, 1.0);
+                panel_parity_scale(pc, n, w2max, dZ2, n, 0.0, 1.0, Pd + i64(2 * k) * n, n, 1.0);
             }
             for (int j = 0; j < nodes; ++j) {
                 D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
                 D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
             }
-            rws[static_cast<size_t>(q)] = rw.download();
-            std::vector<int> ic = ill.download();
-            for (int x : ic) out.warnings += x;
         }
         // Value level panel: q on left rows, t = Z on right rows.
         out.h.set_level(l, k, true);
         panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, out.h.Ul(l), n, 0.0);
-        panel_parity_scale(pc, n, k, Z.get(), n, 0.0, 1.0, out.h.Ul(l), n, 1.0);
+        panel_parity_scale(pc, n, k, Z, n, 0.0, 1.0, out.h.Ul(l), n, 1.0);
         for (int j = 0; j < nodes; ++j) {
             out.h.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;
             out.h.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;
