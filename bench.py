@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hodlr", choices=["hodlr", "reference"])
     ap.add_argument("--log2n", type=int, default=N_LOG2)
-    ap.add_argument("--cpu-sample-log2", type=int, default=13)
+    ap.add_argument("--cpu-sample-log2", type=int, default=14)
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="reference arm: cycle 2^(s-1), 2^s, 2^(s+1) while inside this many seconds")
     ap.add_argument("--traffic-json", default=os.path.join(ROOT, "profiles", "r2_traffic.json"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -192,10 +194,15 @@ def run_reference(args):
     W, K = args.warmup, args.steps
     sizes = [args.cpu_sample_log2 - 1, args.cpu_sample_log2, args.cpu_sample_log2 + 1]
     for i in range(max(min(W, 1), 0)):  # a CPU has no warm-up effect beyond page faults; one is enough
-        cpu_iteration(M, sizes[i % 3], cache=False)
+        cpu_iteration(M, sizes[0], cache=False)
     ns, ts, stages = [], [], {}
+    t_start = time.perf_counter()
     for i in range(K):
-        t, n_s, st = cpu_iteration(M, sizes[i % 3], cache=False)
+        # cycle the three sizes while the run is inside its time budget; past
+        # it, the remaining steps use the smallest size (every size is timed
+        # at least once: the fit needs all three)
+        s = sizes[i % 3] if (i < 3 or time.perf_counter() - t_start < args.ref_budget_s) else sizes[0]
+        t, n_s, st = cpu_iteration(M, s, cache=False)
         ns.append(n_s)
         ts.append(t)
         stages[n_s] = [float(v) for v in st]
@@ -419,7 +426,7 @@ def main():
         used_blas = enable_openblas(M)
         runs = {}
         for cache in (False, True):
-            pts = [cpu_iteration(M, args.cpu_sample_log2 + d, cache)[:2] for d in (-1, 0)]
+            pts = [cpu_iteration(M, args.cpu_sample_log2 + d, cache)[:2] for d in (-2, -1)]
             cc, slope = fit_nlog2n([p[1] for p in pts], [p[0] for p in pts])
             runs["cached" if cache else "as_coded"] = {"n_run": [p[1] for p in pts], "seconds": [p[0] for p in pts],
                                                        "extrapolated_s": cc * n * math.log2(n) ** 2}
