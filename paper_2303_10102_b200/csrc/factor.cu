@@ -440,6 +440,7 @@ struct CapSolveArgs {
     int top_odd;
     int trans;
     double* T;  // per node 2R x w (ld 2R)
+    int stage_lu;
 };
 
 /// One thread per RHS column; LU in global memory (L1/L2 broadcast reads).
@@ -450,6 +451,12 @@ __global__ void k_cap_solve(CapSolveArgs g) {
     const int nthr = blockDim.x;
     double* x = sm;  // x[r * nthr + c]
     const double* A = g.lu + i64(j) * m * m;
+    if (g.stage_lu) {  // the LU in shared memory: every substitution step reads it
+        double* As = sm + m * nthr;
+        for (int e = threadIdx.x; e < m * m; e += nthr) As[e] = A[e];
+        __syncthreads();
+        A = As;
+    }
     const int* piv = g.piv + i64(j) * m;
     const bool active = col < g.w;
     if (active) {
@@ -518,12 +525,14 @@ void cap_solve(const DFactor& f, int i, const double* Q, bool top_odd, bool tran
     const int nodes = 1 << (i - 1);
     int thr = 64;
     while (thr > 8 && static_cast<size_t>(m) * thr * sizeof(double) > SMEM_CAP) thr >>= 1;
-    const size_t smem = static_cast<size_t>(m) * thr * sizeof(double);
+    size_t smem = static_cast<size_t>(m) * thr * sizeof(double);
     if (smem > SMEM_CAP) throw std::length_error("cap_solve: capacitance too large for shared memory");
+    const bool stage = smem + static_cast<size_t>(m) * m * sizeof(double) <= SMEM_CAP;
+    if (stage) smem += static_cast<size_t>(m) * m * sizeof(double);
     ProfScope prof(PROF_CAP_SOLVE, 2.0 * nodes * double(m) * m * w, 8.0 * nodes * (double(m) * m + 2.0 * m * w));
     set_smem(reinterpret_cast<const void*>(k_cap_solve), smem);
     CapSolveArgs g{R, w, f.cap[static_cast<size_t>(i - 1)]->get(), f.cap_piv[static_cast<size_t>(i - 1)]->get(), Q, top_odd ? 1 : 0,
-                   trans ? 1 : 0, T};
+                   trans ? 1 : 0, T, stage ? 1 : 0};
     dim3 grid(unsigned(nodes), unsigned(cdiv(w, thr)));
     k_cap_solve<<<grid, thr, smem, current().stream>>>(g);
     HG_LAUNCH();
