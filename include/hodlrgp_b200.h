@@ -66,11 +66,17 @@ void* hg_ctx_stream(hg_ctx_t ctx);
  *    renormalised, so [q | q2] is orthonormal to roundoff; columns kept near
  *    the w2 floor otherwise overlap q and double-count dK q in the committed
  *    derivative block (the error that dominates dK/dtheta at n = 2^20).
- *    HG_Q2_REFERENCE: q2 exactly as the reference forms it (parity mode). */
-enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2, HG_OPT_Q2_BASIS = 3 };
+ *    HG_Q2_REFERENCE: q2 exactly as the reference forms it (parity mode).
+ *  HG_OPT_COMPRESS_AT — when the derivative blocks are truncated
+ *    (LowRankBlock::compressed at 1e-13). HG_COMPRESS_AT_LEVEL (default): as
+ *    each level is committed, so finer levels peel against the compressed
+ *    (rank ~3..8 instead of 2k + w2) panels. HG_COMPRESS_AT_END: after the
+ *    last level, as sketch.cpp:331-341 (parity mode). */
+enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2, HG_OPT_Q2_BASIS = 3, HG_OPT_COMPRESS_AT = 4 };
 enum { HG_ASSOC_SOLVE = 0, HG_ASSOC_REFERENCE = 1 };
 enum { HG_COMPRESS_PIVOTED_QR = 0, HG_COMPRESS_JACOBI_SVD = 1 };
 enum { HG_Q2_REORTHOGONALIZED = 0, HG_Q2_REFERENCE = 1 };
+enum { HG_COMPRESS_AT_LEVEL = 0, HG_COMPRESS_AT_END = 1 };
 hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value);
 int hg_ctx_get_option(hg_ctx_t ctx, int option);
 

@@ -89,6 +89,7 @@ int or_enable_blas(const char* path, int threads) { return enable_external_blas(
 const char* or_blas_backend() { return blas_backend(); }
 void or_set_solve_association(int on) { set_solve_association(on != 0); }
 void or_set_q2_reorthogonalize(int on) { set_q2_reorthogonalize(on != 0); }
+void or_set_compress_at_level(int on) { set_compress_at_level(on != 0); }
 
 // ------------------------------------------------------------------ tree
 int or_tree_depth(std::int64_t n, std::int64_t lmin, std::int64_t lmax) { return tree_depth(n, lmin, lmax); }

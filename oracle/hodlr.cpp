@@ -18,6 +18,8 @@ namespace oracle {
 
 bool g_q2_reorthogonalize = false;
 void set_q2_reorthogonalize(bool on) { g_q2_reorthogonalize = on; }
+bool g_compress_at_level = false;
+void set_compress_at_level(bool on) { g_compress_at_level = on; }
 
 // ============================================================ cluster tree
 // cluster_tree.cpp:10-22
@@ -723,7 +725,9 @@ BuildResult build_impl(const CovarianceOracle& oracle, const ClusterTree& tree, 
                                                       LowRankBlock{cap[static_cast<size_t>(j)].q, dt[static_cast<size_t>(param)][static_cast<size_t>(j)]});
                 const Mat& b = q2[static_cast<size_t>(j)];
                 if (b.c > 0) d = LowRankBlock::concat(d, LowRankBlock{b, dt2[static_cast<size_t>(param)][static_cast<size_t>(j)]});
-                out.deriv[static_cast<size_t>(param)].upper(l, j) = d;
+                // device HG_COMPRESS_AT_LEVEL: compress at commit, so finer
+                // levels peel against the compressed block
+                out.deriv[static_cast<size_t>(param)].upper(l, j) = g_compress_at_level ? d.compressed(1e-13) : d;
             }
             BuildDecision dec;
             dec.level = l;
@@ -748,7 +752,7 @@ BuildResult build_impl(const CovarianceOracle& oracle, const ClusterTree& tree, 
             out.deriv[static_cast<size_t>(param)].leaf(b) = dyl.block(r.lo, 0, r.size(), r.size());
         }
     }
-    for (Index param = 0; param < p; ++param)
+    for (Index param = 0; param < p && !g_compress_at_level; ++param)
         for (int l = 1; l <= tau; ++l) {
             const Index nodes = Index(tree.level(l - 1).size());
 #pragma omp parallel for schedule(static)

@@ -421,6 +421,11 @@ void set_solve_association(bool on);
 /// each q2 is projected against q once more and its columns renormalised,
 /// the device's default HG_Q2_REORTHOGONALIZED.
 void set_q2_reorthogonalize(bool on);
+/// Diagnostic switch (default off = the reference, sketch.cpp:331-341: every
+/// derivative block compressed after the last level). On: each level's
+/// blocks are compressed when committed, the device's default
+/// HG_COMPRESS_AT_LEVEL.
+void set_compress_at_level(bool on);
 ProductRep multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 ProductRep solve_multiply(const HodlrFactorization& f, const HodlrMatrix& b);
 double trace_product_rep(const ProductRep& p);

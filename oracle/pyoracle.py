@@ -48,6 +48,7 @@ def lib():
             "or_blas_backend": (C.c_char_p, []),
             "or_set_solve_association": (None, [C.c_int]),
             "or_set_q2_reorthogonalize": (None, [C.c_int]),
+            "or_set_compress_at_level": (None, [C.c_int]),
             "or_tree_depth": (C.c_int, [i64, i64, i64]),
             "or_tree_ranges": (C.c_int, [i64, C.c_int, lp]),
             "or_kd_ordering": (C.c_int, [i64, C.c_int, dp, i64, i64, lp, lp, ip]),
@@ -146,6 +147,19 @@ def set_solve_association(on):
 def set_q2_reorthogonalize(on):
     """Diagnostic: the device's default q2 basis (HG_Q2_REORTHOGONALIZED, see oracle.hpp)."""
     lib().or_set_q2_reorthogonalize(int(on))
+
+
+def set_compress_at_level(on):
+    """Diagnostic: the device's default HG_COMPRESS_AT_LEVEL (see oracle.hpp)."""
+    lib().or_set_compress_at_level(int(on))
+
+
+def device_defaults(on):
+    """Every oracle switch set to the device's default numerical modes (on) or
+    back to the reference (off)."""
+    set_solve_association(on)
+    set_q2_reorthogonalize(on)
+    set_compress_at_level(on)
 
 
 def randn(r, c, seed):

@@ -7,7 +7,7 @@
 // implementation itself instead of a restatement.
 //
 // Differences from oracle/capi.cpp, all because the reference exposes no such
-// hook: or_set_solve_association / or_set_q2_reorthogonalize are ignored (the reference has only its own
+// hook: or_set_solve_association / or_set_q2_reorthogonalize / or_set_compress_at_level are ignored (the reference has only its own
 // association, product_rep.cpp:74-78), or_build_decisions reports 0 nodes and
 // or_factor_leaf_llt is unavailable (LeafFactor::use_llt_ is private).
 #include <chrono>
@@ -168,6 +168,7 @@ OR_API int or_enable_blas(const char* path, int threads) { return oracle::enable
 OR_API const char* or_blas_backend() { return oracle::blas_backend(); }
 OR_API void or_set_solve_association(int) {}
 OR_API void or_set_q2_reorthogonalize(int) {}
+OR_API void or_set_compress_at_level(int) {}
 OR_API int or_is_reference() { return 1; }
 
 // ------------------------------------------------------------------ tree

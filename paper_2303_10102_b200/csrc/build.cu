@@ -1196,6 +1196,12 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
                 D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
             }
+            // HG_COMPRESS_AT_LEVEL: compress the level when it is committed, so
+            // every finer level's peels stream the compressed (rank ~3..8)
+            // panels instead of the 2k + w2 wide concatenation
+            if (ctx.compress_at == HG_COMPRESS_AT_LEVEL)
+                compress_level_structured(D, l, k, omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(),
+                                          1e-13);
         }
         // Value level panel: q on left rows, t = Z on right rows.
         out.h.set_level(l, k, true);
@@ -1229,7 +1235,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         }
     }
     // Recompress every derivative off-diagonal block (sketch.cpp:331-341).
-    for (int q = 0; q < p; ++q)
+    for (int q = 0; q < p && ctx.compress_at == HG_COMPRESS_AT_END; ++q)
         for (int l = 1; l <= tau; ++l)
             compress_level_structured(out.deriv[static_cast<size_t>(q)], l, k,
                                       omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(), 1e-13);

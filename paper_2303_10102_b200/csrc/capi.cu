@@ -195,6 +195,8 @@ hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value) {
             ctx->c.compression = value;
         else if (option == HG_OPT_Q2_BASIS && (value == HG_Q2_REORTHOGONALIZED || value == HG_Q2_REFERENCE))
             ctx->c.q2_basis = value;
+        else if (option == HG_OPT_COMPRESS_AT && (value == HG_COMPRESS_AT_LEVEL || value == HG_COMPRESS_AT_END))
+            ctx->c.compress_at = value;
         else
             throw std::invalid_argument("hg_ctx_set_option: unknown option or value");
     });
@@ -205,6 +207,7 @@ int hg_ctx_get_option(hg_ctx_t ctx, int option) {
     if (option == HG_OPT_PRODUCT_ASSOCIATION) return ctx->c.product_assoc;
     if (option == HG_OPT_COMPRESSION) return ctx->c.compression;
     if (option == HG_OPT_Q2_BASIS) return ctx->c.q2_basis;
+    if (option == HG_OPT_COMPRESS_AT) return ctx->c.compress_at;
     return -1;
 }
 

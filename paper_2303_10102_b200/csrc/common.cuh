@@ -53,6 +53,7 @@ struct Ctx {
     int product_assoc = 0;       // HG_OPT_PRODUCT_ASSOCIATION (HG_ASSOC_*)
     int compression = 0;         // HG_OPT_COMPRESSION (HG_COMPRESS_*)
     int q2_basis = 0;            // HG_OPT_Q2_BASIS (HG_Q2_*)
+    int compress_at = 0;         // HG_OPT_COMPRESS_AT (HG_COMPRESS_AT_*)
 };
 
 

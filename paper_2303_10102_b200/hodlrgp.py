@@ -23,8 +23,9 @@ lp = C.POINTER(C.c_int64)
 HOST, DEVICE = 0, 1
 RIGHT, LEFT = 0, 1
 # Context options (include/hodlrgp_b200.h)
-OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION, OPT_Q2_BASIS = 1, 2, 3
+OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION, OPT_Q2_BASIS, OPT_COMPRESS_AT = 1, 2, 3, 4
 Q2_REORTHOGONALIZED, Q2_REFERENCE = 0, 1
+COMPRESS_AT_LEVEL, COMPRESS_AT_END = 0, 1
 ASSOC_SOLVE, ASSOC_REFERENCE = 0, 1
 COMPRESS_PIVOTED_QR, COMPRESS_JACOBI_SVD = 0, 1
 

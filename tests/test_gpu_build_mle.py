@@ -112,23 +112,29 @@ def c1_points(n=4096):
 def reference_modes(H):
     """Device in the reference-faithful parity modes (product association of
     product_rep.cpp:32-45,74-78, Jacobi-SVD truncation of hodlr_matrix.cpp:42-66,
-    q2 exactly as sketch.cpp:194-233) for the duration of one test."""
+    q2 exactly as sketch.cpp:194-233, derivative blocks compressed after the
+    last level as sketch.cpp:331-341) for the duration of one test."""
     ctx = H.context()
     ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, H.ASSOC_REFERENCE)
     ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_JACOBI_SVD)
     ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REFERENCE)
+    ctx.set_option(H.OPT_COMPRESS_AT, H.COMPRESS_AT_END)
     yield ctx
     ctx.set_option(H.OPT_PRODUCT_ASSOCIATION, H.ASSOC_SOLVE)
     ctx.set_option(H.OPT_COMPRESSION, H.COMPRESS_PIVOTED_QR)
     ctx.set_option(H.OPT_Q2_BASIS, H.Q2_REORTHOGONALIZED)
+    ctx.set_option(H.OPT_COMPRESS_AT, H.COMPRESS_AT_LEVEL)
 
 
 @pytest.fixture
 def oracle_q2_reorth():
-    """The oracle switched to the device's default q2 basis (oracle.hpp)."""
+    """The oracle switched to the device's default build modes (q2 basis,
+    compression at commit; oracle.hpp)."""
     O.set_q2_reorthogonalize(True)
+    O.set_compress_at_level(True)
     yield
     O.set_q2_reorthogonalize(False)
+    O.set_compress_at_level(False)
 
 
 BUILD_CASES = [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4), (2048, 128, 40, 5, 0.05, 1e-6),
@@ -216,10 +222,10 @@ def test_mle_iteration_c1_end_to_end(H):
     and Fisher 1e-7."""
     n, tau, k, x, oo, K, y = _c1_setup()
     try:
-        O.set_solve_association(True)
+        O.device_defaults(True)
         ll0, s0, f0, _ = O.mle_iteration(oo, tau, k, 0, y, 2)
     finally:
-        O.set_solve_association(False)
+        O.device_defaults(False)
     do = H.MaternOracle(x, 3, 1.0, 0.2, 1e-4, False)
     ll1, s1, f1, t = H.mle_iteration(do, tau, k, 0, y)
     assert ll1 == pytest.approx(ll0, rel=1e-9)

@@ -139,13 +139,11 @@ def test_c4_settings_agree_with_oracle_and_dense_at_2_14():
     y = np.random.default_rng(1).standard_normal(n)
     tau = H.tree_depth(n, 128, 256)
     ll1, s1, f1, _ = H.mle_iteration(H.MaternOracle(x, 5, 1.0, 0.05, 1e-6, True), tau, K_RANK, SEED, y)
-    O.set_solve_association(True)
-    O.set_q2_reorthogonalize(True)
+    O.device_defaults(True)
     try:
         ll0, s0, f0, _ = O.mle_iteration(O.CovOracle.matern(x, 5, 1.0, 0.05, 1e-6, True), tau, K_RANK, SEED, y, 2)
     finally:
-        O.set_solve_association(False)
-        O.set_q2_reorthogonalize(False)
+        O.device_defaults(False)
     # dense truth (torch FP64 on the GPU)
     xt = torch.tensor(x, dtype=torch.float64, device="cuda")
     a = (xt[:, None] - xt[None, :]).abs_().mul_(np.sqrt(5.0) / 0.05)
