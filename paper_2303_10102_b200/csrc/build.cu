@@ -990,6 +990,13 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
     // Omega (in-span rotation of diff_qr) per param and level, for the recompression.
     std::vector<std::vector<DVecP>> omegas(static_cast<size_t>(p), std::vector<DVecP>(static_cast<size_t>(tau)));
     auto& ctx = current();
+    // which derivatives are compressed as each level is committed
+    // (HG_OPT_COMPRESS_AT; HG_COMPRESS_LEVEL_MASK: per-parameter bit mask, tuning knob)
+    static const unsigned level_mask = [] {
+        const char* e = std::getenv("HG_COMPRESS_LEVEL_MASK");
+        return e ? unsigned(std::strtoul(e, nullptr, 0)) : ~0u;
+    }();
+    auto at_level = [&](int q) { return ctx.compress_at == HG_COMPRESS_AT_LEVEL && ((level_mask >> q) & 1u); };
 
     for (int l = 1; l <= tau; ++l) {
         const Partition& pc = tree->part(l);
@@ -1199,7 +1206,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             // HG_COMPRESS_AT_LEVEL: compress the level when it is committed, so
             // every finer level's peels stream the compressed (rank ~3..8)
             // panels instead of the 2k + w2 wide concatenation
-            if (ctx.compress_at == HG_COMPRESS_AT_LEVEL)
+            if (at_level(q))
                 compress_level_structured(D, l, k, omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(),
                                           1e-13);
         }
@@ -1235,8 +1242,8 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         }
     }
     // Recompress every derivative off-diagonal block (sketch.cpp:331-341).
-    for (int q = 0; q < p && ctx.compress_at == HG_COMPRESS_AT_END; ++q)
-        for (int l = 1; l <= tau; ++l)
+    for (int q = 0; q < p; ++q)
+        for (int l = 1; l <= tau && !at_level(q); ++l)
             compress_level_structured(out.deriv[static_cast<size_t>(q)], l, k,
                                       omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(), 1e-13);
     return out;

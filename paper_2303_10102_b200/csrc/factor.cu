@@ -1,6 +1,7 @@
 // HODLR factorization, Woodbury solves and log-determinant on the device.
 // Reference: factorization.cpp:7-224 (see factor.cuh for the data layout).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "factor.cuh"
@@ -702,9 +703,23 @@ void level_inverse(const DFactor& f, int i, bool transposed, double* Y, i64 ldy,
     // refinement Q <- Q - A T, T += S Q. Without the refinement the explicit
     // inverse loses ~2 digits on the C1 parity case (cond(cap) ~ 1e7); with
     // it the result matches the LU substitution of the reference.
+    static const int refine = [] {  // HG_CAP_REFINE: refinement steps (tuning/diagnostic knob)
+        const char* e = std::getenv("HG_CAP_REFINE");
+        return e ? std::max(0, std::atoi(e)) : 1;
+    }();
     seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w);
-    seg_nn(up, A, L, m, T.get(), m, int(L), TMap::same(), Q.get(), L, w, -1.0, 1.0);
-    seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w, 1.0, 1.0);
+    if (refine > 1) {  // keep the right-hand side: every step needs its residual
+        DVec Q0(static_cast<size_t>(L) * static_cast<size_t>(w));
+        panel_axpby(L, w, 1.0, Q.get(), L, 0.0, Q0.get(), L);
+        for (int it = 0; it < refine; ++it) {
+            panel_axpby(L, w, 1.0, Q0.get(), L, 0.0, Q.get(), L);
+            seg_nn(up, A, L, m, T.get(), m, int(L), TMap::same(), Q.get(), L, w, -1.0, 1.0);
+            seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w, 1.0, 1.0);
+        }
+    } else if (refine == 1) {
+        seg_nn(up, A, L, m, T.get(), m, int(L), TMap::same(), Q.get(), L, w, -1.0, 1.0);
+        seg_nn(up, S, L, m, Q.get(), m, int(L), TMap::same(), T.get(), L, w, 1.0, 1.0);
+    }
     if (!transposed)
         seg_nn(p, f.Wl(i), n, R, T.get(), m, int(L), TMap::parent(0, R), Y, ldy, w, -1.0, 1.0);
     else

@@ -153,7 +153,7 @@ void trace_product_rep(const DProductRep& p, double* out, bool accumulate) {
     if (p.sumC) dot_panels(p.n(), p.sumC, p.Cu->get(), p.n(), p.Cv->get(), p.n(), out, true);
 }
 
-void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool accumulate) {
+void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool accumulate, bool with_pairs) {
     const int tau = pb.tau();
     const i64 n = pb.n();
     const DTree& t = *pb.base.tree;
@@ -226,7 +226,7 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
         seg_tn(p, coarse.Cu->get() + i64(c0) * n, n, W, fine.Cvl(f), n, Cf, G2.get(), i64(W) * Cf, W);
         seg_dot(1, 0, G1.get(), 0, G2.get(), 0, i64(p.nseg()) * W * Cf, out, true);
     };
-    for (int f = 1; f <= tau; ++f) {
+    for (int f = 1; f <= tau && with_pairs; ++f) {
         const int cf = pb.coff[static_cast<size_t>(f - 1)];
         if (same) {  // sum_{i<=f} + sum_{i<f} = 2 sum_{i<f} + (i = f)
             pairs(pb, 0, cf, pb, f, 2.0);
@@ -236,6 +236,57 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
             pairs(pd, 0, pd.coff[static_cast<size_t>(f - 1)], pb, f, 1.0);    // i > j: coarse from pd
         }
     }
+}
+
+std::vector<double> fisher_pairs(const std::vector<DProductRep>& reps) {
+    const size_t p = reps.size();
+    std::vector<double> out(p * p, 0.0);
+    if (p == 0 || !reps[0].sumC) return out;
+    const int tau = reps[0].tau();
+    const i64 n = reps[0].n();
+    const DTree& t = *reps[0].base.tree;
+    for (const auto& r : reps)
+        if (r.C != reps[0].C || r.n() != n) throw std::invalid_argument("fisher_pairs: reps of different factorizations");
+    // cc[i + j p] = sum_f <Cv_i[<f]^T Cu_f, Cu[<f]^T Cv_j,f>, ss likewise over
+    // the level-f columns themselves (product_rep.cpp:227-233: i <= j pairs
+    // align by the finer level; the i = f term appears once, i < f twice for
+    // a rep with itself)
+    DVec cc(p * p), ss(p * p);
+    cc.zero();
+    ss.zero();
+    for (int f = 1; f <= tau; ++f) {
+        const int Cf = reps[0].C[static_cast<size_t>(f - 1)];
+        const int cf = reps[0].coff[static_cast<size_t>(f - 1)];
+        if (!Cf) continue;
+        const Partition& pt = t.part(f - 1);
+        const i64 nseg = pt.nseg();
+        std::vector<DVec> G1c(p), G2c(p), G1s(p), G2s(p);
+        for (size_t a = 0; a < p; ++a) {
+            const DProductRep& r = reps[a];
+            if (cf) {
+                G1c[a].alloc(static_cast<size_t>(nseg) * cf * Cf);
+                G2c[a].alloc(static_cast<size_t>(nseg) * cf * Cf);
+                seg_tn(pt, r.Cv->get(), n, cf, r.Cul(f), n, Cf, G1c[a].get(), i64(cf) * Cf, cf);
+                // (Cv_f^T Cu_c)^T formed directly as Cu_c^T Cv_f: the pair terms are contiguous dots
+                seg_tn(pt, r.Cu->get(), n, cf, r.Cvl(f), n, Cf, G2c[a].get(), i64(cf) * Cf, cf);
+            }
+            G1s[a].alloc(static_cast<size_t>(nseg) * Cf * Cf);
+            G2s[a].alloc(static_cast<size_t>(nseg) * Cf * Cf);
+            seg_tn(pt, r.Cvl(f), n, Cf, r.Cul(f), n, Cf, G1s[a].get(), i64(Cf) * Cf, Cf);
+            seg_tn(pt, r.Cul(f), n, Cf, r.Cvl(f), n, Cf, G2s[a].get(), i64(Cf) * Cf, Cf);
+        }
+        const i64 lc = nseg * i64(cf) * Cf, ls = nseg * i64(Cf) * Cf;
+        for (size_t i = 0; i < p; ++i)
+            for (size_t j = 0; j < p; ++j) {  // cc needs every ordered pair, ss only i <= j
+                if (cf) seg_dot(1, 0, G1c[i].get(), 0, G2c[j].get(), 0, lc, cc.get() + i + j * p, true);
+                if (i <= j) seg_dot(1, 0, G1s[i].get(), 0, G2s[j].get(), 0, ls, ss.get() + i + j * p, true);
+            }
+    }
+    const std::vector<double> c = cc.download(), q = ss.download();
+    for (size_t i = 0; i < p; ++i)
+        for (size_t j = i; j < p; ++j)
+            out[i + j * p] = i == j ? 2.0 * c[i + i * p] + q[i + i * p] : c[i + j * p] + q[i + j * p] + c[j + i * p];
+    return out;
 }
 
 std::vector<double> prodrep_densify(const DProductRep& p) {
