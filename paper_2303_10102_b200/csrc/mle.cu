@@ -28,10 +28,9 @@ std::vector<double> score(const DFactor& f, const std::vector<const DHodlr*>& de
     factor_solve(f, w.get(), n, 1);
     std::vector<DProductRep> local;
     std::vector<DProductRep>& rp = reps ? *reps : local;
-    rp.clear();
+    rp = pipeline_multi(f, deriv, true);
     for (size_t j = 0; j < p; ++j) {
-        rp.push_back(pipeline(f, *deriv[j], true));
-        trace_product_rep(rp.back(), acc.get() + 2 * j, false);
+        trace_product_rep(rp[j], acc.get() + 2 * j, false);
         hodlr_apply(*deriv[j], w.get(), n, 1, kw.get(), n, 1, deriv[j]->tau(), true, false, 0.0);
         dot_panels(n, 1, w.get(), n, kw.get(), n, acc.get() + 2 * j + 1, false);
     }

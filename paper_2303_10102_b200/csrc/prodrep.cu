@@ -56,45 +56,71 @@ void level_multiply(const DFactor& f, int i, double* Y, i64 ldy, int w) {
 }
 
 DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
-    if (!f.tree->host.same_structure(b.tree->host))
-        throw std::invalid_argument("product pipeline: tree structure mismatch");
+    return pipeline_multi(f, std::vector<const DHodlr*>{&b}, inverse)[0];
+}
+
+std::vector<DProductRep> pipeline_multi(const DFactor& f, const std::vector<const DHodlr*>& bs, bool inverse) {
+    for (const DHodlr* b : bs)
+        if (!f.tree->host.same_structure(b->tree->host))
+            throw std::invalid_argument("product pipeline: tree structure mismatch");
     if (!inverse && f.orient != 0) throw std::invalid_argument("multiply: factorization must be Right-oriented");
     if (inverse && f.orient != 1) throw std::invalid_argument("solve_multiply: factorization must be Left-oriented");
     const int tau = f.tau();
     const i64 n = f.n();
-    DProductRep rep;
-    rep.base = b;
-    rep.base.make_asymmetric();
-    rep.C.assign(static_cast<size_t>(tau), 0);
-    rep.coff.assign(static_cast<size_t>(tau), 0);
-    for (int i = 1; i <= tau; ++i) {
-        rep.coff[static_cast<size_t>(i - 1)] = rep.sumC;
-        rep.C[static_cast<size_t>(i - 1)] = 2 * f.Rl(i);
-        rep.sumC += rep.C[static_cast<size_t>(i - 1)];
+    const size_t P = bs.size();
+    std::vector<DProductRep> reps(P);
+    for (size_t j = 0; j < P; ++j) {
+        DProductRep& rep = reps[j];
+        rep.base = *bs[j];
+        rep.base.make_asymmetric();
+        rep.C.assign(static_cast<size_t>(tau), 0);
+        rep.coff.assign(static_cast<size_t>(tau), 0);
+        for (int i = 1; i <= tau; ++i) {
+            rep.coff[static_cast<size_t>(i - 1)] = rep.sumC;
+            rep.C[static_cast<size_t>(i - 1)] = 2 * f.Rl(i);
+            rep.sumC += rep.C[static_cast<size_t>(i - 1)];
+        }
     }
+    if (P == 0) return reps;
     // Every column the pipeline rewrites lives in ONE n-row panel, ordered
-    //   [U_tau | ... | U_2 | U_1 | Cu_1 | ... | Cu_tau | leaves]
-    // so the columns factor level i acts on (the base's coarser left factors
-    // U_{m<i} and the older corrections Cu_{<i}) are one contiguous block, and
-    // the final leaf step is a single call over the whole panel.
-    std::vector<int> ucum(static_cast<size_t>(tau + 1), 0);  // ucum[m] = sum_{m' <= m} R_m'
-    for (int m = 1; m <= tau; ++m) ucum[static_cast<size_t>(m)] = ucum[static_cast<size_t>(m - 1)] + rep.base.Rl(m);
-    const int sumR = ucum[static_cast<size_t>(tau)], cw = std::max(rep.sumC, 1), bm = f.bmax();
-    const int cuo = sumR, lo = sumR + cw, total = lo + bm;
+    //   [G_tau | ... | G_2 | G_1 | Cu_1 | ... | Cu_tau | leaves_0 | .. | leaves_{P-1}]
+    // with G_m = [U_m of base 0 | .. | U_m of base P-1], so the columns factor
+    // level i acts on (every base's coarser left factors U_{m<i} and the older
+    // corrections Cu_{<i}) are one contiguous block, and the final leaf step
+    // is a single call over the whole panel. The corrections' left factors
+    // p = -v cap^{-T}, and every factor level's update of them, depend on the
+    // factorization only (product_rep.cpp:74-78, 84-104): the P reps share one
+    // Cu, formed and updated once.
+    std::vector<int> ucum(static_cast<size_t>(tau + 1), 0);  // ucum[m] = sum_{m' <= m} sum_j R_m'(j)
+    for (int m = 1; m <= tau; ++m) {
+        int g = 0;
+        for (size_t j = 0; j < P; ++j) g += reps[j].base.Rl(m);
+        ucum[static_cast<size_t>(m)] = ucum[static_cast<size_t>(m - 1)] + g;
+    }
+    const int sumR = ucum[static_cast<size_t>(tau)], cw = std::max(reps[0].sumC, 1), bm = f.bmax();
+    const int cuo = sumR, lo = sumR + cw, total = lo + int(P) * bm;
     DVecP store = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(total), false);
     double* S = store->get();
     panel_axpby(n, cw, 0.0, nullptr, 0, 0.0, S + i64(cuo) * n, n);
-    // Left factors are rewritten: the base gets its own copies (right factors stay aliased).
+    // Left factors are rewritten: each base gets its own copies (right factors stay aliased).
     for (int m = 1; m <= tau; ++m) {
-        const int R = rep.base.Rl(m);
-        if (!R) continue;
-        double* dst = S + i64(sumR - ucum[static_cast<size_t>(m)]) * n;
-        panel_axpby(n, R, 1.0, b.Ul(m), n, 0.0, dst, n);
-        rep.base.U[static_cast<size_t>(m - 1)] = make_view(store, dst, static_cast<size_t>(n) * static_cast<size_t>(R));
+        int off = sumR - ucum[static_cast<size_t>(m)];
+        for (size_t j = 0; j < P; ++j) {
+            const int R = reps[j].base.Rl(m);
+            if (!R) continue;
+            double* dst = S + i64(off) * n;
+            panel_axpby(n, R, 1.0, bs[j]->Ul(m), n, 0.0, dst, n);
+            reps[j].base.U[static_cast<size_t>(m - 1)] =
+                make_view(store, dst, static_cast<size_t>(n) * static_cast<size_t>(R));
+            off += R;
+        }
     }
-    rep.base.leaves = std::make_shared<DVec>(*b.leaves);
-    rep.Cu = make_view(store, S + i64(cuo) * n, static_cast<size_t>(n) * static_cast<size_t>(cw));
-    rep.Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(cw), true);
+    DVecP cu_all = make_view(store, S + i64(cuo) * n, static_cast<size_t>(n) * static_cast<size_t>(cw));
+    for (size_t j = 0; j < P; ++j) {
+        reps[j].base.leaves = std::make_shared<DVec>(*bs[j]->leaves);
+        reps[j].Cu = cu_all;
+        reps[j].Cv = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(cw), true);
+    }
 
     const bool ref_assoc = inverse && current().product_assoc == HG_ASSOC_REFERENCE;
     for (int i = 1; i <= tau; ++i) {
@@ -102,7 +128,7 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
         if (R == 0) continue;
         const Partition& p = f.tree->part(i);
         const int C2 = 2 * R;
-        double* cu = rep.Cul(i);
+        double* cu = reps[0].Cul(i);
         // p = -v cap^{-T}: rows cl = -w E[R:2R,:], rows cr = -x E[0:R,:]
         auto form_p = [&] {
             if (ref_assoc)  // the reference's LU substitution on v^T (no explicit inverse)
@@ -112,9 +138,9 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
                        TMap::parent(R, 0), cu, n, C2, -1.0, 0.0);
         };
         // product_rep.cpp:84-104: older corrections' left factors and the
-        // running base's coarser left factors, in one call.
+        // running bases' coarser left factors, in one call.
         const int us = ucum[static_cast<size_t>(i - 1)];
-        const int wu = us + rep.coff[static_cast<size_t>(i - 1)];
+        const int wu = us + reps[0].coff[static_cast<size_t>(i - 1)];
         if (ref_assoc) {
             // The reference's association (product_rep.cpp:32-45,74-78): p is
             // formed first, then rows += p (q^T rows) with q = u.
@@ -138,14 +164,18 @@ DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse) {
             panel_parity_scale(p, n, R, f.Fl(i), n, 0.0, 1.0, Q.get(), n, 0.0);
             panel_parity_scale(p, n, R, f.Fl(i), n, 1.0, 0.0, Q.get() + i64(R) * n, n, 0.0);
         }
-        hodlr_apply(rep.base, Q.get(), n, C2, rep.Cvl(i), n, i, tau, true, true, 0.0);
+        for (size_t j = 0; j < P; ++j)
+            hodlr_apply(reps[j].base, Q.get(), n, C2, reps[j].Cvl(i), n, i, tau, true, true, 0.0);
     }
     // product_rep.cpp:124-152: leaf factor on every stored left factor and the leaves.
-    leaves_panel(*f.tree, rep.base.leaves->get(), S + i64(lo) * n, true);
+    for (size_t j = 0; j < P; ++j)
+        leaves_panel(*f.tree, reps[j].base.leaves->get(), S + i64(lo + int(j) * bm) * n, true);
     leaf_step(f, inverse, S, total);
-    leaves_panel(*f.tree, rep.base.leaves->get(), S + i64(lo) * n, false);
-    rep.base.leaves_zero = false;
-    return rep;
+    for (size_t j = 0; j < P; ++j) {
+        leaves_panel(*f.tree, reps[j].base.leaves->get(), S + i64(lo + int(j) * bm) * n, false);
+        reps[j].base.leaves_zero = false;
+    }
+    return reps;
 }
 
 void trace_product_rep(const DProductRep& p, double* out, bool accumulate) {

@@ -26,6 +26,11 @@ struct DProductRep {
 
 /// product_rep.cpp:47-155 (inverse = solve_multiply, else multiply).
 DProductRep pipeline(const DFactor& f, const DHodlr& b, bool inverse);
+/// The pipeline for several operands of one factorization in one pass: the
+/// correction left factors Cu depend on the factorization only, so the reps
+/// share one Cu panel (formed and updated once) and every factor level
+/// streams its panels once for all operands.
+std::vector<DProductRep> pipeline_multi(const DFactor& f, const std::vector<const DHodlr*>& bs, bool inverse);
 
 /// out (+)= trace_product_rep (product_rep.cpp:188-194).
 void trace_product_rep(const DProductRep& p, double* out, bool accumulate);
