@@ -259,13 +259,19 @@ __device__ double block_sum(double v);
 /// never stored (the cross-term leaf part of trace_pair, product_rep.cpp:212-224).
 /// Each CTA runs `tiles_per` column tiles of one 64-row leaf tile and writes
 /// one partial (fixed order => deterministic).
+struct DotZ {
+    const double* Z[LEAF_DOT_MAXZ];
+    double alpha[LEAF_DOT_MAXZ];
+    int nz;
+};
+
 template <int TBN>
-__global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, const double* Z, i64 ldz, int tiles_per,
+__global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, DotZ zs, i64 ldz, int tiles_per,
                                                          double* partial) {
     extern __shared__ double smem[];
     const int b = blockIdx.x / g.rt, mt = blockIdx.x % g.rt;
     const int lo = g.bounds[b], m = g.bounds[b + 1] - lo, r0 = mt * BM;
-    double part = 0.0;
+    double part[LEAF_DOT_MAXZ] = {};
     if (r0 < m) {
         const double* Lb = g.L + i64(b) * g.lstride;
         const int ntiles = cdiv_d(g.w, TBN);
@@ -278,14 +284,23 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, const dou
             acc.zero();
             tile::run_t<NS_SHORT, BM, TBN>(la, lb, cdiv_d(m, BK), smem, acc);
             __syncthreads();  // every warp is done with the stages before the next tile refills them
+            // one product, dotted with every Z (the product is never stored)
             tile::for_each_slot<BM, TBN>(acc, [&](double& v, int mi0, int ni) {
                 const int mi = r0 + mi0, n = n0 + ni;
-                if (n < g.w && mi < m) part = fma(v, Z[i64(lo + mi) + i64(n) * ldz], part);
+                if (n < g.w && mi < m)
+#pragma unroll
+                    for (int z = 0; z < LEAF_DOT_MAXZ; ++z)
+                        if (z < zs.nz) part[z] = fma(v, zs.Z[z][i64(lo + mi) + i64(n) * ldz], part[z]);
             });
         }
     }
-    part = block_sum(part);
-    if (threadIdx.x == 0) partial[blockIdx.x + i64(blockIdx.y) * gridDim.x] = g.alpha * part;
+#pragma unroll
+    for (int z = 0; z < LEAF_DOT_MAXZ; ++z) {
+        if (z >= zs.nz) break;
+        const double sz = block_sum(part[z]);
+        if (threadIdx.x == 0)
+            partial[i64(z) * gridDim.x * gridDim.y + blockIdx.x + i64(blockIdx.y) * gridDim.x] = zs.alpha[z] * sz;
+    }
 }
 
 // ------------------------------------------------------------ elementwise
@@ -576,30 +591,51 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
 
 void leaf_mm_dot(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
                  const double* Z, i64 ldz, int w, double alpha, double* out, bool accumulate) {
+    leaf_mm_dot_multi(leaves, L, lstride, ldl, X, ldx, {Z}, ldz, w, {alpha}, {out}, accumulate);
+}
+
+void leaf_mm_dot_multi(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
+                       const std::vector<const double*>& Zs, i64 ldz, int w, const std::vector<double>& alphas,
+                       const std::vector<double*>& outs, bool accumulate) {
+    const size_t nzt = Zs.size();
     if (w <= 0) {
-        if (!accumulate) HG_CUDA(cudaMemsetAsync(out, 0, sizeof(double), current().stream));
+        if (!accumulate)
+            for (double* o : outs) HG_CUDA(cudaMemsetAsync(o, 0, sizeof(double), current().stream));
         return;
     }
     auto& c = current();
     const int rt = cdiv(leaves.max_seg(), BM);
     const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
-    ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + 2.0 * rows * w));
-    if (prof_enabled()) prof.key(prof_tag("leafmmdot w=%d", w));
-    LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, nullptr, 0, w, alpha, 0.0};
+    ProfScope prof(PROF_LEAF_MM, 2.0 * rows * bm * w, 8.0 * (rows * bm + (1.0 + double(nzt)) * rows * w));
+    if (prof_enabled()) prof.key(prof_tag("leafmmdot w=%d z=%d", w, int(nzt)));
+    LeafMmArgs g{leaves.dbounds(), rt, L, lstride, ldl, X, ldx, nullptr, 0, w, 1.0, 0.0};
     const int tbn = tile::tile_for_n(w, BM);
-    with_tile(tbn, [&](auto TN) {
-        constexpr int N = decltype(TN)::value;
-        constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
-        const int ntiles = cdiv(w, N), tiles_per = std::min(ntiles, 4);
-        const dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(ntiles, tiles_per)));
-        DVec partial(static_cast<size_t>(grid.x) * grid.y);
-        attr_once<k_leaf_mm_dot<N>>(bytes);
-        k_leaf_mm_dot<N><<<grid, THREADS, bytes, c.stream>>>(g, Z, ldz, tiles_per, partial.get());
-        HG_LAUNCH();
-        k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get(), int(grid.x * grid.y), out, accumulate ? 1 : 0);
-        HG_LAUNCH();
-        c.launches += 2;
-    });
+    for (size_t z0 = 0; z0 < nzt; z0 += LEAF_DOT_MAXZ) {
+        DotZ zs{};
+        zs.nz = int(std::min<size_t>(LEAF_DOT_MAXZ, nzt - z0));
+        for (int z = 0; z < zs.nz; ++z) {
+            zs.Z[z] = Zs[z0 + size_t(z)];
+            zs.alpha[z] = alphas[z0 + size_t(z)];
+        }
+        with_tile(tbn, [&](auto TN) {
+            constexpr int N = decltype(TN)::value;
+            constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, N);
+            const int ntiles = cdiv(w, N), tiles_per = std::min(ntiles, 4);
+            const dim3 grid(unsigned(leaves.nseg() * rt), unsigned(cdiv(ntiles, tiles_per)));
+            const i64 np = i64(grid.x) * grid.y;
+            DVec partial(static_cast<size_t>(np) * static_cast<size_t>(zs.nz));
+            attr_once<k_leaf_mm_dot<N>>(bytes);
+            k_leaf_mm_dot<N><<<grid, THREADS, bytes, c.stream>>>(g, zs, ldz, tiles_per, partial.get());
+            HG_LAUNCH();
+            ++c.launches;
+            for (int z = 0; z < zs.nz; ++z) {
+                k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get() + i64(z) * np, int(np), outs[z0 + size_t(z)],
+                                                        accumulate ? 1 : 0);
+                HG_LAUNCH();
+                ++c.launches;
+            }
+        });
+    }
 }
 
 void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {

@@ -55,6 +55,12 @@ void seg_dot(int nseg, int xr, const double* A, i64 gsa, const double* B, i64 gs
 /// out[0] (+)= alpha sum((L_b X) .* Z) over the leaves (no n x w product stored).
 void leaf_mm_dot(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
                  const double* Z, i64 ldz, int w, double alpha, double* out, bool accumulate);
+/// outs[z] (+)= alphas[z] sum((L_b X) .* Zs[z]) for several Z with ONE leaf
+/// product (the cross terms of every Fisher pair with the same base).
+constexpr int LEAF_DOT_MAXZ = 4;
+void leaf_mm_dot_multi(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
+                       const std::vector<const double*>& Zs, i64 ldz, int w, const std::vector<double>& alphas,
+                       const std::vector<double*>& outs, bool accumulate);
 
 /// out[0] (+)= sum(A .* B) over n x w (deterministic).
 void dot_panels(i64 n, int w, const double* A, i64 lda, const double* B, i64 ldb, double* out, bool accumulate);

@@ -46,7 +46,7 @@ std::vector<double> fisher_from_reps(const std::vector<DProductRep>& reps) {
     acc.zero();
     for (size_t i = 0; i < p; ++i)
         for (size_t j = i; j < p; ++j) trace_pair(reps[i], reps[j], acc.get() + i + j * p, false, false);
-    const std::vector<double> pairs = fisher_pairs(reps);  // Grams shared across the pairs
+    const std::vector<double> pairs = fisher_corrections(reps);  // products shared across the pairs
     std::vector<double> t = acc.download();
     for (size_t e = 0; e < t.size(); ++e) t[e] += pairs[e];
     std::vector<double> info(p * p), out(p * p);

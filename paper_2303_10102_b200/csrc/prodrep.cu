@@ -183,12 +183,13 @@ void trace_product_rep(const DProductRep& p, double* out, bool accumulate) {
     if (p.sumC) dot_panels(p.n(), p.sumC, p.Cu->get(), p.n(), p.Cv->get(), p.n(), out, true);
 }
 
-void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool accumulate, bool with_pairs) {
+void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool accumulate, bool with_corr) {
     const int tau = pb.tau();
     const i64 n = pb.n();
     const DTree& t = *pb.base.tree;
     const bool same = &pb == &pd;  // tr((A^-1 dA)^2): mirrored terms computed once
     hodlr_trace_product(pb.base, pd.base, out, accumulate);
+    if (!with_corr) return;
     // Cross terms sum_i tr(Cv_i^T h_{>=i} Cu_i) (product_rep.cpp:212-224),
     // regrouped by the level of h: the leaves act on every correction, level
     // l on corrections i <= l, i.e. on the column prefix W_l of Cu / Cv, so
@@ -256,7 +257,7 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
         seg_tn(p, coarse.Cu->get() + i64(c0) * n, n, W, fine.Cvl(f), n, Cf, G2.get(), i64(W) * Cf, W);
         seg_dot(1, 0, G1.get(), 0, G2.get(), 0, i64(p.nseg()) * W * Cf, out, true);
     };
-    for (int f = 1; f <= tau && with_pairs; ++f) {
+    for (int f = 1; f <= tau; ++f) {
         const int cf = pb.coff[static_cast<size_t>(f - 1)];
         if (same) {  // sum_{i<=f} + sum_{i<f} = 2 sum_{i<f} + (i = f)
             pairs(pb, 0, cf, pb, f, 2.0);
@@ -268,7 +269,7 @@ void trace_pair(const DProductRep& pb, const DProductRep& pd, double* out, bool 
     }
 }
 
-std::vector<double> fisher_pairs(const std::vector<DProductRep>& reps) {
+std::vector<double> fisher_corrections(const std::vector<DProductRep>& reps) {
     const size_t p = reps.size();
     std::vector<double> out(p * p, 0.0);
     if (p == 0 || !reps[0].sumC) return out;
@@ -276,7 +277,7 @@ std::vector<double> fisher_pairs(const std::vector<DProductRep>& reps) {
     const i64 n = reps[0].n();
     const DTree& t = *reps[0].base.tree;
     for (const auto& r : reps)
-        if (r.C != reps[0].C || r.n() != n) throw std::invalid_argument("fisher_pairs: reps of different factorizations");
+        if (r.C != reps[0].C || r.n() != n) throw std::invalid_argument("fisher_corrections: reps of different factorizations");
     // cc[i + j p] = sum_f <Cv_i[<f]^T Cu_f, Cu[<f]^T Cv_j,f>, ss likewise over
     // the level-f columns themselves (product_rep.cpp:227-233: i <= j pairs
     // align by the finer level; the i = f term appears once, i < f twice for
@@ -312,10 +313,73 @@ std::vector<double> fisher_pairs(const std::vector<DProductRep>& reps) {
                 if (i <= j) seg_dot(1, 0, G1s[i].get(), 0, G2s[j].get(), 0, ls, ss.get() + i + j * p, true);
             }
     }
-    const std::vector<double> c = cc.download(), q = ss.download();
+    // Cross terms (product_rep.cpp:212-224) of every pair: for base a and the
+    // corrections of rep b, tr(Cv_b^T h_a Cu) with the shared Cu. The leaf
+    // product Leaves_a Cu is formed once per base and dotted with every Cv_b;
+    // the projections V_l^T Cu once per base, U_l^T Cv_b per (a, b). A pair
+    // (i, j), i < j, takes cross(base i, rep j) + cross(base j, rep i); (i, i)
+    // takes 2 cross(base i, rep i) (trace_pair's mirrored-term rule).
+    DVec xc(p * p);
+    xc.zero();
+    const int sumC = reps[0].sumC;
+    const DProductRep& r0 = reps[0];
+    for (size_t a = 0; a < p; ++a) {
+        const DHodlr& h = reps[a].base;
+        auto slot = [&](size_t b) { return xc.get() + a + b * p; };  // cross(base a, rep b)
+        if (!h.leaves_zero) {
+            std::vector<const double*> zs;
+            std::vector<double> al;
+            std::vector<double*> os;
+            for (size_t b = 0; b < p; ++b) {
+                zs.push_back(reps[b].Cv->get());
+                al.push_back(1.0);
+                os.push_back(slot(b));
+            }
+            leaf_mm_dot_multi(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), r0.Cu->get(), n, zs, n, sumC, al,
+                              os, true);
+        }
+        std::vector<int> W(static_cast<size_t>(tau), 0);
+        bool any_thin = false;
+        for (int l = 1; l <= tau; ++l) {
+            const int R = h.Rl(l);
+            const int w = r0.coff[static_cast<size_t>(l - 1)] + r0.C[static_cast<size_t>(l - 1)];
+            if (R > 0 && R <= 16 && w > 0) {
+                W[static_cast<size_t>(l - 1)] = w;
+                any_thin = true;
+            }
+        }
+        if (any_thin) {
+            auto Q = hodlr_project(h, r0.Cu->get(), n, sumC, false, W);
+            for (size_t b = 0; b < p; ++b) {
+                auto Pp = hodlr_project(h, reps[b].Cv->get(), n, sumC, true, W);
+                for (int l = 1; l <= tau; ++l) {
+                    const int R = h.Rl(l), w = W[static_cast<size_t>(l - 1)];
+                    if (!R || !w) continue;
+                    seg_xor_dot(t.part(l).nseg(), 1, Pp[static_cast<size_t>(l - 1)]->get(),
+                                Q[static_cast<size_t>(l - 1)]->get(), i64(R) * sumC, R, R, w, slot(b), true);
+                }
+            }
+        }
+        for (int l = 1; l <= tau; ++l) {
+            const int R = h.Rl(l);
+            const int Wl = r0.coff[static_cast<size_t>(l - 1)] + r0.C[static_cast<size_t>(l - 1)];
+            if (!R || !Wl || W[static_cast<size_t>(l - 1)]) continue;
+            const Partition& pl = t.part(l);
+            const size_t sz = static_cast<size_t>(pl.nseg()) * static_cast<size_t>(R) * static_cast<size_t>(Wl);
+            DVec Q(sz);
+            seg_tn(pl, h.Vl(l), n, R, r0.Cu->get(), n, Wl, Q.get(), i64(R) * Wl, R);
+            for (size_t b = 0; b < p; ++b) {
+                DVec Pp(sz);
+                seg_tn(pl, h.Ul(l), n, R, reps[b].Cv->get(), n, Wl, Pp.get(), i64(R) * Wl, R);
+                seg_xor_dot(pl.nseg(), 1, Pp.get(), Q.get(), i64(R) * Wl, R, R, Wl, slot(b), true);
+            }
+        }
+    }
+    const std::vector<double> c = cc.download(), q = ss.download(), x = xc.download();
     for (size_t i = 0; i < p; ++i)
         for (size_t j = i; j < p; ++j)
-            out[i + j * p] = i == j ? 2.0 * c[i + i * p] + q[i + i * p] : c[i + j * p] + q[i + j * p] + c[j + i * p];
+            out[i + j * p] = i == j ? 2.0 * c[i + i * p] + q[i + i * p] + 2.0 * x[i + i * p]
+                                    : c[i + j * p] + q[i + j * p] + c[j + i * p] + x[i + j * p] + x[j + i * p];
     return out;
 }
 

@@ -34,16 +34,17 @@ std::vector<DProductRep> pipeline_multi(const DFactor& f, const std::vector<cons
 
 /// out (+)= trace_product_rep (product_rep.cpp:188-194).
 void trace_product_rep(const DProductRep& p, double* out, bool accumulate);
-/// out (+)= trace_pair (product_rep.cpp:204-235). with_pairs = false leaves
-/// out the correction-pair terms (:227-233), for fisher_pairs.
-void trace_pair(const DProductRep& p, const DProductRep& q, double* out, bool accumulate, bool with_pairs = true);
-/// The correction-pair terms of trace_pair for every i <= j of p
-/// solve_multiply reps of ONE factorization: their Cu panels are the same
-/// (p = -v cap^-T and the factor levels' updates depend on the factorization
-/// only), so the Grams Cv_i^T Cu_f and Cu^T Cv_j,f each rep needs are formed
-/// once per rep and shared by every pair. Returns, per (i, j) column-major,
-/// the terms to add to trace_pair(reps[i], reps[j], .., with_pairs = false).
-std::vector<double> fisher_pairs(const std::vector<DProductRep>& reps);
+/// out (+)= trace_pair (product_rep.cpp:204-235). with_corr = false keeps
+/// only the base-base trace (:206-210), for fisher_corrections.
+void trace_pair(const DProductRep& p, const DProductRep& q, double* out, bool accumulate, bool with_corr = true);
+/// The correction terms of trace_pair — cross terms (:212-224) and
+/// correction pairs (:227-233) — for every i <= j of p solve_multiply reps of
+/// ONE factorization (pipeline_multi). Their Cu panel is shared, so every
+/// product that involves only a base and Cu (leaf products, V_l^T Cu, the
+/// Grams Cu^T Cv_f and Cv^T Cu_f) is formed once and reused by every pair.
+/// Returns, per (i, j) column-major, the terms to add to
+/// trace_pair(reps[i], reps[j], .., with_corr = false).
+std::vector<double> fisher_corrections(const std::vector<DProductRep>& reps);
 
 /// Dense assembly on the host (test support; n <= 2^14).
 std::vector<double> prodrep_densify(const DProductRep& p);
