@@ -694,10 +694,10 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
     }
 }
 
-constexpr int COMPLETE_BATCH_ROWS = 8192;
+constexpr int COMPLETE_BATCH_ROWS = 0;  // every deficient block takes the batched CholeskyQR path first
 
 /// sketch.cpp:60-74 for every node of a level whose numeric rank is below k.
-/// Short blocks run the sequential loop one CTA per node (k_complete). Long
+/// Every deficient block (COMPLETE_BATCH_ROWS = 0) first takes the batched path; a node whose candidates fail the 0.5 test runs the sequential loop one CTA per node (k_complete). Long
 /// blocks project the canonical candidates e_0..e_{c-1} twice against the
 /// kept columns and orthonormalise them with a (TSQR) Householder QR: the
 /// sequential loop computes exactly this Q when every candidate passes the
