@@ -441,7 +441,11 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (x~U[0,1] sorted, y~N(0,I), B~N(0,I))",
                 "config": config(args.log2n, tau), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches, "stages": stages, "h_matvec": matvec,
-                "kernel_ledger": ledger, "results": results}
+                "kernel_ledger": ledger, "results": results,
+                "results_note": ("F[0][0] (sigma2, sigma2) = 1/2 tr((I - eta K^-1)^2) is a few hundred left after "
+                                 "cancelling traces of size n/2 at cond(K) ~ 1e11: in FP64 it carries no significant "
+                                 "digits at n = 2^20 (+-0.7% of n/2 even with dK/dsigma2 set to exactly H - eta I; "
+                                 "profiles/r2_c4_parity.md section 6); loglik, score and F[1][1] keep theirs")}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -13,6 +13,7 @@ import collections
 import csv
 import hashlib
 import json
+import re
 import os
 import sys
 
@@ -30,9 +31,10 @@ CLASSES = {
 
 
 def kernel_base(name):
-    k = name.replace("hg::(anonymous namespace)::", "").replace("(anonymous namespace)::", "")
-    k = k.replace("void ", "").replace("hg::", "").split("(")[0]
-    return k.split("<")[0].strip()
+    """'void unnamed>::k_seg_tn<80, 80>(unnamed>::SegTnArgs)' -> 'k_seg_tn' (every
+    kernel of the library is named k_*)."""
+    m = re.search(r"\b(k_[A-Za-z0-9_]+)", name)
+    return m.group(1) if m else name
 
 
 def klass(base):
