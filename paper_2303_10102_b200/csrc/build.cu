@@ -540,21 +540,37 @@ __global__ void k_svd_tins(int w, int rmax, const int* r, const double* US, cons
 /// (Omega skew). Only Z needs a QR (c' x (k + w2) instead of two c x
 /// (2k + w2) QRs); the core R_Z^T is truncated by a rank-revealing pivoted QR
 /// at rtol (SVD truncation in hodlr_matrix.cpp:56-60).
+void compress_level_pieces(DHodlr& D, int l, int k, int w, const double* Om, double rtol, const double* B,
+                           const double* T, double* Zw);
+
 void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double rtol) {
     const int W = D.Rl(l);
     if (W == 0) return;
     const int w = W - k;
+    const i64 n = D.tree->n();
+    double* P = D.Ul(l);
+    DVec Z(static_cast<size_t>(n) * w);
+    panel_axpby(n, w, 1.0, P + i64(k) * n, n, 0.0, Z.get(), n);
+    compress_level_pieces(D, l, k, w, Om, rtol, P + i64(k) * n, P, Z.get());
+}
+
+/// The recompression from the level's pieces instead of its assembled panel:
+/// B = [q | q2] (left-child rows, n x w), T = t (right-child rows, n x k), and
+/// Zw = [dt | dt2] (right-child rows, n x w), overwritten (Z = [dt - t Omega | dt2]
+/// is formed in place and factored there).
+void compress_level_pieces(DHodlr& D, int l, int k, int w, const double* Om, double rtol, const double* B,
+                           const double* T, double* Zw) {
     const DTree& t = *D.tree;
     const i64 n = t.n();
     const Partition& pc = t.part(l);
     const int nodes = 1 << (l - 1);
     const auto& hb = pc.hbounds();
     auto& ctx = current();
-    double* P = D.Ul(l);
-    DVec Z(static_cast<size_t>(n) * w);
-    panel_axpby(n, k, 1.0, P + i64(k) * n, n, 0.0, Z.get(), n);
-    seg_nn(pc, P, n, k, Om, i64(k) * k, k, TMap::parent(0, 0), Z.get(), n, k, -1.0, 1.0);
-    if (w > k) panel_axpby(n, w - k, 1.0, P + i64(2 * k) * n, n, 0.0, Z.get() + i64(k) * n, n);
+    struct ZView {
+        double* p;
+        double* get() const { return p; }
+    } Z{Zw};
+    seg_nn(pc, T, n, k, Om, i64(k) * k, k, TMap::parent(0, 0), Z.get(), n, k, -1.0, 1.0);
     std::vector<int> wmin(static_cast<size_t>(nodes));
     int zrows = 0;
     for (int j = 0; j < nodes; ++j) {
@@ -601,7 +617,7 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
             HG_LAUNCH();
             count_launch();
             // left' = [Q | q2] P R_Z[:r]^T on left-child rows
-            seg_nn(pc, P + i64(k) * n, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n,
+            seg_nn(pc, B, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n,
                    rmax, 1.0, 0.0);
             // right' = Q_Z[:, :r] on right-child rows
             std::vector<double*> out;
@@ -674,7 +690,7 @@ void compress_level_structured(DHodlr& D, int l, int k, const double* Om, double
         HG_LAUNCH();
         count_launch();
         // left' = [Q | q2] Q_M[:, :r] on left-child rows (odd rows are overwritten next)
-        seg_nn(pc, P + i64(k) * n, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n, rmax,
+        seg_nn(pc, B, n, w, Tin.get(), i64(2) * w * rmax, w, TMap::parent(0, 0), Pn->get(), n, rmax,
                1.0, 0.0);
         // right' = Q_Z P_M R_M[:r, :]^T on right-child rows
         std::vector<double*> out;
@@ -1186,9 +1202,23 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 HG_LAUNCH();
                 ++ctx.launches;
             }
+            DHodlr& D = out.deriv[static_cast<size_t>(q)];
+            if (at_level(q)) {
+                // HG_COMPRESS_AT_LEVEL: compress the level as it is committed,
+                // straight from its pieces (left basis [q | q2] = X2, t = Z,
+                // [dt | dt2] = O2 factored in place), so every finer level's
+                // peels stream the compressed (rank ~3..8) panels instead of
+                // the 2k + w2 wide concatenation, which is never assembled
+                for (int j = 0; j < nodes; ++j) {
+                    D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
+                    D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
+                }
+                compress_level_pieces(D, l, k, wq, omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(),
+                                      1e-13, X2.get(), Z, O2.get());
+                continue;
+            }
             // Derivative level panel: [dqc | q | q2] on left rows, [t | dt | dt2] on right rows.
             const int Wd = 2 * k + w2max;
-            DHodlr& D = out.deriv[static_cast<size_t>(q)];
             D.set_level(l, Wd, true);
             double* Pd = D.Ul(l);
             panel_parity_scale(pc, n, k, ds, n, 1.0, 0.0, Pd, n, 0.0);
@@ -1203,12 +1233,6 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
                 D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
             }
-            // HG_COMPRESS_AT_LEVEL: compress the level when it is committed, so
-            // every finer level's peels stream the compressed (rank ~3..8)
-            // panels instead of the 2k + w2 wide concatenation
-            if (at_level(q))
-                compress_level_structured(D, l, k, omegas[static_cast<size_t>(q)][static_cast<size_t>(l - 1)]->get(),
-                                          1e-13);
         }
         // Value level panel: q on left rows, t = Z on right rows.
         out.h.set_level(l, k, true);
