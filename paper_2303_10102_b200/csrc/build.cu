@@ -1042,8 +1042,17 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         dqmap.upload(qmap);
         DVec Rn(static_cast<size_t>(nodes) * k * k), sign(static_cast<size_t>(nodes) * k);
         DBuf<int> perm(static_cast<size_t>(nodes) * k), nr(static_cast<size_t>(nodes));
-        DVec S(static_cast<size_t>(n) * k);
-        S.zero();
+        // One panel per level, [ds_0 | .. | ds_{p-1} | q | q2]: the value
+        // peel reads [ds | q] and each derivative peel [q | q2] as contiguous
+        // column ranges of it (no copies). q and q2 start zero (their bases
+        // only fill left-child rows).
+        struct PView {
+            double* p;
+            double* get() const { return p; }
+        };
+        DVec SB(static_cast<size_t>(n) * static_cast<size_t>(k * (1 + p) + kp));
+        const PView S{SB.get() + i64(p) * k * n};
+        panel_axpby(n, k + kp, 0.0, nullptr, 0, 0.0, S.get(), n);
         {
             std::unique_ptr<BatchedQR> qr;
             if (!blocks.empty()) qr = std::make_unique<BatchedQR>(blocks, k, true);
@@ -1082,8 +1091,8 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         // S and dY (diff_qr, :245-268), not Z.
         std::vector<DVecP> oms(static_cast<size_t>(p));
         std::vector<std::vector<int>> rws(static_cast<size_t>(p));
-        DVec SX(static_cast<size_t>(n) * k * (1 + p)), ZX(static_cast<size_t>(n) * k * (1 + p));
-        panel_axpby(n, k, 1.0, S.get(), n, 0.0, SX.get(), n);
+        DVec ZX(static_cast<size_t>(n) * k * (1 + p));
+        double* SX = SB.get();  // [ds_0 | .. | ds_{p-1} | q]
         for (int q = 0; q < p; ++q) {
             DVec G(static_cast<size_t>(2 * nodes) * k * k);
             DVecP OmP = make_dvec(static_cast<size_t>(nodes) * k * k, false);
@@ -1095,24 +1104,25 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                                                    OmP->get(), rw.get(), ill.get());
             HG_LAUNCH();
             ++ctx.launches;
-            seg_nn(pc, S.get(), n, k, OmP->get(), i64(k) * k, k, TMap::parent(0, 0), SX.get() + i64(1 + q) * k * n, n,
+            seg_nn(pc, S.get(), n, k, OmP->get(), i64(k) * k, k, TMap::parent(0, 0), SX + i64(q) * k * n, n,
                    k, 1.0, 0.0);
             rws[static_cast<size_t>(q)] = rw.download();
             std::vector<int> ic = ill.download();
             for (int x : ic) out.warnings += x;
         }
-        peel(o, -1, out.h, l - 1, SX.get(), k * (1 + p), ZX.get(), 1);
-        const double* Z = ZX.get();
+        peel(o, -1, out.h, l - 1, SX, k * (1 + p), ZX.get(), 1);
+        const double* Z = ZX.get() + i64(p) * k * n;
 
         // q2 residual bases (sketch.cpp:194-233).
         std::vector<int> w2(static_cast<size_t>(nodes), 0);
         int w2max = 0;
-        DVec S2;
+        const PView S2{S.get() + i64(k) * n};
         DBuf<int> dw2(static_cast<size_t>(nodes));
         dw2.zero();
         if (p > 0) {
-            DVec resid(static_cast<size_t>(n) * kp), presc(static_cast<size_t>(nodes)), G(static_cast<size_t>(2 * nodes) * k * kp);
-            panel_axpby(n, kp, 1.0, dY.get(), n, 0.0, resid.get(), n);
+            // the residual is projected in place: dY's last use (diff_qr) is done
+            const PView resid{dY.get()};
+            DVec presc(static_cast<size_t>(nodes)), G(static_cast<size_t>(2 * nodes) * k * kp);
             {
                 const TileList& tl = pc.tiles(2048);
                 DVec part(static_cast<size_t>(tl.count) * p);
@@ -1152,8 +1162,6 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 for (int x : w2) w2max = std::max(w2max, x);
             }
             if (w2max > 0) {
-                S2.alloc(static_cast<size_t>(n) * w2max);
-                S2.zero();
                 std::vector<double*> qo;
                 std::vector<i64> ql;
                 for (int j = 0; j < nodes; ++j)
@@ -1188,14 +1196,13 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         // dZ_q = K_q S - D_q S + (K ds_q - H ds_q), dZ2_q = K_q q2 - D_q q2,
         // the D_q applies to [S | q2] in one peel.
         for (int q = 0; q < p; ++q) {
-            const double* ds = SX.get() + i64(1 + q) * k * n;
+            const double* ds = SX + i64(q) * k * n;
             const int wq = k + w2max;
-            DVec X2(static_cast<size_t>(n) * wq), O2(static_cast<size_t>(n) * wq);
-            panel_axpby(n, k, 1.0, S.get(), n, 0.0, X2.get(), n);
-            if (w2max > 0) panel_axpby(n, w2max, 1.0, S2.get(), n, 0.0, X2.get() + i64(k) * n, n);
+            const PView X2{S.get()};  // [q | q2]
+            DVec O2(static_cast<size_t>(n) * wq);
             peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, X2.get(), wq, O2.get(), 1);
             double* dZ = O2.get();
-            panel_axpby(n, k, 1.0, ZX.get() + i64(1 + q) * k * n, n, 1.0, dZ, n);
+            panel_axpby(n, k, 1.0, ZX.get() + i64(q) * k * n, n, 1.0, dZ, n);
             double* dZ2 = O2.get() + i64(k) * n;
             if (w2max > 0) {
                 k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 1, dw2.get(), w2max, dZ2, n);
