@@ -807,7 +807,10 @@ void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double*
 /// zparity: X is zero on the level-(lmax+1) children of that parity (0: the
 /// sketch R_l lives on right children, 1: the bases S, ds, S2 on left ones);
 /// -1: no structure (leaf sampler).
-void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y, int zparity) {
+/// The oracle half of a peel (Y = K_j X under the sampler's zero-row hint);
+/// returns the hint the H half uses.
+ZeroRows peel_oracle(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y,
+                     int zparity) {
     const i64 n = H.n();
     ZeroRows z;
     if (zparity >= 0 && lmax + 1 <= H.tau()) {
@@ -818,7 +821,35 @@ void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, i
         o.apply(j, X, n, s, Y, n);
         z.leaf_identity = zparity == -1 && s == H.bmax();  // the leaf sampler
     }
-    hodlr_apply(H, X, n, s, Y, n, 1, lmax, true, false, 1.0, -1.0, z);
+    return z;
+}
+
+void peel(const DOracle& o, int j, const DHodlr& H, int lmax, const double* X, int s, double* Y, int zparity) {
+    const ZeroRows z = peel_oracle(o, j, H, lmax, X, s, Y, zparity);
+    hodlr_apply(H, X, H.n(), s, Y, H.n(), 1, lmax, true, false, 1.0, -1.0, z);
+}
+
+/// Peels of one sampler X for the value and every derivative. A derivative
+/// that is an affine function of the value, dK/dtheta_q = a K + b I (sigma2
+/// of a covariance sigma2 C + nugget I: a = 1/sigma2, b = -nugget/sigma2;
+/// DOracle::affine_derivative), is formed from the value apply instead of a
+/// second forward-model evaluation of the same columns.
+void peel_all(const DOracle& o, const DHodlr& H, const std::vector<DHodlr>& D, int lmax, const double* X, int s,
+              double* Yh, const std::vector<double*>& Yd, int zparity) {
+    const i64 n = H.n();
+    const ZeroRows z = peel_oracle(o, -1, H, lmax, X, s, Yh, zparity);
+    for (size_t q = 0; q < D.size(); ++q) {
+        double a = 0.0, b = 0.0;
+        if (o.affine_derivative(int(q), &a, &b)) {
+            panel_axpby(n, s, a, Yh, n, 0.0, Yd[q], n);
+            if (b != 0.0) panel_axpby(n, s, b, X, n, 1.0, Yd[q], n);
+            o.count_derivative_columns(s);
+            hodlr_apply(D[q], X, n, s, Yd[q], n, 1, lmax, true, false, 1.0, -1.0, z);
+        } else {
+            peel(o, int(q), D[q], lmax, X, s, Yd[q], zparity);
+        }
+    }
+    hodlr_apply(H, X, n, s, Yh, n, 1, lmax, true, false, 1.0, -1.0, z);
 }
 
 /// diff_qr core (sketch.cpp:78-111) on one k x k problem: Y = G R^-1 (row
@@ -1021,8 +1052,11 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         const double* Rs = plan.level[static_cast<size_t>(l - 1)]->get();
         // Pass 1: Y = K R - H R, dY_j = K_j R - D_j R (sketch.cpp:151-154).
         DVec Y(static_cast<size_t>(n) * k), dY(static_cast<size_t>(n) * std::max(kp, 1));
-        peel(o, -1, out.h, l - 1, Rs, k, Y.get(), 0);
-        for (int q = 0; q < p; ++q) peel(o, q, out.deriv[static_cast<size_t>(q)], l - 1, Rs, k, dY.get() + i64(q) * k * n, 0);
+        {
+            std::vector<double*> yd;
+            for (int q = 0; q < p; ++q) yd.push_back(dY.get() + i64(q) * k * n);
+            peel_all(o, out.h, out.deriv, l - 1, Rs, k, Y.get(), yd, 0);
+        }
         // Range finder per node (sketch.cpp:156-175).
         std::vector<int> qmap(static_cast<size_t>(nodes), -1);
         std::vector<BatchedQR::Block> blocks;
@@ -1260,17 +1294,16 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
     // Leaves (sketch.cpp:314-329): identity-concatenation sampler.
     {
         const int bm = tree->bmax;
-        DVec Yl(static_cast<size_t>(n) * bm);
-        peel(o, -1, out.h, tau, plan.leaf->get(), bm, Yl.get(), -1);
+        DVec Yl(static_cast<size_t>(n) * bm * (1 + p));
+        std::vector<double*> yd;
+        for (int q = 0; q < p; ++q) yd.push_back(Yl.get() + i64(1 + q) * bm * n);
+        peel_all(o, out.h, out.deriv, tau, plan.leaf->get(), bm, Yl.get(), yd, -1);
         auto to_leaves = [&](DHodlr& h, double* P) {
             leaves_panel(*tree, h.leaves->get(), P, false);
             h.leaves_zero = false;
         };
         to_leaves(out.h, Yl.get());
-        for (int q = 0; q < p; ++q) {
-            peel(o, q, out.deriv[static_cast<size_t>(q)], tau, plan.leaf->get(), bm, Yl.get(), -1);
-            to_leaves(out.deriv[static_cast<size_t>(q)], Yl.get());
-        }
+        for (int q = 0; q < p; ++q) to_leaves(out.deriv[static_cast<size_t>(q)], yd[static_cast<size_t>(q)]);
     }
     // Recompress every derivative off-diagonal block (sketch.cpp:331-341).
     for (int q = 0; q < p; ++q)

@@ -136,6 +136,13 @@ public:
         sigma2_ = th[0];
         ell_ = th[1];
     }
+    /// K = sigma2 k_nu(d / ell) + nugget I, so dK/dsigma2 = (K - nugget I) / sigma2.
+    bool affine_derivative(int j, double* a, double* b) const override {
+        if (j != 0 || sigma2_ == 0.0) return false;
+        *a = 1.0 / sigma2_;
+        *b = -nugget_ / sigma2_;
+        return true;
+    }
 
 protected:
     void do_apply(int j, const double* V, i64 ldv, int s, double* Y, i64 ldy) const override {

@@ -30,6 +30,16 @@ public:
         (j < 0 ? apply_cols_ : deriv_cols_).fetch_add(std::uint64_t(s), std::memory_order_relaxed);
         do_apply_masked(j, V, ldv, s, Y, ldy, z);
     }
+    /// dK/dtheta_j = a K + b I exactly (e.g. sigma2 of sigma2 C + nugget I):
+    /// callers may form that derivative's applies from value applies of the
+    /// same columns. Default: no such relation.
+    virtual bool affine_derivative(int j, double* a, double* b) const {
+        (void)j, (void)a, (void)b;
+        return false;
+    }
+    /// A derivative apply formed that way still counts as one (the column
+    /// counters keep the reference's meaning, oracle.hpp:37-45).
+    void count_derivative_columns(int s) const { deriv_cols_.fetch_add(std::uint64_t(s), std::memory_order_relaxed); }
     std::uint64_t apply_columns() const { return apply_cols_.load(); }
     std::uint64_t derivative_columns() const { return deriv_cols_.load(); }
     void reset_counters() const {
