@@ -303,6 +303,58 @@ __global__ void __launch_bounds__(THREADS) k_leaf_mm_dot(LeafMmArgs g, DotZ zs, 
     }
 }
 
+/// Per-leaf Grams M_z,b = A_z[b] B[b]^T (A_z, B: n x K, rows of leaf b, K
+/// contracted) dotted with every leaf array L_a: sum_b <L_a,b, M_z,b> =
+/// tr(A_z^T L_a B). One CTA per (leaf, 64-row tile, 64-column tile); the
+/// partial of (z, a) at partial[(z * nl + a) * nblocks + block].
+struct LeafGramArgs {
+    const int* bounds;
+    int rt;
+    const double* A[LEAF_DOT_MAXZ];
+    int na;
+    const double* B;
+    i64 ld;
+    int K;
+    const double* L[LEAF_DOT_MAXZ];
+    int nl;
+    i64 lstride;
+    int ldl;
+};
+
+__global__ void __launch_bounds__(THREADS) k_leaf_gram_dot(const __grid_constant__ LeafGramArgs g, double* partial) {
+    extern __shared__ double smem[];
+    const int blk = blockIdx.x, rt2 = g.rt * g.rt;
+    const int b = blk / rt2, rc = blk % rt2, r0 = (rc / g.rt) * BM, c0 = (rc % g.rt) * BM;
+    const int lo = g.bounds[b], m = g.bounds[b + 1] - lo;
+    double part[LEAF_DOT_MAXZ][LEAF_DOT_MAXZ] = {};
+    if (r0 < m && c0 < m) {
+        for (int z = 0; z < g.na; ++z) {
+            tile::LoadMCT<BM> la{g.A[z] + lo + r0, g.ld, m - r0, g.K};
+            tile::LoadMCT<BM> lb{g.B + lo + c0, g.ld, m - c0, g.K};
+            typename tile::Shape<BM, BM>::Acc acc;
+            acc.zero();
+            tile::run_t<NS_SHORT, BM, BM>(la, lb, cdiv_d(g.K, BK), smem, acc);
+            __syncthreads();  // stages free before the next z refills them
+            tile::for_each_slot<BM, BM>(acc, [&](double& v, int mi0, int ni) {
+                const int r = r0 + mi0, c = c0 + ni;
+                if (r < m && c < m)
+#pragma unroll
+                    for (int a = 0; a < LEAF_DOT_MAXZ; ++a)
+                        if (a < g.nl) part[z][a] = fma(v, g.L[a][i64(b) * g.lstride + r + i64(c) * g.ldl], part[z][a]);
+            });
+        }
+    }
+    const i64 nb = gridDim.x;
+#pragma unroll
+    for (int z = 0; z < LEAF_DOT_MAXZ; ++z)
+#pragma unroll
+        for (int a = 0; a < LEAF_DOT_MAXZ; ++a) {
+            if (z >= g.na || a >= g.nl) continue;
+            const double sv = block_sum(part[z][a]);
+            if (threadIdx.x == 0) partial[i64(z * g.nl + a) * nb + blk] = sv;
+        }
+}
+
 // ------------------------------------------------------------ elementwise
 /// Y = alpha X + beta Y; grid (row blocks, column groups), no 64-bit div/mod.
 __global__ void k_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy) {
@@ -635,6 +687,49 @@ void leaf_mm_dot_multi(const Partition& leaves, const double* L, i64 lstride, in
                 ++c.launches;
             }
         });
+    }
+}
+
+void leaf_gram_dot(const Partition& leaves, const std::vector<const double*>& As, const double* B, i64 ld, int K,
+                   const std::vector<const double*>& Ls, i64 lstride, int ldl, const std::vector<double*>& outs,
+                   bool accumulate) {
+    const int na = int(As.size()), nl = int(Ls.size());
+    if (na > LEAF_DOT_MAXZ || nl > LEAF_DOT_MAXZ) throw std::length_error("leaf_gram_dot: too many operands");
+    if (na == 0 || nl == 0) return;
+    if (K <= 0) {
+        if (!accumulate)
+            for (double* o : outs) HG_CUDA(cudaMemsetAsync(o, 0, sizeof(double), current().stream));
+        return;
+    }
+    auto& c = current();
+    const int rt = cdiv(leaves.max_seg(), BM);
+    const double rows = double(leaves.hbounds().back()), bm = double(leaves.max_seg());
+    ProfScope prof(PROF_LEAF_MM, 2.0 * na * rows * bm * K, 8.0 * ((na + 1.0) * rows * K + nl * na * rows * bm));
+    if (prof_enabled()) prof.key(prof_tag("leafgram K=%d z=%d l=%d", K, na, nl));
+    LeafGramArgs g{};
+    g.bounds = leaves.dbounds();
+    g.rt = rt;
+    for (int z = 0; z < na; ++z) g.A[z] = As[static_cast<size_t>(z)];
+    g.na = na;
+    g.B = B;
+    g.ld = ld;
+    g.K = K;
+    for (int a = 0; a < nl; ++a) g.L[a] = Ls[static_cast<size_t>(a)];
+    g.nl = nl;
+    g.lstride = lstride;
+    g.ldl = ldl;
+    constexpr int bytes = tile::smem_bytes_t(NS_SHORT, BM, BM);
+    const unsigned grid = unsigned(leaves.nseg() * rt * rt);
+    DVec partial(static_cast<size_t>(grid) * static_cast<size_t>(na * nl));
+    attr_once<k_leaf_gram_dot>(bytes);
+    k_leaf_gram_dot<<<grid, THREADS, bytes, c.stream>>>(g, partial.get());
+    HG_LAUNCH();
+    ++c.launches;
+    for (int e = 0; e < na * nl; ++e) {
+        k_reduce_final<<<1, 256, 0, c.stream>>>(partial.get() + i64(e) * grid, int(grid), outs[static_cast<size_t>(e)],
+                                                accumulate ? 1 : 0);
+        HG_LAUNCH();
+        ++c.launches;
     }
 }
 

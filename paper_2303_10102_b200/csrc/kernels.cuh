@@ -58,6 +58,12 @@ void leaf_mm_dot(const Partition& leaves, const double* L, i64 lstride, int ldl,
 /// outs[z] (+)= alphas[z] sum((L_b X) .* Zs[z]) for several Z with ONE leaf
 /// product (the cross terms of every Fisher pair with the same base).
 constexpr int LEAF_DOT_MAXZ = 4;
+/// outs[z * nl + a] (+)= tr(As[z]^T L_a B) over the leaves, L_a = Ls[a] (leaf
+/// arrays, stride lstride, ld ldl), As[z], B n x K (ld ld): per-leaf Grams
+/// As[z][b] B[b]^T formed once and dotted with every L_a.
+void leaf_gram_dot(const Partition& leaves, const std::vector<const double*>& As, const double* B, i64 ld, int K,
+                   const std::vector<const double*>& Ls, i64 lstride, int ldl, const std::vector<double*>& outs,
+                   bool accumulate);
 void leaf_mm_dot_multi(const Partition& leaves, const double* L, i64 lstride, int ldl, const double* X, i64 ldx,
                        const std::vector<const double*>& Zs, i64 ldz, int w, const std::vector<double>& alphas,
                        const std::vector<double*>& outs, bool accumulate);

@@ -323,21 +323,39 @@ std::vector<double> fisher_corrections(const std::vector<DProductRep>& reps) {
     xc.zero();
     const int sumC = reps[0].sumC;
     const DProductRep& r0 = reps[0];
+    {  // leaf parts: tr(Cv_b^T Leaves_a Cu) = sum_leaves <Leaves_a, Cv_b Cu^T>; the per-leaf
+       // Grams Cv_b Cu^T (K = sumC) are formed once per b and dotted with every base's leaves
+        std::vector<const double*> As, Ls;
+        std::vector<size_t> la;
+        for (size_t b = 0; b < p; ++b) As.push_back(reps[b].Cv->get());
+        for (size_t a = 0; a < p; ++a)
+            if (!reps[a].base.leaves_zero) {
+                Ls.push_back(reps[a].base.leaves->get());
+                la.push_back(a);
+            }
+        if (!Ls.empty() && p <= size_t(LEAF_DOT_MAXZ)) {
+            std::vector<double*> os;
+            for (size_t b = 0; b < p; ++b)
+                for (size_t ia = 0; ia < la.size(); ++ia) os.push_back(xc.get() + la[ia] + b * p);
+            leaf_gram_dot(t.leaves(), As, r0.Cu->get(), n, sumC, Ls, r0.base.lstride(), r0.base.bmax(), os, true);
+        } else {
+            for (size_t a : la) {
+                std::vector<const double*> zs;
+                std::vector<double> al;
+                std::vector<double*> os;
+                for (size_t b = 0; b < p; ++b) {
+                    zs.push_back(reps[b].Cv->get());
+                    al.push_back(1.0);
+                    os.push_back(xc.get() + a + b * p);
+                }
+                leaf_mm_dot_multi(t.leaves(), reps[a].base.leaves->get(), reps[a].base.lstride(), reps[a].base.bmax(),
+                                  r0.Cu->get(), n, zs, n, sumC, al, os, true);
+            }
+        }
+    }
     for (size_t a = 0; a < p; ++a) {
         const DHodlr& h = reps[a].base;
         auto slot = [&](size_t b) { return xc.get() + a + b * p; };  // cross(base a, rep b)
-        if (!h.leaves_zero) {
-            std::vector<const double*> zs;
-            std::vector<double> al;
-            std::vector<double*> os;
-            for (size_t b = 0; b < p; ++b) {
-                zs.push_back(reps[b].Cv->get());
-                al.push_back(1.0);
-                os.push_back(slot(b));
-            }
-            leaf_mm_dot_multi(t.leaves(), h.leaves->get(), h.lstride(), h.bmax(), r0.Cu->get(), n, zs, n, sumC, al,
-                              os, true);
-        }
         std::vector<int> W(static_cast<size_t>(tau), 0);
         bool any_thin = false;
         for (int l = 1; l <= tau; ++l) {
