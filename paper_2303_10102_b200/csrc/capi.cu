@@ -565,9 +565,9 @@ hg_status hg_score(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, 
 
 hg_status hg_fisher_information(hg_ctx_t ctx, hg_factor_t f, const hg_hodlr_t* deriv, int p, double* out) {
     return guard(ctx, [&] {
-        std::vector<DProductRep> reps;
-        for (int j = 0; j < p; ++j) reps.push_back(pipeline(f->f, deriv[j]->h, true));
-        auto fi = fisher_from_reps(reps);
+        std::vector<const DHodlr*> d;
+        for (int j = 0; j < p; ++j) d.push_back(&deriv[j]->h);
+        auto fi = fisher_from_reps(pipeline_multi(f->f, d, true));
         for (size_t i = 0; i < fi.size(); ++i) out[i] = fi[i];
     });
 }
