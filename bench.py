@@ -276,7 +276,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2303_10102_b200 import hodlrgp as H
 
-    stream = torch.cuda.current_stream()
+    # one non-default stream shared by torch and the library: torch's default is
+    # the legacy NULL stream, for which hg_ctx_create would make its own stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = H.Context(local, stream.cuda_stream)
     n, x, y, B = workload(args.log2n)
     tau = H.tree_depth(n, LEAF, 2 * LEAF)

@@ -277,6 +277,32 @@ hg_status hg_mle_evaluate(hg_ctx_t ctx, hg_oracle_t o, int tau, int64_t k, uint6
                           const double* B, int64_t nrhs, double* X, int loc, double* loglik, double* score,
                           double* fisher, double* times);
 
+/* ------------------------------------ strong admissibility
+ * Not in the reference (weak HODLR only): an eta-admissible
+ * H-matrix over the KD block-cluster tree of the nside x nside periodic grid
+ * (BASELINE.json configs 3 and 5). order[i] = grid index of row i (a KD
+ * order, e.g. build_kd_ordering of the grid); the cluster tree is the uniform
+ * ClusterTree(nside^2, tau) over it. A pair of one depth is admissible when
+ * min(diam) <= eta * dist on the torus and both sides exceed k rows: rank-k
+ * block U V^T; inadmissible leaf pairs are dense; symmetric (t <= s stored).
+ * hg_hstrong_plan: host only, the block counts and storage of that tree.
+ * hg_hstrong_build: the oracle must be translation invariant on the grid (it
+ *   is probed with two unit vectors; HG_EINVAL otherwise), param = -1 -> K,
+ *   j -> dK/dtheta_j; blocks compressed by a batched randomized range finder
+ *   (width k, power_iters subspace iterations, Gaussian sketch from seed) on
+ *   entries generated from the probed column (matrix-free).
+ * hg_hstrong_trace_product: tr(A B) of two symmetric matrices of one plan. */
+typedef struct hg_hstrong_s* hg_hstrong_t;
+hg_status hg_hstrong_plan(const int64_t* order, int nside, int tau, double eta, int64_t k, int64_t* n_lowrank,
+                          int64_t* n_dense, int64_t* lowrank_entries, int64_t* dense_entries, int64_t* stored_doubles);
+hg_status hg_hstrong_build(hg_ctx_t ctx, hg_oracle_t o, int param, const int64_t* order, int nside, int tau,
+                           double eta, int64_t k, int power_iters, uint64_t seed, hg_hstrong_t* out);
+hg_status hg_hstrong_free(hg_hstrong_t h);
+hg_status hg_hstrong_matvec(hg_ctx_t ctx, hg_hstrong_t h, const double* X, int64_t ldx, int64_t s, double* Y,
+                            int64_t ldy, int loc);
+hg_status hg_hstrong_trace_product(hg_ctx_t ctx, hg_hstrong_t a, hg_hstrong_t b, double* out);
+hg_status hg_hstrong_blocks(hg_hstrong_t h, int64_t* n_lowrank, int64_t* n_dense, int64_t* bytes);
+
 /* ---------------------------------------------------- kernel-level ledger */
 /* Per kernel class (seg_tn, seg_nn, leaf_mm, leaf_solve, leaf_factor, cap_lu,
  * cap_solve, qr, form_q, oracle, reduce, other, hmatvec): device ms from CUDA events

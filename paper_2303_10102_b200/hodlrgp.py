@@ -31,6 +31,12 @@ COMPRESS_PIVOTED_QR, COMPRESS_JACOBI_SVD = 0, 1
 
 _SIGS = {
     "hg_last_error": (C.c_char_p, []),
+    "hg_hstrong_plan": (C.c_int, [vp, C.c_int, C.c_int, dbl, i64, lp, lp, lp, lp, lp]),
+    "hg_hstrong_build": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, C.c_int, dbl, i64, C.c_int, u64, C.POINTER(vp)]),
+    "hg_hstrong_free": (C.c_int, [vp]),
+    "hg_hstrong_matvec": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, C.c_int]),
+    "hg_hstrong_trace_product": (C.c_int, [vp, vp, vp, dp]),
+    "hg_hstrong_blocks": (C.c_int, [vp, lp, lp, lp]),
     "hg_ctx_create": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
     "hg_ctx_destroy": (C.c_int, [vp]),
     "hg_ctx_synchronize": (C.c_int, [vp]),
@@ -247,9 +253,11 @@ def _ptr_ld(x):
     # torch tensor on the device: column-major view required (stride(0) == 1)
     if x.dim() == 1:
         return x.data_ptr(), x.shape[0], x.shape[0], 1, DEVICE, x
-    if x.stride(0) != 1:
+    if x.stride(0) != 1 and x.shape[0] > 1:
         raise ValueError("device tensors must be column-major (use t.T.contiguous().T)")
-    return x.data_ptr(), x.stride(1), x.shape[0], x.shape[1], DEVICE, x
+    # a single column's stride is arbitrary in torch (size-1 dims): ld = rows
+    ld = x.shape[0] if x.shape[1] == 1 else x.stride(1)
+    return x.data_ptr(), ld, x.shape[0], x.shape[1], DEVICE, x
 
 
 # ------------------------------------------------------------------ tree
@@ -593,6 +601,13 @@ class CovarianceOracle:
         _check(lib().hg_oracle_set_parameters(self.ptr, _d(th), len(th)))
 
     def apply(self, v, j=-1):
+        if not isinstance(v, np.ndarray) and hasattr(v, "data_ptr"):  # column-major CUDA tensor
+            px, ldx, rows, cols, loc, keep = _ptr_ld(v)
+            import torch
+
+            y = torch.empty((cols, rows), dtype=torch.float64, device=v.device).T
+            _check(lib().hg_oracle_apply(self.ctx.ptr, self.ptr, j, px, ldx, cols, y.data_ptr(), y.stride(1), DEVICE))
+            return y if v.dim() > 1 else y[:, 0]
         vv = _f(v).reshape(self.n, -1, order="F")
         y = np.zeros_like(vv, order="F")
         _check(lib().hg_oracle_apply(self.ctx.ptr, self.ptr, j, vv.ctypes.data, self.n, vv.shape[1], y.ctypes.data,
@@ -709,6 +724,69 @@ def grid_kd_order(nside, leaf):
     coords = np.stack([(ix + 0.5) / nside, (iy + 0.5) / nside], axis=1)
     _, inv, _ = build_kd_ordering(coords, 1, 2)
     return inv, ClusterTree(n, tree_depth(n, leaf, 2 * leaf))
+
+
+# ------------------------------------------------ strong admissibility (§8f #2)
+def hstrong_plan(order, nside, tau, eta=1.0, k=42):
+    """Block-cluster tree of the eta-admissible H-matrix of the periodic grid
+    (host only): counts of rank-k and dense blocks, entries each covers, and
+    the doubles stored (hg_hstrong_plan). Not in the reference (weak HODLR
+    only, SPEC.md:70,90-96)."""
+    order = np.ascontiguousarray(order, dtype=np.int64)
+    out = [C.c_int64() for _ in range(5)]
+    _check(lib().hg_hstrong_plan(order.ctypes.data, int(nside), int(tau), float(eta), int(k),
+                                 *[C.byref(o) for o in out]))
+    keys = ("n_lowrank", "n_dense", "lowrank_entries", "dense_entries", "stored_doubles")
+    return {kk: int(o.value) for kk, o in zip(keys, out)}
+
+
+class HStrongMatrix:
+    """Strong-admissibility (eta) H-matrix of a grid-stationary covariance
+    (BASELINE.json configs 3 and 5): rank-k far-field blocks from a batched
+    randomized range finder on entries generated from one probed column of the
+    oracle, dense near-field leaf blocks. param = -1 builds K, j >= 0 dK/dtheta_j."""
+
+    def __init__(self, oracle, order, nside, tau, k, eta=1.0, param=-1, power_iters=0, seed=7):
+        self.ctx = oracle.ctx
+        self.n = int(nside) ** 2
+        order = np.ascontiguousarray(order, dtype=np.int64)
+        h = vp()
+        _check(lib().hg_hstrong_build(self.ctx.ptr, oracle.ptr, int(param), order.ctypes.data, int(nside), int(tau),
+                                      float(eta), int(k), int(power_iters), int(seed), C.byref(h)))
+        self.ptr = h
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hg_hstrong_free(self.ptr)
+            self.ptr = None
+
+    @property
+    def blocks(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().hg_hstrong_blocks(self.ptr, C.byref(a), C.byref(b), C.byref(c)))
+        return {"n_lowrank": a.value, "n_dense": b.value, "bytes": c.value}
+
+    def matvec(self, x):
+        """y = H x (numpy in -> numpy out; column-major CUDA tensor in -> CUDA tensor out)."""
+        vec = getattr(x, "ndim", None) == 1
+        if isinstance(x, np.ndarray):
+            xx = _f(x).reshape(x.shape[0], -1, order="F")
+            y = np.zeros_like(xx, order="F")
+            _check(lib().hg_hstrong_matvec(self.ctx.ptr, self.ptr, xx.ctypes.data, xx.shape[0], xx.shape[1],
+                                           y.ctypes.data, y.shape[0], HOST))
+            return y[:, 0] if vec else y
+        px, ldx, rows, cols, loc, keep = _ptr_ld(x)
+        import torch
+
+        y = torch.empty((cols, rows), dtype=torch.float64, device=x.device).T
+        _check(lib().hg_hstrong_matvec(self.ctx.ptr, self.ptr, px, ldx, cols, y.data_ptr(), y.stride(1), DEVICE))
+        return y
+
+    def trace_product(self, other):
+        """tr(A B) for two symmetric matrices of one block-cluster tree."""
+        out = C.c_double()
+        _check(lib().hg_hstrong_trace_product(self.ctx.ptr, self.ptr, other.ptr, C.byref(out)))
+        return out.value
 
 
 # ---------------------------------------------------------------- fit
