@@ -1262,14 +1262,9 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             const int Wd = 2 * k + w2max;
             D.set_level(l, Wd, true);
             double* Pd = D.Ul(l);
-            panel_parity_scale(pc, n, k, ds, n, 1.0, 0.0, Pd, n, 0.0);
-            panel_parity_scale(pc, n, k, Z, n, 0.0, 1.0, Pd, n, 1.0);
-            panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, Pd + i64(k) * n, n, 0.0);
-            panel_parity_scale(pc, n, k, dZ, n, 0.0, 1.0, Pd + i64(k) * n, n, 1.0);
-            if (w2max > 0) {
-                panel_parity_scale(pc, n, w2max, S2.get(), n, 1.0, 0.0, Pd + i64(2 * k) * n, n, 0.0);
-                panel_parity_scale(pc, n, w2max, dZ2, n, 0.0, 1.0, Pd + i64(2 * k) * n, n, 1.0);
-            }
+            panel_parity_select(pc, k, ds, n, 1.0, Z, n, 1.0, Pd, n);
+            panel_parity_select(pc, k, S.get(), n, 1.0, dZ, n, 1.0, Pd + i64(k) * n, n);
+            if (w2max > 0) panel_parity_select(pc, w2max, S2.get(), n, 1.0, dZ2, n, 1.0, Pd + i64(2 * k) * n, n);
             for (int j = 0; j < nodes; ++j) {
                 D.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
                 D.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = 2 * k + w2[static_cast<size_t>(j)];
@@ -1277,8 +1272,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
         }
         // Value level panel: q on left rows, t = Z on right rows.
         out.h.set_level(l, k, true);
-        panel_parity_scale(pc, n, k, S.get(), n, 1.0, 0.0, out.h.Ul(l), n, 0.0);
-        panel_parity_scale(pc, n, k, Z, n, 0.0, 1.0, out.h.Ul(l), n, 1.0);
+        panel_parity_select(pc, k, S.get(), n, 1.0, Z, n, 1.0, out.h.Ul(l), n);
         for (int j = 0; j < nodes; ++j) {
             out.h.rank_up[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;
             out.h.rank_lo[static_cast<size_t>(l - 1)][static_cast<size_t>(j)] = k;

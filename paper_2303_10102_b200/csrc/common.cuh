@@ -62,6 +62,19 @@ void set_current(Ctx* c);
 
 inline void count_launch() { ++current().launches; }
 
+/// Per-device one-time flag: function attributes (dynamic shared memory
+/// opt-in) are per device, and hg_ctx_create allows contexts on several
+/// devices in one process. `static DeviceOnce o; if (o.first()) ...`.
+struct DeviceOnce {
+    bool seen[64] = {};
+    bool first() {
+        const int d = current().device & 63;
+        if (seen[d]) return false;
+        seen[d] = true;
+        return true;
+    }
+};
+
 // ------------------------------------------------------- device allocator
 /// Stream-ordered caching allocator. A step of the MLE pipeline allocates
 /// the same multiset of multi-GB panels every iteration; the driver pool

@@ -638,11 +638,8 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
     ProfScope prof(PROF_LEAF_SOLVE, 2.0 * rows * m * w, 8.0 * (rows * m + 2.0 * rows * w));
     if (prof_enabled()) prof.key(prof_tag("leafsolve w=%d", w));
     if (f.all_llt && f.bmax() <= TS_MAX) {
-        static bool attr = false;
-        if (!attr) {
-            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc<TS_S>), TS_SMEM);
-            attr = true;
-        }
+        static DeviceOnce attr;
+        if (attr.first()) set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc<TS_S>), TS_SMEM);
         // Column tiles per CTA: enough CTAs for ~4 waves, the factor loaded once per CTA.
         const int ct = cdiv(w, TS_NC);
         const int groups = std::max(1, std::min(ct, cdiv(4 * 2 * current().num_sms, lv.nseg())));
@@ -655,11 +652,8 @@ void leaf_solve_subst(const DFactor& f, double* Y, i64 ldy, int w) {
         return;
     }
     if (f.all_llt && f.bmax() <= TS2_MAX) {  // 129..256-row leaves: 2 x 2 blocks
-        static bool attr2 = false;
-        if (!attr2) {
-            set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc2), TS2_SMEM);
-            attr2 = true;
-        }
+        static DeviceOnce attr2;
+        if (attr2.first()) set_smem(reinterpret_cast<const void*>(k_leaf_solve_tc2), TS2_SMEM);
         const int ct = cdiv(w, TS_NC);
         const int groups = std::max(1, std::min(ct, cdiv(4 * current().num_sms, lv.nseg())));
         const int cpt = cdiv(ct, groups);
@@ -749,8 +743,7 @@ DFactor factorize(const DHodlr& h, int orient) {
         } else {
             auto P = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(R), false);
             const Partition& p = h.tree->part(l);
-            panel_parity_scale(p, n, R, h.Ul(l), n, 1.0, 0.0, P->get(), n, 0.0);
-            panel_parity_scale(p, n, R, h.Vl(l), n, 0.0, 1.0, P->get(), n, 1.0);
+            panel_parity_select(p, R, h.Ul(l), n, 1.0, h.Vl(l), n, 1.0, P->get(), n);
             f.F[static_cast<size_t>(l - 1)] = P;
         }
     }

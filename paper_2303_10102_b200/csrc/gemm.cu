@@ -366,20 +366,25 @@ __global__ void k_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, do
         }
 }
 
-__global__ void k_parity_scale(const WorkItem* items, int w, const double* X, i64 ldx, double ae, double ao,
-                               double* Y, i64 ldy, double beta) {
+/// Y rows of even segments = ae Xe, of odd segments = ao Xo (a null source
+/// writes zeros): each row reads the one source it keeps.
+__global__ void k_parity_select(const WorkItem* items, int w, const double* Xe, i64 ldxe, double ae,
+                                const double* Xo, i64 ldxo, double ao, double* Y, i64 ldy) {
     const WorkItem it = items[blockIdx.x];
-    const double a = (it.seg & 1) ? ao : ae;
     if (int(threadIdx.x) >= it.rows) return;  // one thread per row (items have <= blockDim rows)
+    const bool odd = it.seg & 1;
+    const double a = odd ? ao : ae;
+    const double* X = odd ? Xo : Xe;
+    const i64 ldx = odd ? ldxo : ldxe;
     const i64 row = i64(it.row0) + threadIdx.x;
-    const double* x = X + row;
     double* y = Y + row;
-    if (beta != 0.0) {
-#pragma unroll 4
-        for (int j = 0; j < w; ++j) y[i64(j) * ldy] = fma(a, x[i64(j) * ldx], beta * y[i64(j) * ldy]);
-    } else {
+    if (X) {
+        const double* x = X + row;
 #pragma unroll 4
         for (int j = 0; j < w; ++j) y[i64(j) * ldy] = a * x[i64(j) * ldx];
+    } else {
+#pragma unroll 4
+        for (int j = 0; j < w; ++j) y[i64(j) * ldy] = 0.0;
     }
 }
 
@@ -743,13 +748,12 @@ void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double be
     ++c.launches;
 }
 
-void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 ldx, double a_even, double a_odd,
-                        double* Y, i64 ldy, double beta) {
-    (void)n;
+void panel_parity_select(const Partition& p, int w, const double* Xe, i64 ldxe, double a_even, const double* Xo,
+                         i64 ldxo, double a_odd, double* Y, i64 ldy) {
     if (w <= 0) return;
     auto& c = current();
     const TileList& tl = p.tiles(256);
-    k_parity_scale<<<tl.count, 256, 0, c.stream>>>(tl.items.get(), w, X, ldx, a_even, a_odd, Y, ldy, beta);
+    k_parity_select<<<tl.count, 256, 0, c.stream>>>(tl.items.get(), w, Xe, ldxe, a_even, Xo, ldxo, a_odd, Y, ldy);
     HG_LAUNCH();
     ++c.launches;
 }

@@ -548,22 +548,18 @@ void launch(MvArgs& a, int nleaves, int rmax, int bmax) {
     if (NT == 64 && a.tau >= 2) {  // row pairs: 4 leaves per CTA, the two deepest levels finish in-CTA
         constexpr int NTH = 64 * LPC, NWM = NTH / 32;
         const int sm1 = int(sizeof(double)) * ((3 * NWM + 1 + LPC) * rmax * S + LPC * 128 * S);
-        static bool once = [] {
+        static DeviceOnce once;
+        if (once.first())
             HG_CUDA(cudaFuncSetAttribute(k_mv_sweep_multi<S, LPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          100 * 1024));
-            return true;
-        }();
-        (void)once;
         a.dleft = a.tau - 2;
         k_mv_sweep_multi<S, LPC><<<unsigned(nleaves / LPC), NTH, size_t(sm1), c.stream>>>(a);
     } else {
         const int sm1 = int(sizeof(double)) * ((3 * NW + 1) * rmax * S + bmax * S);
-        static bool once = [] {
+        static DeviceOnce once;
+        if (once.first())
             HG_CUDA(cudaFuncSetAttribute(k_mv_sweep<S, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          100 * 1024));
-            return true;
-        }();
-        (void)once;
         a.dleft = a.tau;
         k_mv_sweep<S, RPT, NT><<<unsigned(nleaves), NT, size_t(sm1), c.stream>>>(a);
     }

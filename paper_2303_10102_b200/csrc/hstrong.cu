@@ -7,6 +7,7 @@
 
 #include "hstrong.cuh"
 #include "prof.cuh"
+#include "tile.cuh"
 
 namespace hg {
 
@@ -406,6 +407,95 @@ __global__ void __launch_bounds__(256) k_hs_update_tiled(const DHStrong::Tile* t
         }
 }
 
+// ---- wide blocks (s > 4): both passes on the FP64 tensor cores (tile.cuh)
+
+/// partials[part] (k x s, ld k) = M[rows]^T X[rows]: one TBM x TBN DMMA tile
+/// per (projection chunk, column chunk); both operands k-contiguous (rows are
+/// the reduction index).
+template <int TBM, int TBN>
+__global__ void __launch_bounds__(tile::THREADS) k_hs_proj_tc(const DHStrong::ProjItem* items, const double* Xc,
+                                                              i64 ldxc, int k, int s, double* partials) {
+    extern __shared__ double smem[];
+    const DHStrong::ProjItem it = items[blockIdx.x];
+    const int c0 = blockIdx.y * TBN;
+    const double* X = it.X ? it.X : Xc;
+    const i64 ldx = it.X ? it.ldx : ldxc;
+    tile::LoadKCT<TBM> la{it.M, it.ldm, it.rows, k};
+    tile::LoadKCT<TBN> lb{X + it.xoff + i64(c0) * ldx, ldx, it.rows, s - c0};
+    typename tile::Shape<TBM, TBN>::Acc acc;
+    acc.zero();
+    tile::run_t<tile::STAGES, TBM, TBN>(la, lb, (it.rows + tile::BK - 1) / tile::BK, smem, acc);
+    double* o = partials + i64(it.part) * k * s;
+    tile::for_each_t<TBM, TBN>(acc, [&](int a, int ci, double v) {
+        const int col = c0 + ci;
+        if (a < k && col < s) o[a + i64(col) * k] = v;
+    });
+}
+
+constexpr int UTC_MAXC = 1024;  // contributions of one leaf staged in shared memory
+
+/// Y[64-row tile, TBN columns] = sum over the tile's contributions of
+/// M(rows, :) R: ONE GEMM whose K runs over the concatenated contributions
+/// (each padded to whole 16-slices by the loaders' zero fill), the panels
+/// streamed through the cp.async pipeline; fixed order (deterministic).
+template <int TBN>
+__global__ void __launch_bounds__(tile::THREADS) k_hs_update_tc(const DHStrong::Tile* tiles,
+                                                                const DHStrong::Contrib* contrib, const double* P,
+                                                                const double* X, i64 ldx, int k, int s, double* Y,
+                                                                i64 ldy) {
+    constexpr int TBM = UP_ROWS, NS = tile::STAGES, BK = tile::BK;
+    constexpr int AE = tile::stage_elems(TBM), BE = tile::stage_elems(TBN);
+    extern __shared__ double smem[];
+    __shared__ int pref[UTC_MAXC + 1];
+    const DHStrong::Tile tl = tiles[blockIdx.x];
+    const int c0 = blockIdx.y * TBN, nc = tl.clast - tl.cfirst;
+    if (threadIdx.x == 0) {  // K-slice prefix of the contributions
+        int acc = 0;
+        for (int i = 0; i < nc; ++i) {
+            pref[i] = acc;
+            acc += (contrib[tl.cfirst + i].K + BK - 1) / BK;
+        }
+        pref[nc] = acc;
+    }
+    __syncthreads();
+    const int ktiles = pref[nc];
+    double* As = smem;
+    double* Bs = smem + NS * AE;
+    int cur = 0;
+    auto issue = [&](int stage, int vt) {  // vt increases from call to call
+        while (vt >= pref[cur + 1]) ++cur;
+        const DHStrong::Contrib C = contrib[tl.cfirst + cur];
+        const int kt = vt - pref[cur];
+        tile::LoadMCT<TBM> la{C.M + C.moff + tl.rin, C.ldm, tl.rows, C.K};
+        la.issue(As + stage * AE, kt);
+        const bool lowrank = C.rkind == 0;
+        tile::LoadKCT<TBN> lb{lowrank ? P + (C.ridx * s + c0) * i64(k) : X + C.ridx + i64(c0) * ldx,
+                              lowrank ? i64(k) : ldx, C.K, s - c0};
+        lb.issue(Bs + stage * BE, kt);
+    };
+    typename tile::Shape<TBM, TBN>::Acc acc;
+    acc.zero();
+#pragma unroll
+    for (int st = 0; st < NS - 1; ++st) {
+        if (st < ktiles) issue(st, st);
+        tile::cp_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        tile::cp_wait<NS - 2>();
+        __syncthreads();
+        const int nk = kt + NS - 1;
+        if (nk < ktiles) issue(nk % NS, nk);
+        tile::cp_commit();
+        const int st = kt % NS;
+        tile::mma_stage<false, true, TBM, TBN>(As + st * AE, Bs + st * BE, acc);
+    }
+    tile::cp_wait<0>();
+    tile::for_each_t<TBM, TBN>(acc, [&](int r, int ci, double v) {
+        const int col = c0 + ci;
+        if (r < tl.rows && col < s) Y[tl.row0 + r + i64(col) * ldy] = v;
+    });
+}
+
 struct DotItem {
     const double* A;
     const double* B;
@@ -656,6 +746,7 @@ DHStrong hs_build(const DOracle& o, int param, const std::int64_t* order, int ns
     for (int l = 0; l < nleaves; ++l) {
         const int first = int(cl.size());
         cl.insert(cl.end(), per[static_cast<size_t>(l)].begin(), per[static_cast<size_t>(l)].end());
+        h.max_contrib = std::max(h.max_contrib, int(per[static_cast<size_t>(l)].size()));
         const Range lr = range(P.tau, l);
         for (i64 r0 = 0; r0 < lr.size(); r0 += UP_ROWS)
             tl.push_back({int(lr.lo + r0), int(r0), int(std::min<i64>(UP_ROWS, lr.size() - r0)), first, int(cl.size()), 0});
@@ -667,19 +758,49 @@ DHStrong hs_build(const DOracle& o, int param, const std::int64_t* order, int ns
     return h;
 }
 
+namespace {
+
+void proj_tc(const DHStrong::ProjItem* items, int nitems, const double* X, i64 ldx, int k, int s, double* partials) {
+    auto& c = current();
+    with_tile(tile::tile_for(k), [&](auto TM) {
+        constexpr int M = decltype(TM)::value;
+        if constexpr (!tile::shape_ok(M, 16) || !tile::shape_ok(M, 64)) {
+            throw std::logic_error("hstrong proj_tc: tile extent");
+        } else if (s <= 16) {
+            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, 16);
+            attr_once<k_hs_proj_tc<M, 16>>(bytes);
+            k_hs_proj_tc<M, 16><<<dim3(unsigned(nitems), unsigned(cdiv(s, 16))), tile::THREADS, bytes, c.stream>>>(
+                items, X, ldx, k, s, partials);
+        } else {
+            constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, 64);
+            attr_once<k_hs_proj_tc<M, 64>>(bytes);
+            k_hs_proj_tc<M, 64><<<dim3(unsigned(nitems), unsigned(cdiv(s, 64))), tile::THREADS, bytes, c.stream>>>(
+                items, X, ldx, k, s, partials);
+        }
+    });
+}
+
+}  // namespace
+
 // ------------------------------------------------------------------ apply
 void hs_apply(const DHStrong& h, const double* X, i64 ldx, int s, double* Y, i64 ldy) {
     if (s <= 0) return;
     auto& c = current();
     const int k = h.k(), nslots = 2 * int(h.plan.lr.size());
     const unsigned cy = unsigned(cdiv(s, 16));
+    // wide blocks on the tensor cores (one M tile covers k; a leaf's contributions fit the staged prefix)
+    const bool tc = s > 4 && k <= 96 && h.max_contrib <= UTC_MAXC;
     DVec partials, P;
     if (nslots) {
         partials.alloc(static_cast<size_t>(h.nparts) * k * s);
         P.alloc(static_cast<size_t>(nslots) * k * s);
         {
             ProfScope prof(PROF_MATVEC, 2.0 * double(h.U.size() + h.V.size()) * s, 8.0 * double(h.U.size() + h.V.size()));
-            k_hs_proj<<<dim3(unsigned(h.proj.size()), cy), 256, 0, c.stream>>>(h.proj.get(), X, ldx, k, s, partials.get());
+            if (tc)
+                proj_tc(h.proj.get(), int(h.proj.size()), X, ldx, k, s, partials.get());
+            else
+                k_hs_proj<<<dim3(unsigned(h.proj.size()), cy), 256, 0, c.stream>>>(h.proj.get(), X, ldx, k, s,
+                                                                                     partials.get());
             HG_LAUNCH();
             k_hs_reduce<<<blocks_for(i64(nslots) * k * s), 256, 0, c.stream>>>(h.dslot_first.get(), nslots,
                                                                                 partials.get(), k, s, P.get());
@@ -693,7 +814,17 @@ void hs_apply(const DHStrong& h, const double* X, i64 ldx, int s, double* Y, i64
         k_hs_update<1><<<h.ntiles, 256, 0, c.stream>>>(h.tiles.get(), h.contrib.get(), P.get(), X, ldx, k, s, Y, ldy);
     else if (s <= 4)
         k_hs_update<4><<<h.ntiles, 256, 0, c.stream>>>(h.tiles.get(), h.contrib.get(), P.get(), X, ldx, k, s, Y, ldy);
-    else
+    else if (tc && s <= 16) {
+        constexpr int bytes = tile::smem_bytes_t(tile::STAGES, UP_ROWS, 16);
+        attr_once<k_hs_update_tc<16>>(bytes);
+        k_hs_update_tc<16><<<dim3(unsigned(h.ntiles), unsigned(cdiv(s, 16))), tile::THREADS, bytes, c.stream>>>(
+            h.tiles.get(), h.contrib.get(), P.get(), X, ldx, k, s, Y, ldy);
+    } else if (tc) {
+        constexpr int bytes = tile::smem_bytes_t(tile::STAGES, UP_ROWS, 64);
+        attr_once<k_hs_update_tc<64>>(bytes);
+        k_hs_update_tc<64><<<dim3(unsigned(h.ntiles), unsigned(cdiv(s, 64))), tile::THREADS, bytes, c.stream>>>(
+            h.tiles.get(), h.contrib.get(), P.get(), X, ldx, k, s, Y, ldy);
+    } else
         k_hs_update_tiled<<<dim3(unsigned(h.ntiles), cy), 256, 0, c.stream>>>(h.tiles.get(), h.contrib.get(), P.get(),
                                                                               X, ldx, k, s, Y, ldy);
     HG_LAUNCH();

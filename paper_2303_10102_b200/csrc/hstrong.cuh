@@ -90,6 +90,7 @@ public:
     DBuf<Contrib> contrib;
     DBuf<Tile> tiles;
     int ntiles = 0;
+    int max_contrib = 0;  // most contributions of one leaf
     i64 n() const { return plan.n; }
     int k() const { return plan.k; }
     size_t bytes() const { return (U.size() + V.size() + D.size()) * sizeof(double); }

@@ -42,10 +42,10 @@ void leaf_mm(const Partition& leaves, const double* L, i64 lstride, int ldl, boo
 /// Copy / scale / add panels: Y = alpha X + beta Y over n x w.
 void panel_axpby(i64 n, int w, double alpha, const double* X, i64 ldx, double beta, double* Y, i64 ldy);
 
-/// Masked copy by segment parity at a depth: rows of even (odd) segments
-/// take alpha_even * X (alpha_odd * X); columns [0, w).
-void panel_parity_scale(const Partition& p, i64 n, int w, const double* X, i64 ldx, double a_even,
-                        double a_odd, double* Y, i64 ldy, double beta);
+/// Y rows of even segments = a_even Xe, of odd segments = a_odd Xo (a null
+/// source writes zeros); each row reads only the source it keeps.
+void panel_parity_select(const Partition& p, int w, const double* Xe, i64 ldxe, double a_even, const double* Xo,
+                         i64 ldxo, double a_odd, double* Y, i64 ldy);
 
 /// out[0] (+)= sum_s sum_{e<len} A[s gsa + e] B[(s^xr) gsb + e] (deterministic
 /// streaming reduction; the HBM-bound core of every trace).

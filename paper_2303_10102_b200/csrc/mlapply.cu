@@ -571,11 +571,9 @@ void proj_cat(const DHodlr& h, const double* X, i64 ldx, int s, bool transpose, 
             constexpr int M = decltype(TM)::value, N = decltype(TN)::value;
             if constexpr (tile::shape_ok(M, N)) {
                 constexpr int bytes = tile::smem_bytes_t(tile::STAGES, M, N);
-                static bool once = [] {
+                static DeviceOnce once;
+                if (once.first())
                     HG_CUDA(cudaFuncSetAttribute(k_proj_cat<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-                    return true;
-                }();
-                (void)once;
                 k_proj_cat<M, N><<<dim3(unsigned(n / span), unsigned(tiles_m)), THREADS, bytes, c.stream>>>(a);
             } else {
                 throw std::logic_error("proj_cat: unsupported tile shape");
@@ -854,11 +852,9 @@ void hodlr_apply(const DHodlr& h, const double* X, i64 ldx, int s, double* Y, i6
         constexpr int bytes = tile::smem_bytes_t(2, BM, N);
         if (packed) {
             constexpr int pbytes = tile::smem_bytes_t(UPD_NS, BM, N);
-            static bool once = [] {  // static table + dynamic stages exceed the default 48 KB
+            static DeviceOnce once;  // static table + dynamic stages exceed the default 48 KB
+            if (once.first())
                 HG_CUDA(cudaFuncSetAttribute(k_ml_update_packed<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, pbytes));
-                return true;
-            }();
-            (void)once;
             k_ml_update_packed<N><<<dim3(unsigned(tl.count), unsigned(tiles_nu)), THREADS, pbytes, c.stream>>>(ua);
         } else {
             attr_once<k_ml_update<N>>(bytes);

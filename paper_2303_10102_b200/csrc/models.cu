@@ -292,12 +292,10 @@ private:
         auto& c = current();
         const size_t smem = static_cast<size_t>(m_) * sizeof(double);
         if (smem <= 200 * 1024) {  // column resident: parallel-scan sweeps, one CTA per column
-            static bool attr = false;
-            if (!attr) {
+            static DeviceOnce attr;
+            if (attr.first())
                 HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_thomas_col),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                attr = true;
-            }
             k_thomas_col<<<unsigned(s), TS_THR, smem, c.stream>>>(int(m_), a_, cp_.get(), im_.get(), D, m_, X, m_);
         } else {
             k_thomas<<<unsigned(cdiv(s, 32)), 32, 0, c.stream>>>(int(m_), s, a_, cp_.get(), im_.get(), D, m_, X, m_);

@@ -160,12 +160,10 @@ private:
         ProfScope prof(PROF_ORACLE, scan_ ? 2.0 * double(n_) * s * (MC_ROWS + 4 * P.nt) : 2.0 * double(n_) * n_ * s,
                        24.0 * double(n_) * s);
         if (!scan_) {
-            static bool attr = false;
-            if (!attr) {
+            static DeviceOnce attr;
+            if (attr.first())
                 HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_matern_dense),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, tile::SMEM_BYTES));
-                attr = true;
-            }
             dim3 grid(unsigned(cdiv(n_, BM)), unsigned(cdiv(s, BN)));
             k_matern_dense<<<grid, tile::THREADS, tile::SMEM_BYTES, c.stream>>>(x_.get(), int(n_), P, V, ldv, s, Y,
                                                                                 ldy);
@@ -180,13 +178,12 @@ private:
         MatChunkArgs g{x_.get(), int(n_), nsup, s, P.nt, P.lambda, {P.c[0], P.c[1], P.c[2], P.c[3]},
                        j < 0 ? nugget_ : 0.0, V, ldv, Y, ldy, Lf.get(), Lb.get(), Ff.get(), Fb.get(),
                        z.bounds, z.nseg, z.parity, z.out_depth >= 0 ? 1 : 0};
-        static bool attr = false;
-        if (!attr) {
+        static DeviceOnce attr;
+        if (attr.first()) {
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_mat_moments),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM)));
             HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_mat_apply),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(MC_SMEM)));
-            attr = true;
         }
         const dim3 grid(static_cast<unsigned>(nsup), 1u);
         k_mat_moments<<<grid, MC_TILE, MC_SMEM, c.stream>>>(g);

@@ -154,15 +154,15 @@ std::vector<DProductRep> pipeline_multi(const DFactor& f, const std::vector<cons
         if (inverse) {
             if (!ref_assoc) form_p();
             // q = u = [wbar 0; 0 xbar]
-            panel_parity_scale(p, n, R, f.Wl(i), n, 1.0, 0.0, Q.get(), n, 0.0);
-            panel_parity_scale(p, n, R, f.Wl(i), n, 0.0, 1.0, Q.get() + i64(R) * n, n, 0.0);
+            panel_parity_select(p, R, f.Wl(i), n, 1.0, nullptr, 0, 0.0, Q.get(), n);
+            panel_parity_select(p, R, nullptr, 0, 0.0, f.Wl(i), n, 1.0, Q.get() + i64(R) * n, n);
         } else {
             // p = u = [wbar 0; 0 xbar]
-            panel_parity_scale(p, n, R, f.Wl(i), n, 1.0, 0.0, cu, n, 0.0);
-            panel_parity_scale(p, n, R, f.Wl(i), n, 0.0, 1.0, cu + i64(R) * n, n, 0.0);
+            panel_parity_select(p, R, f.Wl(i), n, 1.0, nullptr, 0, 0.0, cu, n);
+            panel_parity_select(p, R, nullptr, 0, 0.0, f.Wl(i), n, 1.0, cu + i64(R) * n, n);
             // q = v = [0 w; x 0]
-            panel_parity_scale(p, n, R, f.Fl(i), n, 0.0, 1.0, Q.get(), n, 0.0);
-            panel_parity_scale(p, n, R, f.Fl(i), n, 1.0, 0.0, Q.get() + i64(R) * n, n, 0.0);
+            panel_parity_select(p, R, nullptr, 0, 0.0, f.Fl(i), n, 1.0, Q.get(), n);
+            panel_parity_select(p, R, f.Fl(i), n, 1.0, nullptr, 0, 0.0, Q.get() + i64(R) * n, n);
         }
         for (size_t j = 0; j < P; ++j)
             hodlr_apply(reps[j].base, Q.get(), n, C2, reps[j].Cvl(i), n, i, tau, true, true, 0.0);

@@ -356,12 +356,11 @@ void with_tile(int t, F&& f) {
 /// Host: opt the kernel KFN into `bytes` of dynamic shared memory (once).
 template <auto KFN>
 void attr_once(int bytes) {
-    static bool done = false;
-    if (done) return;
+    static DeviceOnce once;
+    if (!once.first()) return;
     if (bytes > 48 * 1024)
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(KFN), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bytes));
-    done = true;
 }
 
 }  // namespace hg

@@ -40,6 +40,12 @@ def test_strong_dense_accuracy_and_structure(H):
     # matvec of a block equals the densified operator applied to it
     X = np.random.default_rng(0).standard_normal((n, 5))
     assert np.linalg.norm(hs.matvec(X) - Hd @ X) <= 1e-13 * np.linalg.norm(Hd @ X)
+    # wide blocks (tensor-core path): ragged column counts, bitwise repeatable, columns independent of the batch
+    for s in (9, 16, 70):
+        Xs = np.random.default_rng(s).standard_normal((n, s))
+        Ys = hs.matvec(Xs)
+        assert np.linalg.norm(Ys - Hd @ Xs) <= 1e-13 * np.linalg.norm(Hd @ Xs), s
+        assert np.array_equal(Ys, hs.matvec(Xs)), s
     # near-field blocks are exact entries: the diagonal of H is the covariance's
     assert np.max(np.abs(np.diag(Hd) - np.diag(K))) <= 1e-12 * np.max(np.abs(K))
 
