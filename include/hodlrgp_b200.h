@@ -211,7 +211,7 @@ hg_status hg_sketch_sampler(hg_ctx_t ctx, int64_t n, int tau, int64_t k, uint64_
 /* randomized_range(y, k) (sketch.cpp:37-76): rows x k block y -> q (rows x k,
  * orthonormal), r (k x k upper, diag >= 0, host), perm (k, host; y.col(perm[i])
  * -> position i), numeric rank (#|r_ii| > 64 eps |r_00|); deficient columns
- * completed with unit vectors orthogonalised twice. k <= 64. */
+ * completed with unit vectors orthogonalised twice. k <= 128. */
 hg_status hg_randomized_range(hg_ctx_t ctx, const double* y, int64_t ldy, int64_t rows, int64_t k, double* q,
                               int64_t ldq, double* r, int* perm, int64_t* numeric_rank, int loc);
 /* diff_qr(b, db, q, r) (sketch.cpp:78-111): derivative of b = q r under db ->

@@ -18,6 +18,8 @@ namespace hg {
 
 namespace {
 
+constexpr int MAX_RANK = 128;  // sketch width k: per-node k x k work arrays live in shared memory
+
 __global__ void k_leaf_identity(const int* bounds, double* P, i64 ldp) {
     const int b = blockIdx.x;
     const int lo = bounds[b], m = bounds[b + 1] - lo;
@@ -223,7 +225,8 @@ __global__ void k_completion_cholqr(const int* cj, int cmax, const double* Gw, d
     const double* G = Gw + i64(2 * j) * cmax * cmax;
     double* Ri = Rinv + i64(2 * j) * cmax * cmax;
     double* Rd = Rdiag + i64(j) * cmax * cmax;
-    __shared__ double L[64 * 65];
+    extern __shared__ double L[];  // cmax x cmax, row stride ls (odd)
+    const int ls = cmax | 1;
     for (int e = lane; e < cmax * cmax; e += 32) {
         Ri[e] = 0.0;
         Rinv[i64(2 * j + 1) * cmax * cmax + e] = 0.0;
@@ -233,19 +236,19 @@ __global__ void k_completion_cholqr(const int* cj, int cmax, const double* Gw, d
         if (lane == 0) fail[j] = 0;
         return;
     }
-    for (int e = lane; e < c * c; e += 32) L[(e % c) * 65 + e / c] = G[(e % c) + i64(e / c) * cmax];
+    for (int e = lane; e < c * c; e += 32) L[(e % c) * ls + e / c] = G[(e % c) + i64(e / c) * cmax];
     __syncwarp();
     int bad = 0;
-    for (int t = 0; t < c; ++t) {  // right-looking Cholesky, lower L (row r, col t at L[r * 65 + t])
-        const double d = L[t * 65 + t];
+    for (int t = 0; t < c; ++t) {  // right-looking Cholesky, lower L (row r, col t at L[r * ls + t])
+        const double d = L[t * ls + t];
         const double ltt = d > 0.0 ? sqrt(d) : 0.0;
         bad |= !(ltt >= 0.5);
         __syncwarp();
-        for (int r = t + 1 + lane; r < c; r += 32) L[r * 65 + t] = ltt > 0.0 ? L[r * 65 + t] / ltt : 0.0;
+        for (int r = t + 1 + lane; r < c; r += 32) L[r * ls + t] = ltt > 0.0 ? L[r * ls + t] / ltt : 0.0;
         __syncwarp();
-        if (lane == 0) L[t * 65 + t] = ltt;
+        if (lane == 0) L[t * ls + t] = ltt;
         for (int r = t + 1 + lane; r < c; r += 32)
-            for (int q = t + 1; q <= r; ++q) L[r * 65 + q] -= L[r * 65 + t] * L[q * 65 + t];
+            for (int q = t + 1; q <= r; ++q) L[r * ls + q] -= L[r * ls + t] * L[q * ls + t];
         __syncwarp();
     }
     if (lane == 0) fail[j] = bad;
@@ -254,10 +257,10 @@ __global__ void k_completion_cholqr(const int* cj, int cmax, const double* Gw, d
     for (int col = lane; col < c; col += 32) {
         for (int i = col; i >= 0; --i) {
             double s = (i == col) ? 1.0 : 0.0;
-            for (int q = i + 1; q <= col; ++q) s -= L[q * 65 + i] * Ri[q + i64(col) * cmax];
-            Ri[i + i64(col) * cmax] = s / L[i * 65 + i];
+            for (int q = i + 1; q <= col; ++q) s -= L[q * ls + i] * Ri[q + i64(col) * cmax];
+            Ri[i + i64(col) * cmax] = s / L[i * ls + i];
         }
-        Rd[col + i64(col) * cmax] = L[col * 65 + col];
+        Rd[col + i64(col) * cmax] = L[col * ls + col];
     }
 }
 
@@ -315,7 +318,8 @@ __global__ void k_diffqr(int k, const double* G, const double* R, const int* per
     const double* Rj = R + i64(j) * k * k;
     double* O = Om + i64(j) * k * k;
     __shared__ int s_rw;
-    __shared__ double y[64 * 65];
+    extern __shared__ double y[];  // k x k, row stride ys (odd); blockDim >= k
+    const int ys = k | 1;
     if (threadIdx.x == 0) {
         int rw = 0;
         const int r = nr[j];
@@ -339,15 +343,15 @@ __global__ void k_diffqr(int k, const double* G, const double* R, const int* per
     if (a < rw) {
         for (int c = 0; c < rw; ++c) {  // y(a,:) R_rw = y0(a,:), column by column
             double s = Gj[a + perm[j * k + c] * k];
-            for (int i = 0; i < c; ++i) s -= y[a * 65 + i] * Rj[i + c * k];
-            y[a * 65 + c] = s / Rj[c + c * k];
+            for (int i = 0; i < c; ++i) s -= y[a * ys + i] * Rj[i + c * k];
+            y[a * ys + c] = s / Rj[c + c * k];
         }
     }
     __syncthreads();
     if (a < rw)
         for (int c = 0; c < a; ++c) {
-            O[a + c * k] = y[a * 65 + c];
-            O[c + a * k] = -y[a * 65 + c];
+            O[a + c * k] = y[a * ys + c];
+            O[c + a * k] = -y[a * ys + c];
         }
 }
 
@@ -765,14 +769,21 @@ void complete_deficient(const Partition& pc, int k, const DBuf<int>& nr, double*
     k_mask_cols<<<nodes, 256, 0, ctx.stream>>>(pc.dbounds(), 0, dcj.get(), cmax, W.get(), n);
     HG_LAUNCH();
     ctx.launches += 4;
-    if (cmax > 64) throw std::length_error("complete_deficient: more than 64 completion columns");
+    if (cmax > MAX_RANK) throw std::length_error("complete_deficient: more than 128 completion columns");
     std::vector<int> rmap(static_cast<size_t>(nodes), -1);
     for (int j : big) rmap[static_cast<size_t>(j)] = j;
     DVec Gw(static_cast<size_t>(2 * nodes) * cmax * cmax), Rinv(static_cast<size_t>(2 * nodes) * cmax * cmax),
         Rd(static_cast<size_t>(nodes) * cmax * cmax);
     DBuf<int> dfail(static_cast<size_t>(nodes));
     seg_tn(pc, W.get(), n, cmax, W.get(), n, cmax, Gw.get(), i64(cmax) * cmax, cmax);
-    k_completion_cholqr<<<nodes, 32, 0, ctx.stream>>>(dcj.get(), cmax, Gw.get(), Rinv.get(), Rd.get(), dfail.get());
+    {
+        const size_t lbytes = sizeof(double) * size_t(cmax) * size_t(cmax | 1);
+        if (lbytes > 48 * 1024)
+            HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_completion_cholqr),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(lbytes)));
+        k_completion_cholqr<<<nodes, 32, lbytes, ctx.stream>>>(dcj.get(), cmax, Gw.get(), Rinv.get(), Rd.get(),
+                                                                dfail.get());
+    }
     HG_LAUNCH();
     count_launch();
     const std::vector<int> failh = dfail.download();
@@ -910,11 +921,22 @@ __global__ void k_solve_upper_right(int m, int k, const double* R, double* X, i6
         }
 }
 
+size_t diffqr_smem(int k) {
+    const size_t b = sizeof(double) * size_t(k) * size_t(k | 1);
+    if (b > 48 * 1024)
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_diffqr), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(b)));
+    return b;
+}
+
 }  // namespace
 
 void diff_qr(const double* dB, i64 lddb, const double* Q, i64 ldq, const double* R, int rows, int k, double* dQ,
              i64 lddq, double* dQspan, i64 ldds, double* dR, int* ill) {
-    if (k <= 0 || k > 64 || rows < k) throw std::invalid_argument("diff_qr: need rows >= k, 1 <= k <= 64");
+    if (k <= 0 || k > MAX_RANK || rows < k) throw std::invalid_argument("diff_qr: need rows >= k, 1 <= k <= 128");
+    if (sizeof(double) * k * k > 48 * 1024)
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_diffqr_core),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(double) * k * k)));
     auto& ctx = current();
     const Partition one(std::vector<int>{0, rows});
     DVec G(static_cast<size_t>(k) * k), Y(static_cast<size_t>(k) * k), Om(static_cast<size_t>(k) * k);
@@ -935,7 +957,7 @@ void diff_qr(const double* dB, i64 lddb, const double* Q, i64 ldq, const double*
 void randomized_range(const double* Y, i64 ldy, int rows, int k, double* Q, i64 ldq, double* R, int* perm,
                       int* nr) {
     if (k <= 0 || rows < k) throw std::invalid_argument("randomized_range: need rows >= k >= 1");
-    if (k > 64) throw std::length_error("randomized_range: rank above 64 not supported");
+    if (k > MAX_RANK) throw std::length_error("randomized_range: rank above 128 not supported");
     auto& ctx = current();
     // one node: the block is the left child, the right child is empty
     const Partition pc(std::vector<int>{0, rows, rows});
@@ -1027,7 +1049,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
                 throw std::invalid_argument("build_hodlr: rank " + std::to_string(kk) +
                                             " exceeds block dimension at level " + std::to_string(l));
     }
-    if (k > 64) throw std::length_error("build_hodlr: rank above 64 not supported");
+    if (k > MAX_RANK) throw std::length_error("build_hodlr: rank above 128 not supported");
     const int p = with_deriv ? o.num_params() : 0;
     const int kp = k * p;
     DBuildResult out;
@@ -1134,7 +1156,7 @@ DBuildResult build(const DOracle& o, DTreeP tree, i64 kk, const DSketchPlan& pla
             DBuf<int> rw(static_cast<size_t>(nodes)), ill(static_cast<size_t>(nodes));
             const double* dYq = dY.get() + i64(q) * k * n;
             seg_tn(pc, S.get(), n, k, dYq, n, k, G.get(), i64(k) * k, k);
-            k_diffqr<<<nodes, 64, 0, ctx.stream>>>(k, G.get(), Rn.get(), perm.get(), nr.get(), dqmap.get(),
+            k_diffqr<<<nodes, k <= 64 ? 64 : 128, diffqr_smem(k), ctx.stream>>>(k, G.get(), Rn.get(), perm.get(), nr.get(), dqmap.get(),
                                                    OmP->get(), rw.get(), ill.get());
             HG_LAUNCH();
             ++ctx.launches;

@@ -137,8 +137,9 @@ def oracle_q2_reorth():
     O.set_compress_at_level(False)
 
 
+# the last two: sketch widths above 64 (per-node work arrays in dynamic shared memory), most blocks deficient
 BUILD_CASES = [(1024, 64, 16, 3, 0.2, 1e-4), (4096, 64, 24, 3, 0.2, 1e-4), (2048, 128, 40, 5, 0.05, 1e-6),
-               (1500, 64, 16, 3, 0.2, 1e-4)]
+               (1500, 64, 16, 3, 0.2, 1e-4), (2048, 256, 96, 3, 0.2, 1e-4), (4096, 256, 128, 5, 0.05, 1e-6)]
 
 
 @pytest.mark.parametrize("n,leaf,k,nu2,ell,nug", BUILD_CASES)
@@ -235,6 +236,27 @@ def test_mle_iteration_c1_end_to_end(H):
     w = np.linalg.solve(K, y)
     ll_dense = -0.5 * n * np.log(2 * np.pi) - 0.5 * ld - 0.5 * y @ w
     assert abs(ll1 - ll_dense) <= 1e-6 * abs(ll_dense)
+
+
+def test_mle_iteration_wide_sketch(H):
+    """One iteration at sketch width k = 96 (> 64: 2R = 192 capacitances, completion of
+    up to 90 columns) against the oracle in the device's modes; the rank limit is 128."""
+    n, leaf, k = 4096, 256, 96
+    x = np.sort(np.random.default_rng(11).uniform(size=n))
+    tau = O.tree_depth(n, leaf, 2 * leaf)
+    oo = O.CovOracle.matern(x, 3, 1.0, 0.2, 1e-4, True)
+    y = O.randn(n, 1, 5)[:, 0]
+    try:
+        O.device_defaults(True)
+        ll0, s0, f0, _ = O.mle_iteration(oo, tau, k, 0, y, 2)
+    finally:
+        O.device_defaults(False)
+    do = H.MaternOracle(x, 3, 1.0, 0.2, 1e-4, True)
+    ll1, s1, f1, t = H.mle_iteration(do, tau, k, 0, y)
+    assert ll1 == pytest.approx(ll0, rel=1e-9)
+    assert _rel(s1, s0) <= 1e-7 and _rel(f1, f0) <= 1e-7, (_rel(s1, s0), _rel(f1, f0))
+    with pytest.raises(Exception):
+        H.build_hodlr_with_derivatives(do, H.ClusterTree(n, tau), 129, 0)
 
 
 def test_mle_glue_dense_family(H):  # test_mle.cpp:53-84 on the device
