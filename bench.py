@@ -369,9 +369,10 @@ def main():
         tj = json.load(open(args.traffic_json))
         sha = hashlib.sha256(open(H.LIB_PATH, "rb").read()).hexdigest()
         tc = tj.get("classes", {}).get(dom)
-        if tj.get("lib_sha256") == sha and tc and d["launches"]:
+        same = tj.get("lib_sha256") == sha or tj.get("src_sha256") == H.source_sha256()
+        if same and tc and d["launches"]:
             traffic = tc["dram_bytes"] / d["launches"]
-            traffic_src = (f"{os.path.relpath(args.traffic_json, ROOT)} (ncu, same .so sha256): "
+            traffic_src = (f"{os.path.relpath(args.traffic_json, ROOT)} (ncu, same library sources/.so sha256): "
                            f"{tc['dram_bytes']:.4g} B over one step's {tc['kernels']} kernels / {d['launches']} ledger calls")
     except (OSError, ValueError, KeyError):
         pass

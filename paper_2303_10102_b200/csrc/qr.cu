@@ -14,6 +14,7 @@ constexpr int QNT = 512;   // QR: more warps share each step's column updates
 constexpr int FQNT = 256;  // Q formation
 constexpr int MAXW = 512;
 constexpr size_t QR_SMEM = 200 * 1024;
+constexpr int QR_RPL = 32;  // rows per lane a trailing column may keep in registers (in-place blocks)
 
 __device__ double qr_block_sum(double v) {
     __shared__ double sh[32];
@@ -32,7 +33,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <bool PIVOT>
+template <bool PIVOT, bool INPLACE>
 __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem_elems) {
     extern __shared__ double sm[];
     __shared__ double nu[MAXW], nd[MAXW];
@@ -134,12 +135,44 @@ __global__ void __launch_bounds__(QNT) k_qr(const QrDesc* descs, int w, int smem
                 break;
             }
         }
-        for (int i = k + 1 + tid; i < rows; i += blockDim.x) W[i + k * ldw] = zero ? 0.0 : W[i + k * ldw] / div;
+        // In-place (global-memory) blocks: the scaled Householder vector is
+        // staged in the otherwise unused shared buffer and each trailing
+        // column is held in registers between its dot product and its update
+        // (one global read and one write per element instead of three reads;
+        // same operations in the same order as the resident path).
+        const bool staged = INPLACE && !use_smem && rows <= min(smem_elems, 32 * QR_RPL);
+        for (int i = k + 1 + tid; i < rows; i += blockDim.x) {
+            const double vi = zero ? 0.0 : W[i + k * ldw] / div;
+            W[i + k * ldw] = vi;
+            if (staged) sm[i] = vi;
+        }
         __syncthreads();
         for (int j = k + 1 + warp; j < w; j += nwarps) {
             double* cj = W + j * ldw;
             if (rows - k == 1) {
                 if (lane == 0) cj[k] *= (1.0 - tau);
+            } else if (tau != 0.0 && staged) {
+                double cr[QR_RPL];
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < QR_RPL; ++q) {
+                    const int i = k + 1 + lane + 32 * q;
+                    if (i < rows) {
+                        cr[q] = cj[i];
+                        t += sm[i] * cr[q];
+                    }
+                }
+                t = warp_sum(t) + cj[k];
+#pragma unroll
+                for (int q = 0; q < QR_RPL; ++q) {
+                    const int i = k + 1 + lane + 32 * q;
+                    if (i < rows) {
+                        cr[q] -= tau * sm[i] * t;
+                        cj[i] = cr[q];
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) cj[k] -= tau * t;
             } else if (tau != 0.0) {
                 double t = 0.0;
                 for (int i = k + 1 + lane; i < rows; i += 32) t += W[i + k * ldw] * cj[i];
@@ -242,6 +275,22 @@ __global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int
 
 #include "qr_blocked.cuh"
 
+/// INPLACE instantiation only when some block does not fit shared memory
+/// (its register-held columns would cost the resident path occupancy).
+template <bool PIVOT>
+void launch_qr(const QrDesc* dd, int nblocks, int qnt, size_t smem, int w, int smem_elems, bool inplace) {
+    auto& c = current();
+    if (inplace) {
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<PIVOT, true>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_qr<PIVOT, true><<<unsigned(nblocks), qnt, smem, c.stream>>>(dd, w, smem_elems);
+    } else {
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<PIVOT, false>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_qr<PIVOT, false><<<unsigned(nblocks), qnt, smem, c.stream>>>(dd, w, smem_elems);
+    }
+}
+
 }  // namespace
 
 void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
@@ -269,13 +318,9 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
         k_qr_blocked<<<unsigned(blocks.size()), QB_THREADS, sb, c.stream>>>(dd.get(), w);
     } else if (pivot) {
-        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<true>),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_qr<true><<<unsigned(blocks.size()), qnt, smem, c.stream>>>(dd.get(), w, smem_elems);
+        launch_qr<true>(dd.get(), int(blocks.size()), qnt, smem, w, smem_elems, smem_elems < max_rows * w);
     } else {
-        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr<false>),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_qr<false><<<unsigned(blocks.size()), qnt, smem, c.stream>>>(dd.get(), w, smem_elems);
+        launch_qr<false>(dd.get(), int(blocks.size()), qnt, smem, w, smem_elems, smem_elems < max_rows * w);
     }
     HG_LAUNCH();
     ++c.launches;

@@ -15,6 +15,21 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libhodlrgp_b200.so")
 
+
+def source_sha256():
+    """sha256 over the library's sources (csrc/*, Makefile, the C header): names a
+    build independently of where and when it was compiled (profiles/*traffic*.json)."""
+    import glob
+    import hashlib
+
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(_HERE, "csrc", "*.cu")) + glob.glob(os.path.join(_HERE, "csrc", "*.cuh")))
+    files += [os.path.join(_HERE, "Makefile"), os.path.join(os.path.dirname(_HERE), "include", "hodlrgp_b200.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()
+
 i64, u64, dbl, vp = C.c_int64, C.c_uint64, C.c_double, C.c_void_p
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int)

@@ -6,8 +6,8 @@ of scripts/one_step.py (warm-up step + measured step, same build):
   python scripts/traffic_capture.py gpurun_out/traffic.csv profiles/r2_traffic.json
 
 Writes per-class totals of the measured (second) step plus the sha256 of the
-libhodlrgp_b200.so that ran, so bench.py only uses the figure for the same
-build (dividing the class's step bytes by its own ledger call count).
+libhodlrgp_b200.so that ran and of its sources, so bench.py only uses the
+figure for the same build (dividing the class's step bytes by its own ledger call count).
 """
 import collections
 import csv
@@ -63,7 +63,10 @@ def main():
         agg[c]["kernels"] += 1
         agg[c]["bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
         agg[c]["ns"] += d.get("gpu__time_duration.sum", 0)
-    out = {"lib_sha256": hashlib.sha256(open(LIB, "rb").read()).hexdigest(),
+    sys.path.insert(0, ROOT)
+    from paper_2303_10102_b200.hodlrgp import source_sha256
+
+    out = {"lib_sha256": hashlib.sha256(open(LIB, "rb").read()).hexdigest(), "src_sha256": source_sha256(),
            "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
                      "--clock-control none, second step of scripts/one_step.py",
            "step_kernels": len(step),
