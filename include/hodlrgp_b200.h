@@ -156,6 +156,12 @@ hg_status hg_trace_product_rep(hg_ctx_t ctx, hg_prodrep_t p, double* out);
 hg_status hg_trace_pair(hg_ctx_t ctx, hg_prodrep_t p, hg_prodrep_t q, double* out);
 hg_status hg_trace_solve(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, double* out);
 hg_status hg_trace_quad(hg_ctx_t ctx, hg_factor_t fa, hg_hodlr_t b, hg_factor_t fc, hg_hodlr_t d, double* out);
+/* hutchinson_trace — mle.cpp:56-75: stochastic cross-check of tr(K^-1 B) with
+ * n_samples >= 2 Rademacher probes (HG_EINVAL below 2), generated on the host
+ * with std::mt19937_64(seed) + std::bernoulli_distribution(0.5) in the
+ * reference's order; probes are applied 64 at a time (B Z, then the solve). */
+hg_status hg_hutchinson_trace(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, int n_samples, uint64_t seed,
+                              double* estimate, double* std_error);
 
 /* ------------------------------------------------------ covariance oracle */
 /* CovarianceOracle (oracle.hpp:15-52) implemented on the device.

@@ -350,6 +350,17 @@ inline double trace_solve(const HodlrFactorization& f_left, const HodlrMatrix& b
 inline double trace_solve(const HodlrMatrix& a, const HodlrMatrix& b) {
     return trace_solve(factorize(a, Orientation::Left), b);
 }
+/// mle.hpp:28-34
+struct HutchinsonResult {
+    double estimate = 0;
+    double std_error = 0;
+};
+inline HutchinsonResult hutchinson_trace(const HodlrFactorization& f, const HodlrMatrix& b, int n_samples,
+                                         std::uint64_t seed) {
+    HutchinsonResult r;
+    check(hg_hutchinson_trace(ctx(), f.handle(), b.handle(), n_samples, seed, &r.estimate, &r.std_error));
+    return r;
+}
 inline double trace_quad(const HodlrFactorization& fa, const HodlrMatrix& b, const HodlrFactorization& fc,
                          const HodlrMatrix& d) {
     double t = 0;

@@ -330,6 +330,13 @@ int or_prodrep_densify(void* p, double* out) {
 double or_trace_product_rep(void* p) { return trace_product_rep(static_cast<ORep*>(p)->p); }
 double or_trace_pair(void* p, void* q) { return trace_pair(static_cast<ORep*>(p)->p, static_cast<ORep*>(q)->p); }
 
+int or_hutchinson_trace(void* fp, void* bp, int n_samples, std::uint64_t seed, double* out2) {
+    return guard([&] {
+        const HutchinsonResult r = hutchinson_trace(static_cast<OFactor*>(fp)->f, static_cast<OHodlr*>(bp)->h, n_samples, seed);
+        out2[0] = r.estimate;
+        out2[1] = r.std_error;
+    });
+}
 int or_trace_solve(void* fp, void* bp, double* out) {
     return guard([&] { *out = trace_solve(static_cast<OFactor*>(fp)->f, static_cast<OHodlr*>(bp)->h); });
 }

@@ -1206,6 +1206,28 @@ std::vector<double> score(const HodlrFactorization& f, const std::vector<HodlrMa
     return s;
 }
 
+// mle.cpp:56-75
+HutchinsonResult hutchinson_trace(const HodlrFactorization& f, const HodlrMatrix& b, int n_samples,
+                                  std::uint64_t seed) {
+    if (n_samples < 2) throw std::invalid_argument("hutchinson_trace: need >= 2 samples");
+    std::mt19937_64 rng(seed);
+    std::bernoulli_distribution coin(0.5);
+    const Index n = f.size();
+    double sum = 0, sumsq = 0;
+    for (int s = 0; s < n_samples; ++s) {
+        Mat z(n, 1);
+        for (Index i = 0; i < n; ++i) z(i, 0) = coin(rng) ? 1.0 : -1.0;
+        const double v = dot_sum(z, f.solve(b.matvec(z)));
+        sum += v;
+        sumsq += v * v;
+    }
+    HutchinsonResult out;
+    out.estimate = sum / n_samples;
+    const double var = (sumsq - sum * sum / n_samples) / (n_samples - 1);
+    out.std_error = std::sqrt(std::max(var, 0.0) / n_samples);
+    return out;
+}
+
 // mle.cpp:43-54
 Mat fisher_information(const HodlrFactorization& f, const std::vector<HodlrMatrix>& deriv, bool cache) {
     const Index p = Index(deriv.size());

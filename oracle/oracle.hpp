@@ -438,6 +438,14 @@ double trace_quad(const HodlrMatrix& a, const HodlrMatrix& b, const HodlrMatrix&
                   const HodlrMatrix& d);
 
 // --------------------------------------------------------------- mle glue
+/// mle.cpp:56-75: Rademacher-probe estimate of tr(K^-1 B) (mt19937_64 +
+/// bernoulli_distribution(0.5), one probe at a time, in the reference's order).
+struct HutchinsonResult {
+    double estimate = 0;
+    double std_error = 0;
+};
+HutchinsonResult hutchinson_trace(const HodlrFactorization& f, const HodlrMatrix& b, int n_samples,
+                                  std::uint64_t seed);
 /// mle.cpp:25-54
 double log_likelihood(const HodlrFactorization& f, const Mat& y, const Mat& ybar);
 std::vector<double> score(const HodlrFactorization& f, const std::vector<HodlrMatrix>& deriv,

@@ -78,6 +78,7 @@ def lib():
             "or_trace_product_rep": (dbl, [vp]),
             "or_trace_pair": (dbl, [vp, vp]),
             "or_trace_solve": (C.c_int, [vp, vp, dp]),
+            "or_hutchinson_trace": (C.c_int, [vp, vp, C.c_int, u64, dp]),
             "or_trace_quad": (C.c_int, [vp, vp, vp, vp, dp]),
             "or_sketch_sampler": (C.c_int, [i64, C.c_int, i64, u64, C.c_int, dp]),
             "or_randomized_range": (C.c_int, [dp, i64, i64, dp, dp, ip, lp]),
@@ -381,6 +382,13 @@ def trace_solve(f, b):
     out = C.c_double()
     _check(lib().or_trace_solve(f.ptr, b.ptr, C.byref(out)))
     return out.value
+
+
+def hutchinson_trace(f, b, n_samples, seed):
+    """mle.cpp:56-75 -> (estimate, std_error)."""
+    out = (C.c_double * 2)()
+    _check(lib().or_hutchinson_trace(f.ptr, b.ptr, n_samples, seed, out))
+    return out[0], out[1]
 
 
 def trace_quad(fa, b, fc, d):

@@ -410,6 +410,13 @@ OR_API double or_trace_pair(void* p, void* q) {
     return trace_pair(static_cast<ORep*>(p)->p, static_cast<ORep*>(q)->p);
 }
 
+OR_API int or_hutchinson_trace(void* fp, void* bp, int n_samples, std::uint64_t seed, double* out2) {
+    return guard([&] {
+        const HutchinsonResult r = hutchinson_trace(static_cast<OFactor*>(fp)->f, static_cast<OHodlr*>(bp)->h, n_samples, seed);
+        out2[0] = r.estimate;
+        out2[1] = r.std_error;
+    });
+}
 OR_API int or_trace_solve(void* fp, void* bp, double* out) {
     return guard([&] { *out = trace_solve(static_cast<OFactor*>(fp)->f, static_cast<OHodlr*>(bp)->h); });
 }

@@ -424,6 +424,15 @@ hg_status hg_trace_solve(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, double* out)
     });
 }
 
+hg_status hg_hutchinson_trace(hg_ctx_t ctx, hg_factor_t f, hg_hodlr_t b, int n_samples, uint64_t seed,
+                              double* estimate, double* std_error) {
+    return guard(ctx, [&] {
+        const auto r = hutchinson_trace(f->f, b->h, n_samples, seed);
+        *estimate = r.first;
+        *std_error = r.second;
+    });
+}
+
 hg_status hg_trace_quad(hg_ctx_t ctx, hg_factor_t fa, hg_hodlr_t b, hg_factor_t fc, hg_hodlr_t d, double* out) {
     return guard(ctx, [&] {
         DProductRep p = pipeline(fa->f, b->h, true);

@@ -1,5 +1,7 @@
 // Statistics glue of one MLE iteration (mle.cpp:25-54) on the device.
+#include <algorithm>
 #include <cmath>
+#include <random>
 
 #include "api.cuh"
 
@@ -38,6 +40,34 @@ std::vector<double> score(const DFactor& f, const std::vector<const DHodlr*>& de
     std::vector<double> s(p);
     for (size_t j = 0; j < p; ++j) s[j] = -0.5 * h[2 * j] + 0.5 * h[2 * j + 1];
     return s;
+}
+
+std::pair<double, double> hutchinson_trace(const DFactor& f, const DHodlr& b, int n_samples, std::uint64_t seed) {
+    if (n_samples < 2) throw std::invalid_argument("hutchinson_trace: need >= 2 samples");
+    if (b.n() != f.n()) throw std::invalid_argument("hutchinson_trace: dimension mismatch");
+    const i64 n = f.n();
+    constexpr int CH = 64;
+    std::mt19937_64 rng(seed);
+    std::bernoulli_distribution coin(0.5);
+    DVec Z(static_cast<size_t>(n) * CH), X(static_cast<size_t>(n) * CH), d(CH);
+    std::vector<double> hz(static_cast<size_t>(n) * CH);
+    double sum = 0, sumsq = 0;
+    for (int s0 = 0; s0 < n_samples; s0 += CH) {
+        const int sc = std::min(CH, n_samples - s0);
+        for (int s = 0; s < sc; ++s)
+            for (i64 i = 0; i < n; ++i) hz[static_cast<size_t>(i + i64(s) * n)] = coin(rng) ? 1.0 : -1.0;
+        Z.upload(hz.data(), static_cast<size_t>(n) * CH);
+        hodlr_apply(b, Z.get(), n, sc, X.get(), n, 1, b.tau(), true, false, 0.0);
+        factor_solve(f, X.get(), n, sc);
+        for (int s = 0; s < sc; ++s) dot_panels(n, 1, Z.get() + i64(s) * n, n, X.get() + i64(s) * n, n, d.get() + s, false);
+        const std::vector<double> v = d.download();  // synchronises: hz may be refilled
+        for (int s = 0; s < sc; ++s) {
+            sum += v[static_cast<size_t>(s)];
+            sumsq += v[static_cast<size_t>(s)] * v[static_cast<size_t>(s)];
+        }
+    }
+    const double var = (sumsq - sum * sum / n_samples) / (n_samples - 1);
+    return {sum / n_samples, std::sqrt(std::max(var, 0.0) / n_samples)};
 }
 
 std::vector<double> fisher_from_reps(const std::vector<DProductRep>& reps) {

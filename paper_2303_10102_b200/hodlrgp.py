@@ -90,6 +90,7 @@ _SIGS = {
     "hg_trace_product_rep": (C.c_int, [vp, vp, dp]),
     "hg_trace_pair": (C.c_int, [vp, vp, vp, dp]),
     "hg_trace_solve": (C.c_int, [vp, vp, vp, dp]),
+    "hg_hutchinson_trace": (C.c_int, [vp, vp, vp, C.c_int, C.c_uint64, dp, dp]),
     "hg_trace_quad": (C.c_int, [vp, vp, vp, vp, vp, dp]),
     "hg_oracle_dense": (C.c_int, [vp, i64, dp, C.c_int, dp, C.POINTER(vp)]),
     "hg_oracle_matern": (C.c_int, [vp, i64, dp, C.c_int, dbl, dbl, dbl, C.c_int, C.POINTER(vp)]),
@@ -581,6 +582,13 @@ def trace_solve(f, b):
     out = C.c_double()
     _check(lib().hg_trace_solve(f.ctx.ptr, f.ptr, b.ptr, C.byref(out)))
     return out.value
+
+
+def hutchinson_trace(f, b, n_samples, seed):
+    """mle.cpp:56-75 -> (estimate, std_error) of tr(K^-1 B) from Rademacher probes."""
+    e, se = C.c_double(), C.c_double()
+    _check(lib().hg_hutchinson_trace(f.ctx.ptr, f.ptr, b.ptr, int(n_samples), int(seed), C.byref(e), C.byref(se)))
+    return e.value, se.value
 
 
 def trace_quad(fa, b, fc, d):

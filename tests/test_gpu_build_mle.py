@@ -287,6 +287,53 @@ def test_mle_glue_dense_family(H):  # test_mle.cpp:53-84 on the device
     assert fi[1, 1] == pytest.approx(0.5 * np.trace(m1 @ m1), rel=1e-9)
 
 
+def test_mle_nonzero_mean_and_score_fd(H):
+    """test_mle.cpp:107-118 (the likelihood subtracts a nonzero mean) and :86-105 (the
+    score is the finite-difference gradient of the likelihood) on the device."""
+    g = np.random.default_rng(2)
+
+    def rnd(n, shift):
+        m = g.standard_normal((n, n))
+        return m @ m.T / n + shift * np.eye(n)
+
+    n = 64
+    k0, d0, d1 = rnd(n, 4.0), rnd(n, 1.0), rnd(n, 1.0)
+
+    def kmat(t):
+        return k0 + t[0] * d0 + t[1] * d1
+
+    def dense_ll(t, r):
+        kk = kmat(t)
+        return -0.5 * n * np.log(2 * np.pi) - 0.5 * np.linalg.slogdet(kk)[1] - 0.5 * r @ np.linalg.solve(kk, r)
+
+    def dev_ll(t, y, mu=None):
+        f = H.factorize(dev(H, O.Hodlr.from_dense(2, kmat(t))), H.LEFT)
+        return H.log_likelihood(f, y, mu), f
+
+    y = O.randn(n, 1, 909)[:, 0]
+    mu = np.full(n, 0.37)
+    t = np.array([1.0, 1.0])
+    ll, f = dev_ll(t, y, mu)
+    assert ll == pytest.approx(dense_ll(t, y - mu), rel=1e-10)
+    der = [dev(H, O.Hodlr.from_dense(2, d0)), dev(H, O.Hodlr.from_dense(2, d1))]
+    s_mu = H.score(f, der, y, mu)
+    t = np.array([0.8, 1.2])
+    ll, f = dev_ll(t, y)
+    s = H.score(f, der, y)
+    eps = 1e-5
+    for j in range(2):
+        tp, tm = t.copy(), t.copy()
+        tp[j] += eps
+        tm[j] -= eps
+        fd = (dev_ll(tp, y)[0] - dev_ll(tm, y)[0]) / (2 * eps)
+        assert s[j] == pytest.approx(fd, rel=1e-6)
+    # the mean enters the score through the residual only
+    w = np.linalg.solve(kmat(np.array([1.0, 1.0])), y - mu)
+    kinv = np.linalg.inv(kmat(np.array([1.0, 1.0])))
+    for j, dj in enumerate((d0, d1)):
+        assert s_mu[j] == pytest.approx(-0.5 * np.trace(kinv @ dj) + 0.5 * w @ dj @ w, rel=1e-9)
+
+
 def test_build_long_deficient_blocks(H):
     """Long rank-deficient blocks (Matérn 3/2 blocks have exact rank 2 < k;
     level-1 children of 16384 rows) exercise the batched completion path.

@@ -448,6 +448,19 @@ def test_mle_glue_dense():  # test_mle.cpp:53-84
     assert np.array_equal(fi, fic)
 
 
+def test_hutchinson_trace():  # test_mle.cpp:119-133
+    ha, hb = O.Hodlr.random_spd(256, 3, 4, 5), O.Hodlr.random_spd(256, 3, 4, 6)
+    f = O.factorize(ha, O.Factor.LEFT)
+    exact = O.trace_solve(f, hb)
+    e, se = O.hutchinson_trace(f, hb, 400, 17)
+    assert se > 0.0 and abs(e - exact) <= 4.0 * se
+    e4, se4 = O.hutchinson_trace(f, hb, 1600, 17)
+    assert se4 <= 0.6 * se
+    assert O.hutchinson_trace(f, hb, 400, 17) == (e, se)
+    with pytest.raises(ValueError):
+        O.hutchinson_trace(f, hb, 1, 17)
+
+
 def test_mle_nonzero_mean():  # test_mle.cpp:107-118
     k0, d0, d1 = _family(64, 3)
     kk = k0 + d0 + d1

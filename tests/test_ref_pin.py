@@ -82,6 +82,14 @@ def test_fixtures_factor_and_traces_bitwise(n, tau, k, seed):
     assert np.array_equal(fr.solve(x), fo.solve(x))
 
 
+def test_hutchinson_trace_bitwise():  # mle.cpp:56-75 (same libstdc++ Rademacher stream, same solves)
+    ar, br = R.Hodlr.random_spd(256, 3, 4, 5), R.Hodlr.random_spd(256, 3, 4, 6)
+    ao, bo = O.Hodlr.random_spd(256, 3, 4, 5), O.Hodlr.random_spd(256, 3, 4, 6)
+    er, sr = R.hutchinson_trace(R.factorize(ar, 1), br, 400, 17)
+    eo, so = O.hutchinson_trace(O.factorize(ao, 1), bo, 400, 17)
+    assert er == eo and sr == pytest.approx(so, rel=1e-10)
+
+
 @pytest.mark.parametrize("scan", [False, True])
 def test_build_matches_reference(scan):
     n = 512
