@@ -1,4 +1,6 @@
 // Batched (column-pivoted) Householder QR and Q formation — see qr.cuh.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <cstdlib>
 
@@ -274,6 +276,18 @@ __global__ void __launch_bounds__(FQNT) k_form_q(const QfDesc* descs, int w, int
 }
 
 #include "qr_blocked.cuh"
+#include "qr_cluster.cuh"
+
+/// Cluster path (qr_cluster.cuh): few blocks (the clusters fit the chip at
+/// once), wide enough to be worth two cluster barriers per column, and a
+/// CTA's share of the columns fits shared memory. HG_QR_CLUSTER=0 disables.
+bool cluster_qr_fits(int nblocks, int max_rows, int w, int num_sms) {
+    static const bool on = [] {
+        const char* e = std::getenv("HG_QR_CLUSTER");
+        return !(e && e[0] == '0');
+    }();
+    return on && w >= 64 && w <= MAXW && nblocks * QC_CS <= num_sms && qc_smem(max_rows, w) <= QR_SMEM;
+}
 
 /// INPLACE instantiation only when some block does not fit shared memory
 /// (its register-held columns would cost the resident path occupancy).
@@ -317,6 +331,12 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_blocked),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
         k_qr_blocked<<<unsigned(blocks.size()), QB_THREADS, sb, c.stream>>>(dd.get(), w);
+    } else if (pivot && cluster_qr_fits(int(blocks.size()), max_rows, w, c.num_sms)) {
+        // a few wide blocks: one thread-block cluster per block, columns resident in DSMEM
+        const size_t sb = qc_smem(max_rows, w);
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_cluster),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
+        k_qr_cluster<<<unsigned(blocks.size()) * QC_CS, QC_THREADS, sb, c.stream>>>(dd.get(), w);
     } else if (pivot) {
         launch_qr<true>(dd.get(), int(blocks.size()), qnt, smem, w, smem_elems, smem_elems < max_rows * w);
     } else {

@@ -31,10 +31,15 @@ def _blocks():
     low = g.standard_normal((300, 5)) @ g.standard_normal((5, 24))  # numeric rank 5 -> completion
     tall = g.standard_normal((5000, 40)) * np.logspace(0, -6, 40)   # TSQR chunks, graded columns
     wide = g.standard_normal((2100, 64))                             # blocked-QR chunks
-    return [full, low, tall, wide]
+    # widths above 64, one block: the thread-block-cluster pivoted QR (qr_cluster.cuh), resident and
+    # as the root of a TSQR tree, graded columns and a numerically rank-deficient block
+    c96 = g.standard_normal((700, 96)) * np.logspace(0, -5, 96)
+    c128 = g.standard_normal((6000, 128)) * np.logspace(0, -4, 128)
+    clow = g.standard_normal((900, 7)) @ g.standard_normal((7, 80))
+    return [full, low, tall, wide, c96, c128, clow]
 
 
-@pytest.mark.parametrize("i", range(4))
+@pytest.mark.parametrize("i", range(7))
 def test_randomized_range_matches_oracle(H, i):
     y = _blocks()[i]
     k = y.shape[1]
