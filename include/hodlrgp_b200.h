@@ -71,12 +71,22 @@ void* hg_ctx_stream(hg_ctx_t ctx);
  *    (LowRankBlock::compressed at 1e-13). HG_COMPRESS_AT_LEVEL (default): as
  *    each level is committed, so finer levels peel against the compressed
  *    (rank ~3..8 instead of 2k + w2) panels. HG_COMPRESS_AT_END: after the
- *    last level, as sketch.cpp:331-341 (parity mode). */
-enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2, HG_OPT_Q2_BASIS = 3, HG_OPT_COMPRESS_AT = 4 };
+ *    last level, as sketch.cpp:331-341 (parity mode).
+ *  HG_OPT_SKETCH_RNG — where the SketchPlan's Gaussian samplers come from.
+ *    HG_SKETCH_RNG_REFERENCE (default): std::mt19937_64(seed) +
+ *    std::normal_distribution<double> on the host in the reference's fill
+ *    order (sketch.cpp:10-31), byte-identical to the reference's plan — a
+ *    sequential stream (seconds at n = 2^20: 2.7e8 draws). HG_SKETCH_RNG_DEVICE:
+ *    a counter-based generator on the device (a hash of (seed, level, row,
+ *    column) through Box-Muller), milliseconds; same sparsity pattern, not the
+ *    reference's bytes (no parity with a CPU run of the same seed). */
+enum { HG_OPT_PRODUCT_ASSOCIATION = 1, HG_OPT_COMPRESSION = 2, HG_OPT_Q2_BASIS = 3, HG_OPT_COMPRESS_AT = 4,
+       HG_OPT_SKETCH_RNG = 5 };
 enum { HG_ASSOC_SOLVE = 0, HG_ASSOC_REFERENCE = 1 };
 enum { HG_COMPRESS_PIVOTED_QR = 0, HG_COMPRESS_JACOBI_SVD = 1 };
 enum { HG_Q2_REORTHOGONALIZED = 0, HG_Q2_REFERENCE = 1 };
 enum { HG_COMPRESS_AT_LEVEL = 0, HG_COMPRESS_AT_END = 1 };
+enum { HG_SKETCH_RNG_REFERENCE = 0, HG_SKETCH_RNG_DEVICE = 1 };
 hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value);
 int hg_ctx_get_option(hg_ctx_t ctx, int option);
 

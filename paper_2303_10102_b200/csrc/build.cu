@@ -990,11 +990,43 @@ void randomized_range(const double* Y, i64 ldy, int rows, int k, double* Q, i64 
     HG_CUDA(cudaMemcpyAsync(nr, dnr.get(), sizeof(int), cudaMemcpyDeviceToDevice, ctx.stream));
 }
 
+namespace {
+
+__device__ __forceinline__ std::uint64_t plan_mix(std::uint64_t z) {  // splitmix64 finalizer
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/// HG_SKETCH_RNG_DEVICE: level sampler rows of odd (right-child) segments get
+/// N(0, 1) = Box-Muller of two hashes of (seed, level, row, column); rows of
+/// even segments are zero (the pattern of sketch.cpp:12-24).
+__global__ void k_plan_level_device(const WorkItem* items, int k, std::uint64_t key, double* P, i64 ldp) {
+    const WorkItem it = items[blockIdx.x];
+    if (int(threadIdx.x) >= it.rows) return;
+    const i64 row = i64(it.row0) + threadIdx.x;
+    double* p = P + row;
+    if (!(it.seg & 1)) {
+        for (int c = 0; c < k; ++c) p[i64(c) * ldp] = 0.0;
+        return;
+    }
+    for (int c = 0; c < k; ++c) {
+        const std::uint64_t h1 = plan_mix(key ^ (std::uint64_t(row) * 0x100000001B3ull + std::uint64_t(c)));
+        const std::uint64_t h2 = plan_mix(h1 ^ 0xD1B54A32D192ED03ull);
+        const double u1 = (double(h1 >> 11) + 1.0) * 0x1.0p-53, u2 = double(h2 >> 11) * 0x1.0p-53;
+        p[i64(c) * ldp] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+}
+
+}  // namespace
+
 DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
     static std::mutex mu;
-    static std::map<std::tuple<const DTree*, i64, std::uint64_t>, std::weak_ptr<const DSketchPlan>> cache;
+    static std::map<std::tuple<const DTree*, i64, std::uint64_t, int>, std::weak_ptr<const DSketchPlan>> cache;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(tree.get(), k, seed);
+    const int rng_mode = current().sketch_rng;
+    auto key = std::make_tuple(tree.get(), k, seed, rng_mode);
     auto it = cache.find(key);
     if (it != cache.end())
         if (auto sp = it->second.lock()) return sp;
@@ -1004,10 +1036,22 @@ DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
     plan->seed = seed;
     const ClusterTree& t = tree->host;
     const i64 n = t.size();
+    if (rng_mode == 1) {  // HG_SKETCH_RNG_DEVICE
+        for (int l = 1; l <= t.depth(); ++l) {
+            auto d = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(k), false);
+            const TileList& tl = tree->part(l).tiles(256);
+            k_plan_level_device<<<tl.count, 256, 0, current().stream>>>(
+                tl.items.get(), int(k), seed * 0x9E3779B97F4A7C15ull + std::uint64_t(l) * 0xD6E8FEB86659FD93ull,
+                d->get(), n);
+            HG_LAUNCH();
+            count_launch();
+            plan->level.push_back(d);
+        }
+    }
     std::mt19937_64 rng(seed);
     std::normal_distribution<double> gauss(0.0, 1.0);
-    std::vector<double> buf(static_cast<size_t>(n) * static_cast<size_t>(k));
-    for (int l = 1; l <= t.depth(); ++l) {
+    std::vector<double> buf(rng_mode == 1 ? 0 : static_cast<size_t>(n) * static_cast<size_t>(k));
+    for (int l = 1; rng_mode != 1 && l <= t.depth(); ++l) {
         std::fill(buf.begin(), buf.end(), 0.0);
         const auto& kids = t.level(l);
         for (size_t j = 0; j < t.level(l - 1).size(); ++j) {

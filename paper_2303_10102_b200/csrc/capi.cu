@@ -197,6 +197,8 @@ hg_status hg_ctx_set_option(hg_ctx_t ctx, int option, int value) {
             ctx->c.q2_basis = value;
         else if (option == HG_OPT_COMPRESS_AT && (value == HG_COMPRESS_AT_LEVEL || value == HG_COMPRESS_AT_END))
             ctx->c.compress_at = value;
+        else if (option == HG_OPT_SKETCH_RNG && (value == HG_SKETCH_RNG_REFERENCE || value == HG_SKETCH_RNG_DEVICE))
+            ctx->c.sketch_rng = value;
         else
             throw std::invalid_argument("hg_ctx_set_option: unknown option or value");
     });
@@ -208,6 +210,7 @@ int hg_ctx_get_option(hg_ctx_t ctx, int option) {
     if (option == HG_OPT_COMPRESSION) return ctx->c.compression;
     if (option == HG_OPT_Q2_BASIS) return ctx->c.q2_basis;
     if (option == HG_OPT_COMPRESS_AT) return ctx->c.compress_at;
+    if (option == HG_OPT_SKETCH_RNG) return ctx->c.sketch_rng;
     return -1;
 }
 

@@ -54,6 +54,7 @@ struct Ctx {
     int compression = 0;         // HG_OPT_COMPRESSION (HG_COMPRESS_*)
     int q2_basis = 0;            // HG_OPT_Q2_BASIS (HG_Q2_*)
     int compress_at = 0;         // HG_OPT_COMPRESS_AT (HG_COMPRESS_AT_*)
+    int sketch_rng = 0;          // HG_OPT_SKETCH_RNG (HG_SKETCH_RNG_*)
 };
 
 

@@ -325,7 +325,13 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     // short blocks: fewer threads per CTA (more CTAs per SM, cheaper barriers)
     // (the trailing update runs a warp per column: wide blocks keep 16 warps)
     const int qnt = max_rows <= 64 ? 128 : (max_rows <= 256 && w <= 48) ? 256 : QNT;
-    if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS) {
+    if (!pivot && w >= 128 && cluster_qr_fits(int(blocks.size()), max_rows, w, c.num_sms)) {
+        // a few wide blocks, unpivoted: the cluster kernel, one cluster barrier per column
+        const size_t sb = qc_smem(max_rows, w);
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_cluster<false>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
+        k_qr_cluster<false><<<unsigned(blocks.size()) * QC_CS, QC_THREADS, sb, c.stream>>>(dd.get(), w);
+    } else if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS) {
         // wide blocks that do not fit shared memory: blocked compact-WY QR
         const size_t sb = qb_smem(max_rows, w);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_blocked),
@@ -334,9 +340,9 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
     } else if (pivot && cluster_qr_fits(int(blocks.size()), max_rows, w, c.num_sms)) {
         // a few wide blocks: one thread-block cluster per block, columns resident in DSMEM
         const size_t sb = qc_smem(max_rows, w);
-        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_cluster),
+        HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_cluster<true>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
-        k_qr_cluster<<<unsigned(blocks.size()) * QC_CS, QC_THREADS, sb, c.stream>>>(dd.get(), w);
+        k_qr_cluster<true><<<unsigned(blocks.size()) * QC_CS, QC_THREADS, sb, c.stream>>>(dd.get(), w);
     } else if (pivot) {
         launch_qr<true>(dd.get(), int(blocks.size()), qnt, smem, w, smem_elems, smem_elems < max_rows * w);
     } else {

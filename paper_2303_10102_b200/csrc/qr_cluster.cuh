@@ -11,8 +11,9 @@
 // swaps). Per step: every CTA posts its best remaining column norm into all
 // peers' shared memory (DSMEM), barrier, the owner of the pivot column forms
 // the reflector and broadcasts it through DSMEM, barrier, every CTA updates
-// its own columns. Two cluster barriers per step instead of ~5 CTA barriers
-// over an L2-resident matrix.
+// its own columns. Two cluster barriers per step (one when unpivoted: the
+// reflector buffers alternate) instead of ~5 CTA barriers over an L2-resident
+// matrix.
 //
 // Same arithmetic as k_qr<true>: per column the same lane-strided dot product
 // and update, the same 512-thread tail norm, Eigen's pivot rule (largest
@@ -26,15 +27,16 @@ constexpr int QC_THREADS = QNT;  // 512: the tail-norm reduction order of k_qr
 struct QcShared {
     double cand_v[QC_CS];
     int cand_p[QC_CS];
-    double bc[4];  // beta, tau, zero flag (broadcast by the pivot column's owner)
+    double bc[2][4];  // per step parity: beta, tau, zero flag (broadcast by the pivot column's owner)
     int pos_of[MAXW], at_pos[MAXW];
 };
 
 __host__ __device__ inline size_t qc_smem(int rows, int w) {
     const int cpc = (w + QC_CS - 1) / QC_CS;
-    return sizeof(double) * (size_t(rows) * cpc + size_t(rows) + 2 * size_t(cpc));
+    return sizeof(double) * (size_t(rows) * cpc + 2 * size_t(rows) + 2 * size_t(cpc));
 }
 
+template <bool PIVOT>
 __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
     k_qr_cluster(const QrDesc* descs, int w) {
     namespace cg = cooperative_groups;
@@ -45,8 +47,8 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
     const QrDesc d = descs[blockIdx.x / QC_CS];
     const int rows = d.rows, cpc = (w + QC_CS - 1) / QC_CS;
     double* W = sm;                     // owned columns: local c <-> column c * QC_CS + rank
-    double* vb = W + size_t(rows) * cpc;  // current Householder vector (rows)
-    double* nu = vb + rows;             // updated / direct norms of the owned columns
+    double* vb2 = W + size_t(rows) * cpc;  // Householder vectors of even / odd steps (2 x rows)
+    double* nu = vb2 + 2 * size_t(rows);   // updated / direct norms of the owned columns
     double* nd = nu + cpc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int nown = rank < w ? (w - rank + QC_CS - 1) / QC_CS : 0;
@@ -54,21 +56,22 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
         for (int i = tid; i < rows; i += blockDim.x) W[i + size_t(c) * rows] = d.A[i + i64(c * QC_CS + rank) * d.lda];
     for (int j = tid; j < w; j += blockDim.x) sh.pos_of[j] = sh.at_pos[j] = j;
     __syncthreads();
-    for (int c = warp; c < nown; c += nwarps) {
-        double s = 0.0;
-        for (int i = lane; i < rows; i += 32) s += W[i + size_t(c) * rows] * W[i + size_t(c) * rows];
-        s = warp_sum(s);
-        if (lane == 0) nd[c] = nu[c] = sqrt(s);
-    }
+    if (PIVOT)
+        for (int c = warp; c < nown; c += nwarps) {
+            double s = 0.0;
+            for (int i = lane; i < rows; i += 32) s += W[i + size_t(c) * rows] * W[i + size_t(c) * rows];
+            s = warp_sum(s);
+            if (lane == 0) nd[c] = nu[c] = sqrt(s);
+        }
     cluster.sync();  // every CTA has read its columns of A (they are rewritten at the end) and is running
     const int nsz = min(rows, w);
     const double downdate_thr = sqrt(DBL_EPSILON);
     int steps = nsz;
     double beta0 = 0.0, stop_abs = -1.0;
-    if (d.stop.active && d.stop.abs_ptr) stop_abs = d.stop.abs_scale * *d.stop.abs_ptr;
+    if (PIVOT && d.stop.active && d.stop.abs_ptr) stop_abs = d.stop.abs_scale * *d.stop.abs_ptr;
     for (int k = 0; k < nsz; ++k) {
         // ---- pivot: best owned column among positions >= k, posted to every CTA
-        if (warp == 0) {
+        if (PIVOT && warp == 0) {
             double bv = -1.0;
             int bp = 1 << 30;
             for (int c = lane; c < nown; c += 32) {
@@ -93,16 +96,21 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
                 peer->cand_p[rank] = bp;
             }
         }
-        cluster.sync();
-        double bv = -1.0;
         int best = k;
+        if (PIVOT) {
+            cluster.sync();
+            double bv = -1.0;
 #pragma unroll
-        for (int r = 0; r < QC_CS; ++r)
-            if (sh.cand_v[r] > bv || (sh.cand_v[r] == bv && sh.cand_p[r] < best)) {
-                bv = sh.cand_v[r];
-                best = sh.cand_p[r];
-            }
-        __syncthreads();  // everyone has read the map before it changes
+            for (int r = 0; r < QC_CS; ++r)
+                if (sh.cand_v[r] > bv || (sh.cand_v[r] == bv && sh.cand_p[r] < best)) {
+                    bv = sh.cand_v[r];
+                    best = sh.cand_p[r];
+                }
+            __syncthreads();  // everyone has read the map before it changes
+        }
+        // (vb and bc alternate between two buffers: step k's owner may write while peers
+        // still read step k-1's; everyone passed step k-1's barrier after finishing step k-2)
+        double* vb = vb2 + size_t(k & 1) * rows;
         if (tid == 0 && best != k) {  // positions k and best trade columns (identically in every CTA)
             const int ck = sh.at_pos[k], cb = sh.at_pos[best];
             sh.at_pos[k] = cb;
@@ -139,14 +147,14 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
             }
             if (tid < QC_CS) {
                 QcShared* peer = cluster.map_shared_rank(&sh, tid);
-                peer->bc[0] = beta;
-                peer->bc[1] = tau;
-                peer->bc[2] = zero ? 1.0 : 0.0;
+                peer->bc[k & 1][0] = beta;
+                peer->bc[k & 1][1] = tau;
+                peer->bc[k & 1][2] = zero ? 1.0 : 0.0;
             }
         }
         cluster.sync();
-        const double beta = sh.bc[0], tau = sh.bc[1];
-        if (d.stop.active) {  // uniform over the cluster: every CTA holds the same beta
+        const double beta = sh.bc[k & 1][0], tau = sh.bc[k & 1][1];
+        if (PIVOT && d.stop.active) {  // uniform over the cluster: every CTA holds the same beta
             if (k == 0) beta0 = fabs(beta);
             if (fabs(beta) <= fmax(d.stop.rel * beta0, stop_abs) || k + 1 >= d.stop.max_steps) {
                 if (rank == 0)
@@ -170,6 +178,7 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
                 if (lane == 0) cj[k] -= tau * t;
             }
             __syncwarp();
+            if (!PIVOT) continue;
             int recompute = 0;
             if (lane == 0 && nu[c] != 0.0) {
                 double temp = fabs(cj[k]) / nu[c];
@@ -201,7 +210,7 @@ __global__ void __cluster_dims__(QC_CS, 1, 1) __launch_bounds__(QC_THREADS)
         if (d.R)
             for (int i = tid; i < w; i += blockDim.x) d.R[i + i64(p) * d.ldr] = (i <= p && i < nsz) ? col[i] : 0.0;
     }
-    if (rank == 0)
+    if (PIVOT && rank == 0)
         for (int p = tid; p < w; p += blockDim.x) d.perm[p] = sh.at_pos[p];
     (void)steps;
     cluster.sync();  // no CTA leaves while a peer may still write into its shared memory

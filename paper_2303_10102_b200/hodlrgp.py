@@ -38,7 +38,8 @@ lp = C.POINTER(C.c_int64)
 HOST, DEVICE = 0, 1
 RIGHT, LEFT = 0, 1
 # Context options (include/hodlrgp_b200.h)
-OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION, OPT_Q2_BASIS, OPT_COMPRESS_AT = 1, 2, 3, 4
+OPT_PRODUCT_ASSOCIATION, OPT_COMPRESSION, OPT_Q2_BASIS, OPT_COMPRESS_AT, OPT_SKETCH_RNG = 1, 2, 3, 4, 5
+SKETCH_RNG_REFERENCE, SKETCH_RNG_DEVICE = 0, 1
 Q2_REORTHOGONALIZED, Q2_REFERENCE = 0, 1
 COMPRESS_AT_LEVEL, COMPRESS_AT_END = 0, 1
 ASSOC_SOLVE, ASSOC_REFERENCE = 0, 1

@@ -25,6 +25,44 @@ def test_sketch_sampler_bit_exact(H, n, tau, k, seed):
         assert np.array_equal(a, b), level
 
 
+def test_device_sketch_rng(H):
+    """HG_OPT_SKETCH_RNG = HG_SKETCH_RNG_DEVICE: counter-based Gaussian samplers generated on
+    the device with the reference's sparsity pattern (sketch.cpp:12-24: N(0,1) on right-child
+    rows, zero on left-child rows); not the reference's bytes. The build stays exact."""
+    n, tau, k = 4096, 4, 24
+    ctx = H.context()
+    ctx.set_option(H.OPT_SKETCH_RNG, H.SKETCH_RNG_DEVICE)
+    try:
+        tree = H.ClusterTree(n, tau)
+        for level in (1, 3, tau):
+            a = H.sketch_sampler(n, tau, k, 5, level)
+            assert np.array_equal(a, H.sketch_sampler(n, tau, k, 5, level))       # deterministic
+            assert not np.array_equal(a, H.sketch_sampler(n, tau, k, 6, level))  # seeded
+            assert not np.array_equal(a, O.sketch_sampler(n, tau, k, 5, level))  # not the host stream
+            right = np.zeros(n, bool)
+            for j, (lo, hi) in enumerate(tree.level(level)):
+                right[lo:hi] = j & 1
+            assert np.all(a[~right] == 0.0)
+            g = a[right]
+            assert abs(g.mean()) < 0.02 and abs(g.std() - 1.0) < 0.02 and abs((g ** 4).mean() - 3.0) < 0.2
+            # neighbouring rows / columns uncorrelated (>= 2047 x 23 pairs: sigma <= 0.005)
+            assert abs(np.corrcoef(g[:-1].ravel(), g[1:].ravel())[0, 1]) < 0.025
+            assert abs(np.corrcoef(g[:, :-1].ravel(), g[:, 1:].ravel())[0, 1]) < 0.025
+        assert np.array_equal(H.sketch_sampler(n, tau, k, 5, 0), O.sketch_sampler(n, tau, k, 5, 0))  # identity stacks
+        x = np.sort(np.random.default_rng(0).uniform(size=n))
+        o = H.MaternOracle(x, 3, 1.0, 0.2, 1e-4, False)
+        K = o.apply(np.eye(n))
+        br = H.build_hodlr_with_derivatives(o, tree, k, 5)
+        assert np.linalg.norm(br.h.densify() - K) <= 1e-9 * np.linalg.norm(K)
+        y = np.linalg.cholesky(K) @ O.randn(n, 1, 1)[:, 0]
+        ll1, s1, f1, _ = H.mle_iteration(o, tau, k, 5, y)
+    finally:
+        ctx.set_option(H.OPT_SKETCH_RNG, H.SKETCH_RNG_REFERENCE)
+    ll0, s0, f0, _ = H.mle_iteration(o, tau, k, 5, y)
+    assert ll1 == pytest.approx(ll0, rel=1e-8)
+    assert np.allclose(s1, s0, rtol=1e-5, atol=1e-6 * np.abs(s0).max()) and np.allclose(f1, f0, rtol=1e-5)
+
+
 def _blocks():
     g = np.random.default_rng(11)
     full = g.standard_normal((300, 24))
