@@ -1019,6 +1019,19 @@ __global__ void k_plan_level_device(const WorkItem* items, int k, std::uint64_t 
     }
 }
 
+/// Reference stream: `stage` holds a level's draws in draw order (per node the
+/// right child's rows x k block, row-major: sketch.cpp:12-24 fills row by row);
+/// scatter them into the column-major level sampler, zeros on left-child rows.
+__global__ void k_plan_level_scatter(const WorkItem* items, const int* bounds, int k, const double* stage,
+                                     const i64* base, double* P, i64 ldp) {
+    const WorkItem it = items[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const bool right = it.seg & 1;
+    const double* src = right ? stage + base[it.seg >> 1] + i64(it.row0 - bounds[it.seg]) * k : nullptr;
+    for (int r = warp; r < it.rows; r += nwarps)  // a warp reads one row's k contiguous draws
+        for (int c = lane; c < k; c += 32) P[i64(it.row0 + r) + i64(c) * ldp] = right ? src[i64(r) * k + c] : 0.0;
+}
+
 }  // namespace
 
 DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
@@ -1050,18 +1063,32 @@ DSketchPlanP get_plan(DTreeP tree, i64 k, std::uint64_t seed) {
     }
     std::mt19937_64 rng(seed);
     std::normal_distribution<double> gauss(0.0, 1.0);
+    // The stream is sequential (2.7e8 draws at C4): draws land contiguously in draw order
+    // (a strided column-major fill cost more than the generator) and are scattered on the device.
     std::vector<double> buf(rng_mode == 1 ? 0 : static_cast<size_t>(n) * static_cast<size_t>(k));
+    DVec stage(buf.size());
+    DBuf<i64> dbase;
     for (int l = 1; rng_mode != 1 && l <= t.depth(); ++l) {
-        std::fill(buf.begin(), buf.end(), 0.0);
         const auto& kids = t.level(l);
+        std::vector<i64> base(t.level(l - 1).size());
+        size_t pos = 0;
         for (size_t j = 0; j < t.level(l - 1).size(); ++j) {
             const Range cr = kids[2 * j + 1];
-            for (i64 i = cr.lo; i < cr.hi; ++i)
-                for (i64 c = 0; c < k; ++c) buf[static_cast<size_t>(i + c * n)] = gauss(rng);
+            base[j] = i64(pos);
+            const size_t cnt = static_cast<size_t>(cr.size()) * static_cast<size_t>(k);
+            for (size_t e = 0; e < cnt; ++e) buf[pos + e] = gauss(rng);
+            pos += cnt;
         }
-        auto d = make_dvec(buf.size(), false);
-        d->upload(buf);
-        sync();  // the host buffer is reused for the next level
+        auto d = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(k), false);
+        HG_CUDA(cudaMemcpyAsync(stage.get(), buf.data(), pos * sizeof(double), cudaMemcpyHostToDevice, current().stream));
+        dbase.upload(base);
+        const Partition& pl = tree->part(l);
+        const TileList& tl = pl.tiles(256);
+        k_plan_level_scatter<<<tl.count, 256, 0, current().stream>>>(tl.items.get(), pl.dbounds(), int(k), stage.get(),
+                                                                      dbase.get(), d->get(), n);
+        HG_LAUNCH();
+        count_launch();
+        sync();  // the host buffers are reused for the next level
         plan->level.push_back(d);
     }
     plan->leaf = make_dvec(static_cast<size_t>(n) * static_cast<size_t>(tree->bmax), true);
