@@ -796,7 +796,7 @@ void hs_apply(const DHStrong& h, const double* X, i64 ldx, int s, double* Y, i64
         P.alloc(static_cast<size_t>(nslots) * k * s);
         {
             ProfScope prof(PROF_MATVEC, 2.0 * double(h.U.size() + h.V.size()) * s, 8.0 * double(h.U.size() + h.V.size()));
-            if (tc)
+            if (tc || k <= 96)  // narrow blocks too: the DMMA tile streams the panels at ~5.5 TB/s (the FMA kernel: 1.3)
                 proj_tc(h.proj.get(), int(h.proj.size()), X, ldx, k, s, partials.get());
             else
                 k_hs_proj<<<dim3(unsigned(h.proj.size()), cy), 256, 0, c.stream>>>(h.proj.get(), X, ldx, k, s,

@@ -54,6 +54,7 @@ def run(name, power_iters=0):
     order, tree = H.grid_kd_order(N, leaf)
     o = H.Spde2dOracle(N, 1.0, ell, 4.0, order=order, nugget=nug)
     plan = H.hstrong_plan(order, N, tree.tau, 1.0, k)
+    H.HStrongMatrix(o, order, N, tree.tau, k, 1.0, -1, power_iters, 7)  # warm-up (allocator, module load)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     hs = H.HStrongMatrix(o, order, N, tree.tau, k, 1.0, -1, power_iters, 7)
