@@ -702,7 +702,7 @@ def CoKrigingOracle(m, sigma2, ell, kappa, nugget=1e-6, ctx=None):
 # (the reference's only format) at BASELINE's ranks approximates the 2D SPDE
 # covariance to ~7e-4 relative in operator norm (C3, k = 42), i.e. ~30 Var(u)
 # in absolute terms: below ~10 Var(u) of nugget the built HODLR is not
-# positive definite (scripts/probe_spde_nugget.py). Strong admissibility is
+# positive definite (tests/diagnostics/probe_spde_nugget.py). Strong admissibility is
 # the fix (no parity oracle).
 SPDE_NUGGET_REL = 10.0
 

@@ -2,7 +2,7 @@
 device) in each product association, against the unmodified restated oracle,
 the oracle in the solve association, and the reference itself (oracle/_ref).
 Also the spread of the oracle itself across thread counts (summation order).
-Usage: python scripts/probe_glue_modes.py
+Usage: python tests/diagnostics/probe_glue_modes.py
 """
 import ctypes as C
 import sys

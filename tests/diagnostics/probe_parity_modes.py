@@ -1,7 +1,7 @@
 """Parity modes on config C1 (n = 4096) and its n = 512 cut: the device path in
 each (association, compression) mode against the reference itself (oracle/_ref),
 the restated oracle in both associations, and the dense truth.
-Usage: python scripts/probe_parity_modes.py [n]
+Usage: python tests/diagnostics/probe_parity_modes.py [n]
 """
 import sys
 

@@ -191,7 +191,7 @@ def test_mle_glue_c1_identical_inputs(H):
     """mle.cpp:25-54 on identical H, dK/dtheta_j (oracle-built, imported).
 
     C1's covariance has condition ~1.6e7. Measured against the dense truth
-    (scripts/diag_fisher.py): device Fisher 7e-9, oracle with the device's
+    (tests/diagnostics/diag_fisher.py): device Fisher 7e-9, oracle with the device's
     product association (oracle.hpp set_solve_association) 4e-8, oracle with
     the reference's association 2e-5 — the reference's own rounding, from
     forming p = -(cap^-1 v^T)^T with ||cap^-1|| large, dominates. Stated
