@@ -108,3 +108,40 @@ def test_diff_qr_matches_oracle(H):
     r2 = r.copy()
     r2[-1, -1] = 1e-13 * r2[0, 0]
     assert H.diff_qr(db, q, r2)[3] and O.diff_qr(db, q, r2)[3]
+
+
+def test_cluster_qr_bitwise_equals_single_cta(H, tmp_path):
+    """The thread-block-cluster pivoted QR (qr_cluster.cuh) performs the same operations in the
+    same order as the one-CTA kernel: with HG_QR_CLUSTER=0 (read once per process, hence the
+    subprocess) the range finder returns bitwise the same q, r, pivots and numeric rank
+    whenever only the pivoted kernel is swapped."""
+    import os
+    import subprocess
+    import sys
+
+    mats = {f"m{i}": y for i, y in enumerate(_blocks()[4:])}
+    g = np.random.default_rng(3)
+    mats["m3"] = g.standard_normal((400, 128)) * np.logspace(0, -9, 128)
+    mats["m4"] = g.standard_normal((180, 100))
+    np.savez(tmp_path / "in.npz", **mats)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.')\n"
+        "from paper_2303_10102_b200 import hodlrgp as H\n"
+        f"d = np.load(r'{tmp_path / 'in.npz'}'); out = {{}}\n"
+        "for k in d.files:\n"
+        "    q, r, p, nr = H.randomized_range(d[k], d[k].shape[1])\n"
+        "    out[k + '_q'], out[k + '_r'], out[k + '_p'], out[k + '_n'] = q, r, p, np.array(nr)\n"
+        f"np.savez(r'{tmp_path / 'out.npz'}', **out)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, HG_QR_CLUSTER="0"))
+    ref = np.load(tmp_path / "out.npz")
+    for k, y in mats.items():
+        q, r, p, nr = H.randomized_range(y, y.shape[1])
+        assert nr == int(ref[k + "_n"]) and np.array_equal(p[:nr], ref[k + "_p"][:nr]), k
+        if y.shape[1] < 128 or y.shape[0] <= 4 * y.shape[1]:
+            assert np.array_equal(r, ref[k + "_r"]) and np.array_equal(q, ref[k + "_q"]), k
+        else:
+            # TSQR chunks of >= 128 columns: the unpivoted cluster kernel replaces the blocked
+            # compact-WY kernel (same reflectors in exact arithmetic, another summation order)
+            assert np.linalg.norm(r - ref[k + "_r"]) <= 1e-12 * np.linalg.norm(r), k
+            assert np.linalg.norm(q[:, :nr] - ref[k + "_q"][:, :nr]) <= 1e-10 * np.sqrt(nr), k
