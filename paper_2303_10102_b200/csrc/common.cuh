@@ -33,6 +33,7 @@ struct CudaError : std::runtime_error {
 #define HG_CUDA(x)                                                                              \
     do {                                                                                        \
         cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) (void)cudaGetLastError(); /* do not leave it for a later check */ \
         if (e_ != cudaSuccess)                                                                  \
             throw ::hg::CudaError(std::string(#x) + " failed: " + cudaGetErrorString(e_) +     \
                                   " at " __FILE__ ":" + std::to_string(__LINE__));              \

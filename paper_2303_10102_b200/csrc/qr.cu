@@ -331,7 +331,8 @@ void batched_qr(const std::vector<QrDesc>& blocks, int w, bool pivot) {
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_cluster<false>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
         k_qr_cluster<false><<<unsigned(blocks.size()) * QC_CS, QC_THREADS, sb, c.stream>>>(dd.get(), w);
-    } else if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS) {
+    } else if (!pivot && (smem_elems < max_rows * w || w >= 32) && max_rows <= QB_MAXROWS &&
+               qb_smem(max_rows, w) <= QB_SMEM_MAX) {
         // wide blocks that do not fit shared memory: blocked compact-WY QR
         const size_t sb = qb_smem(max_rows, w);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_qr_blocked),
@@ -367,7 +368,8 @@ void batched_form_q(const std::vector<QfDesc>& blocks, int w, int qcols) {
     for (const auto& b : blocks) rows += b.rows;
     ProfScope prof(PROF_FORM_Q, 4.0 * rows * w * qcols, 8.0 * rows * (w + 2.0 * qcols));
     if (prof_enabled()) prof.key(prof_tag("formq w=%d q=%d blocks=%d rows=%d", w, qcols, int(blocks.size()), max_rows));
-    if ((smem_elems < max_rows * qcols || qcols >= 16) && max_rows <= QB_MAXROWS) {
+    if ((smem_elems < max_rows * qcols || qcols >= 16) && max_rows <= QB_MAXROWS &&
+        qb_smem(max_rows, qcols) <= QB_SMEM_MAX) {
         const size_t sb = qb_smem(max_rows, qcols);
         HG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_form_q_blocked),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
@@ -398,7 +400,11 @@ int chunk_rows(int w) {
     }();
     int fit = int(std::min(budget, QR_SMEM) / (sizeof(double) * static_cast<size_t>(std::max(w, 1))));
     fit = (fit / 32) * 32;
-    return std::max(fit, 4 * w);
+    int rows = std::max(fit, 4 * w);
+    // very wide panels (w > ~250: derivative blocks at k > 80): shorter chunks, down to 2w rows,
+    // keep the blocked kernels' shared-memory budget (a taller TSQR tree instead of the in-place path)
+    while (rows - 32 >= 2 * w && (rows > QB_MAXROWS || qb_smem(rows, w) > QB_SMEM_MAX)) rows -= 32;
+    return rows;
 }
 }  // namespace
 

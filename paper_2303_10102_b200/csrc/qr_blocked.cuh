@@ -18,6 +18,7 @@
 constexpr int QB_NB = 16;
 constexpr int QB_THREADS = 256;
 constexpr int QB_MAXROWS = 1400;  // panel (rows x 16) in shared memory
+constexpr size_t QB_SMEM_MAX = 220 * 1024;  // panel + the two 16 x w work panels must fit one CTA
 
 __host__ __device__ __forceinline__ int qb_ld(int rows) { return ((rows + 11) / 16) * 16 + 4; }  // 4 mod 16
 __host__ __device__ __forceinline__ size_t qb_smem(int rows, int wmax) {
