@@ -96,3 +96,25 @@ def test_strong_c3_full_size_against_fft(H):
     weak = np.linalg.norm(H.build_hodlr(o, tree, k, 7).matvec(V) - KV) / np.linalg.norm(KV)
     assert err <= 1e-6, err
     assert err <= 1e-2 * weak, (err, weak)
+
+
+def test_strong_traces_c3_full_size_against_spectrum(H):
+    """tr(A B) of the strong-format K, dK/dtheta_j at C3's full size against the exact value: both
+    are diagonal in the 2D DFT, so tr(A B) = sum of the products of their multipliers
+    (oracle/models.spde2d_spectra). The H-matrix traces carry the compression error of both factors."""
+    from oracle import models as M
+
+    N, k = 256, 42
+    th = (1.0, 0.05, 4.0)
+    order, tree = H.grid_kd_order(N, 256)
+    var = H.spde2d_variance(N, *th)
+    nug = 1e-8 * var
+    o = H.Spde2dOracle(N, *th, order=order, nugget=nug)
+    lam = M.spde2d_spectra(N, *th, nug)
+    mats = [H.HStrongMatrix(o, order, N, tree.tau, k, param=j) for j in (-1, 0, 1, 2)]
+    for a in range(4):
+        for b in range(a, 4):
+            exact = float((lam[a] * lam[b]).sum())
+            scale = float(np.sqrt((lam[a] ** 2).sum() * (lam[b] ** 2).sum()))
+            t = mats[a].trace_product(mats[b])
+            assert abs(t - exact) <= 1e-9 * scale, (a, b, t, exact)
