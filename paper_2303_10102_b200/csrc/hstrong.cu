@@ -3,6 +3,7 @@
 #include <array>
 #include <tuple>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "hstrong.cuh"
@@ -194,6 +195,70 @@ __global__ void __launch_bounds__(EG_THREADS) k_hs_egemm(const EgItem* items, Gr
             if (col < k) it.Y[i64(row) + i64(col) * it.ldy] = acc[r][c];
         }
     }
+}
+
+/// The same product on the FP64 tensor cores: a 64 x TBN tile per CTA (4
+/// warps, tile.cuh), K = the block's columns in slices of 16. The A slice
+/// (64 rows x 16 generated entries) is produced one slice ahead: the gathers
+/// from the generating column are issued before the current slice's DMMA work
+/// and stored to the other shared buffer after it; X slices arrive by
+/// cp.async. (The FMA kernel above is bound by shared-memory bandwidth:
+/// 11 loads per 24 FMAs; a DMMA fragment feeds 16x more FMAs per load.)
+template <int TBN>
+__global__ void __launch_bounds__(tile::THREADS) k_hs_egemm_tc(const EgItem* items, GridEntries E, int k) {
+    constexpr int TBM = 64, BK = tile::BK, AE = tile::stage_elems(TBM), BE = tile::stage_elems(TBN);
+    constexpr int LDA = TBM + 4;  // MC layout: element (m, kk) at [kk * LDA + m]
+    constexpr int EPT = TBM * BK / tile::THREADS;  // generated entries per thread and slice (8)
+    __shared__ double As[2][AE];
+    __shared__ double Xs[2][BE];
+    const EgItem it = items[blockIdx.x];
+    const int tid = threadIdx.x, m = tid % TBM, kk0 = tid / TBM;  // this thread's row, first slice column
+    const bool rvalid = it.row0 + m < it.r_m;
+    const int gi = it.r_lo + it.row0 + (rvalid ? m : 0);
+    const int rx = __ldg(E.gx + gi), ry = __ldg(E.gy + gi);
+    const int ktiles = (it.c_m + BK - 1) / BK;
+    double ent[EPT];
+    auto gen = [&](int kt) {
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int j = kt * BK + kk0 + (tile::THREADS / TBM) * q;
+            double v = 0.0;
+            if (rvalid && j < it.c_m) {
+                const int col = it.c_lo + j;
+                v = grid_entry(E, rx, ry, __ldg(E.gx + col), __ldg(E.gy + col));
+            }
+            ent[q] = v;
+        }
+    };
+    auto put = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) As[buf][(kk0 + (tile::THREADS / TBM) * q) * LDA + m] = ent[q];
+    };
+    tile::LoadKCT<TBN> lx{it.X, it.ldx, it.c_m, k};
+    typename tile::Shape<TBM, TBN>::Acc acc;
+    acc.zero();
+    gen(0);
+    lx.issue(Xs[0], 0);
+    tile::cp_commit();
+    put(0);
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < ktiles) {
+            lx.issue(Xs[buf ^ 1], kt + 1);  // the other buffers were last read in slice kt - 1 (barrier below)
+            gen(kt + 1);                    // gathers in flight during this slice's DMMA work
+        }
+        tile::cp_commit();
+        tile::cp_wait<1>();
+        __syncthreads();  // slice kt: X landed, A stored by every thread
+        tile::mma_stage<false, true, TBM, TBN>(As[buf], Xs[buf], acc);
+        if (kt + 1 < ktiles) put(buf ^ 1);
+        __syncthreads();  // every warp is done with slice kt's buffers; slice kt + 1's A is stored
+    }
+    tile::cp_wait<0>();
+    tile::for_each_t<TBM, TBN>(acc, [&](int mi, int ci, double v) {
+        const int row = it.row0 + mi;
+        if (row < it.r_m && ci < k) it.Y[i64(row) + i64(ci) * it.ldy] = v;
+    });
 }
 
 struct DnItem {
@@ -537,9 +602,13 @@ int blocks_for(i64 tot) { return int(std::max<i64>(1, std::min<i64>((tot + 255) 
 void egemm(const std::vector<EgItem>& blocks, const GridEntries& E, int k, double flops_per_entry) {
     if (blocks.empty()) return;
     auto& c = current();
+    static const bool use_tc = [] {  // HG_HS_EGEMM_TC=0: the FMA kernel
+        const char* e = std::getenv("HG_HS_EGEMM_TC");
+        return !(e && e[0] == '0');
+    }();
     int minrows = 1 << 30;
     for (const auto& b : blocks) minrows = std::min(minrows, b.r_m);
-    const int TR = minrows >= 128 ? 128 : 64;
+    const int TR = (!use_tc && minrows >= 128) ? 128 : 64;
     std::vector<EgItem> items;
     double entries = 0.0;
     for (const auto& b : blocks) {
@@ -556,6 +625,17 @@ void egemm(const std::vector<EgItem>& blocks, const GridEntries& E, int k, doubl
     ProfScope prof(PROF_ORACLE, 2.0 * entries * k * flops_per_entry, 8.0 * entries / TR * KC);
     if (prof_enabled()) prof.key(prof_tag("hs_egemm k=%d items=%d", k, int(items.size())));
     const unsigned g = unsigned(items.size());
+    if (use_tc) {
+        if (k <= 32)
+            k_hs_egemm_tc<32><<<g, tile::THREADS, 0, c.stream>>>(d.get(), E, k);
+        else if (k <= 48)
+            k_hs_egemm_tc<48><<<g, tile::THREADS, 0, c.stream>>>(d.get(), E, k);
+        else
+            k_hs_egemm_tc<64><<<g, tile::THREADS, 0, c.stream>>>(d.get(), E, k);
+        HG_LAUNCH();
+        ++c.launches;
+        return;
+    }
     // inner slice KS: 32 columns, 16 where 32 would exceed 48 KB of static shared memory
     if (TR == 128 && KC == 48) k_hs_egemm<128, 48, 32><<<g, EG_THREADS, 0, c.stream>>>(d.get(), E, k);
     else if (TR == 128) k_hs_egemm<128, 64, 16><<<g, EG_THREADS, 0, c.stream>>>(d.get(), E, k);
